@@ -1,0 +1,279 @@
+/*
+ * shapflow_b200 — C-ABI of the B200-native DistShap explanation hot path
+ * (coalition sampler -> masked GCN inference -> weighted least squares).
+ *
+ * Plain pointers and sizes only. Every entry point returns an int status
+ * that maps onto the reference's exception types (error.hpp:10-27):
+ *   SF_OK 0, SF_ERR_INTERNAL 1 (CUDA / allocation), SF_ERR_DATA 2
+ *   (DataError), SF_ERR_NUMERICAL 3 (NumericalError), SF_ERR_PROTOCOL 4
+ *   (ProtocolError). sf_last_error() returns the thread-local message.
+ * The C++ drop-in (include/shapflow_b200.hpp) rethrows the matching type.
+ *
+ * Each declaration cites the reference interface it replaces
+ * (paths relative to /root/reference/proj/core).
+ */
+#ifndef SHAPFLOW_B200_H
+#define SHAPFLOW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SF_OK = 0,
+  SF_ERR_INTERNAL = 1,
+  SF_ERR_DATA = 2,
+  SF_ERR_NUMERICAL = 3,
+  SF_ERR_PROTOCOL = 4
+};
+
+typedef struct sf_ctx sf_ctx;           /* one rank = one GPU + stream + comm */
+typedef struct sf_graph sf_graph;       /* graph.hpp:16-31  Graph */
+typedef struct sf_model sf_model;       /* gcn.hpp:13-30    GcnModel */
+typedef struct sf_subgraph sf_subgraph; /* graph.hpp:36-53  ComputationalGraph */
+
+const char* sf_last_error(void);
+const char* sf_version(void);
+
+/* ------------------------------------------------------------ context
+ * A context owns one CUDA device, one stream and (optionally) one NCCL
+ * communicator; it replaces the reference's per-rank Communicator
+ * (comm.hpp:28-52) for the hot path. */
+int sf_ctx_create(int device, sf_ctx** out);
+int sf_ctx_destroy(sf_ctx* ctx);
+int sf_ctx_rank(const sf_ctx* ctx);
+int sf_ctx_world(const sf_ctx* ctx);
+/* NCCL over NVLink: 128-byte ncclUniqueId from rank 0, shared by the caller
+ * (e.g. through torch.distributed), then every rank joins. */
+int sf_nccl_unique_id(void* out_128_bytes);
+int sf_ctx_join_nccl(sf_ctx* ctx, const void* unique_id_128, int rank,
+                     int world);
+/* CollectiveStats (comm.hpp:13-19) */
+int sf_ctx_stats(const sf_ctx* ctx, uint64_t* scalar_allreduce,
+                 uint64_t* vector_allreduce, uint64_t* barriers,
+                 uint64_t* doubles_reduced);
+int sf_ctx_barrier(sf_ctx* ctx); /* Communicator::barrier (comm.hpp:37) */
+/* kernel launches issued by this context so far (for bench accounting) */
+uint64_t sf_ctx_launches(const sf_ctx* ctx);
+/* host<->device bytes copied by this context so far */
+int sf_ctx_io_bytes(const sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
+/* CUDA-event timers on the context stream (slots 0..7) */
+int sf_ctx_event_record(sf_ctx* ctx, int slot);
+int sf_ctx_event_elapsed(sf_ctx* ctx, int from_slot, int to_slot, float* ms);
+int sf_ctx_synchronize(sf_ctx* ctx);
+/* Per-launch timing of the dominant kernel (layer-0 masked SpMM): enable,
+ * run work, then read the summed duration (ms), launch count and the
+ * complement pairs those launches covered. */
+int sf_ctx_time_dominant(sf_ctx* ctx, int enable);
+int sf_ctx_dominant_stats(sf_ctx* ctx, double* total_ms, uint64_t* launches,
+                          uint64_t* pairs);
+/* Algorithmic bytes of the masked SpMM per complement pair for a
+ * (subgraph, model): (sum_{u in R} deg(u) + 2|R|) d 4
+ * gathered + 2|R| d 4 written + 2 W 8 mask, R = rows layer 0 produces. */
+int sf_spmm_bytes_per_pair(const sf_model* m, const sf_subgraph* sg,
+                           double* bytes, double* flops);
+
+/* ------------------------------------------------------------ primitives */
+/* explain.cpp:37-40 */
+uint64_t sf_node_sampling_seed(uint64_t seed, uint32_t node);
+/* explain.cpp:33-35 */
+uint64_t sf_auto_samples(uint64_t num_players);
+/* sampler.cpp:67-77 */
+uint64_t sf_binomial_or_max(uint32_t n, uint32_t s);
+/* sampler.cpp:79-91 */
+int sf_kernel_weight(uint32_t n, uint32_t s, double* out);
+/* Philox-4x32-10 stream (philox.hpp:13-73) generated ON THE DEVICE; used to
+ * pin the device generator bit-for-bit. */
+int sf_philox_u64(sf_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t count,
+                  uint64_t* out_host);
+
+/* sampler.hpp:49-50 plan_sizes. Arrays of capacity `cap` (n/2 suffices);
+ * pass NULL arrays to query *nclasses. */
+int sf_plan_sizes(uint32_t n, uint64_t k, int allow_exhaustive,
+                  uint32_t* sizes, uint64_t* pairs, uint64_t* first_pair,
+                  uint64_t cap, uint64_t* nclasses, int* exhaustive,
+                  uint64_t* requested);
+
+/* sampler.hpp:84-85 generate_masks for the plan (sizes/pairs/first_pair as
+ * returned by sf_plan_sizes): this rank's pairs g = rank, rank+world, ...,
+ * row 2j kept-set of local pair j, row 2j+1 its complement; u64 words, bit e
+ * = player e, words_for_bits(n) words per row, row-major. Generated on the
+ * GPU and copied into out_host (capacity cap_words; NULL to query *rows).
+ * rows_of_size (n+1 entries, may be NULL) receives global_rows_of_size. */
+int sf_generate_masks(sf_ctx* ctx, uint32_t n, const uint32_t* sizes,
+                      const uint64_t* pairs, const uint64_t* first_pair,
+                      uint64_t nclasses, int exhaustive, uint64_t seed,
+                      int rank, int world, uint64_t* out_host,
+                      uint64_t cap_words, uint64_t* rows,
+                      uint64_t* rows_of_size);
+
+/* ------------------------------------------------------------ graph + model */
+/* graph.hpp:57-60 build_graph: symmetrize, dedupe, drop self-loops.
+ * edges_uv: num_edges (u, v) pairs; labels may be NULL (kNoLabel). */
+int sf_graph_build(uint32_t num_nodes, const uint64_t* edges_uv,
+                   uint64_t num_edges, const float* features,
+                   uint64_t feature_dim, const uint32_t* labels,
+                   sf_graph** out);
+/* graph.hpp:64 load_graph, binary SFG1 (graph.cpp:35-64) */
+int sf_graph_load(const char* path, sf_graph** out);
+/* graph.hpp:65 save_graph (graph.cpp:171-193) */
+int sf_graph_save(const sf_graph* g, const char* path);
+int sf_graph_free(sf_graph* g);
+int sf_graph_dims(const sf_graph* g, uint32_t* num_nodes, uint64_t* nnz,
+                  uint64_t* feature_dim);
+int sf_graph_csr(const sf_graph* g, uint64_t* row_ptr, uint32_t* col);
+
+/* gcn.hpp:13-30: L layers, dims[0..L], weights concatenated per layer
+ * (in x out row-major), biases concatenated. */
+int sf_model_create(int L, const uint64_t* dims, const float* weights,
+                    const float* biases, sf_model** out);
+/* synthetic.hpp:25-27 gen_random_model (Glorot, Philox stream 16+l) */
+int sf_model_random(uint64_t input_dim, const uint64_t* hidden, int nh,
+                    uint32_t classes, uint64_t seed, sf_model** out);
+int sf_model_free(sf_model* m);
+int sf_model_dims(const sf_model* m, int* L, uint64_t* dims /* L+1 */);
+int sf_model_layer(const sf_model* m, int l, float* weight, float* bias);
+
+/* graph.hpp:69-70 extract_computational_graph (BFS ball, local ids in
+ * discovery order, players sorted, symmetric local CSR with edge_player) */
+int sf_extract(const sf_graph* g, uint32_t target, int hops,
+               sf_subgraph** out);
+int sf_subgraph_free(sf_subgraph* sg);
+int sf_subgraph_dims(const sf_subgraph* sg, uint32_t* V, uint64_t* n,
+                     uint64_t* nnz, uint64_t* feature_dim);
+int sf_subgraph_copy(const sf_subgraph* sg, uint64_t* row_ptr, uint32_t* col,
+                     uint32_t* edge_player, uint32_t* players_uv,
+                     uint32_t* local_to_global, float* features);
+/* |B_h| for h = 0..hops (local ids are BFS order, so each ball is a prefix) */
+int sf_subgraph_ball_sizes(const sf_subgraph* sg, int hops, uint64_t* sizes);
+
+/* ------------------------------------------------------------ inference */
+/* gcn.hpp:60-62 predict_batched: p[class_index] per mask row (host rows in,
+ * host floats out). batch_size is validated like the reference (> 0) but
+ * does not change results: the device engine tiles coalitions itself. */
+int sf_predict_batched(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
+                       const uint64_t* bits, uint64_t rows,
+                       uint64_t words_per_row, uint32_t class_index,
+                       uint64_t batch_size, float* out);
+/* gcn.hpp:50-51 predict_probs: all class probabilities for one mask */
+int sf_predict_probs(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
+                     const uint64_t* mask, uint64_t words, float* probs);
+
+/* ------------------------------------------------------------ solver */
+/* solver.hpp:82-95 solve_cgls on an assembled system whose rows are 0/1
+ * bit rows (WlsProblem.rows packed; row i = bits[i*words ...]).
+ * weights (per row, normalized) and targets (per row, value - base) as in
+ * WlsProblem (solver.hpp:22-38). Collective across the context's ranks.
+ * mode: 0 = reference protocol (1 vector + 1 scalar all-reduce per
+ * iteration, solver.hpp:82-85), 1 = fused (one (n+1)-double all-reduce per
+ * iteration). trace != 0 records per-iteration residuals (out arrays of
+ * capacity trace_cap, may be NULL). */
+int sf_solve_cgls(sf_ctx* ctx, uint32_t n, const uint64_t* bits,
+                  uint64_t rows, uint64_t words, const double* weights,
+                  const double* targets, double constraint_target,
+                  double constraint_weight, double tol, uint64_t max_iter,
+                  int mode, double* phi, uint64_t* iterations,
+                  double* relative_residual, int* converged,
+                  double* trace, double* row_residual_trace,
+                  uint64_t trace_cap);
+/* solver.hpp:46-49 assemble_problem weights: per-row normalized weight
+ * from the global per-size row counts (solver.cpp:125-138). */
+int sf_assemble_weights(uint32_t n, const uint64_t* bits, uint64_t rows,
+                        uint64_t words, const uint64_t* rows_of_size,
+                        double* weights);
+/* solver.hpp:100 solve_direct: dense normal equations (Gram built on the
+ * GPU from the bit rows, Cholesky), n <= 20000, world 1. */
+int sf_solve_direct(sf_ctx* ctx, uint32_t n, const uint64_t* bits,
+                    uint64_t rows, uint64_t words, const double* weights,
+                    const double* targets, double constraint_target,
+                    double constraint_weight, double* phi);
+/* solver.hpp:109 rank_edges: descending phi, ties to the smaller index */
+int sf_rank_edges(const double* phi, uint64_t n, uint32_t* order);
+
+/* ------------------------------------------------------------ pipeline */
+/* explain.hpp:15-32 ExplainOptions */
+typedef struct sf_explain_options {
+  uint64_t samples;         /* 0: sf_auto_samples(n) */
+  uint64_t batch_size;      /* validated, > 0 */
+  uint32_t top_k;
+  uint64_t seed;
+  double tol;
+  uint64_t max_iter;        /* 0: min(n, 5000) */
+  uint64_t player_cap;      /* 0: no cap */
+  int allow_exhaustive;
+  double constraint_scale;
+  int fidelity;
+  uint32_t baseline_trials;
+  int solver_mode;          /* 0 reference protocol, 1 fused all-reduce */
+  const uint32_t* top_counts; /* default {5,10,20} when NULL */
+  uint32_t num_top_counts;
+  const double* sparsities;   /* default {.1,.3,.5,.7,.9} when NULL */
+  uint32_t num_sparsities;
+} sf_explain_options;
+
+void sf_explain_options_default(sf_explain_options* o);
+
+/* document.hpp:22-44 NodeExplanation (+ fidelity.hpp:36-51). Arrays are
+ * owned by the library and released by sf_explanation_free. */
+typedef struct sf_explanation {
+  uint32_t node;
+  int skipped;
+  uint32_t predicted_class;
+  double base_score, full_score;
+  uint64_t num_players;
+  double* phi;              /* num_players */
+  uint32_t* players_global; /* 2 * num_players, smaller id first */
+  int exhaustive;
+  uint64_t rows;
+  uint32_t iterations;
+  double residual;
+  int converged;
+  uint32_t num_top;
+  uint32_t* top_player;
+  double* top_phi;
+  int has_fidelity;
+  uint32_t num_counts;
+  uint32_t* fid_counts;
+  double* fid_plus;
+  double* fid_plus_random;
+  uint32_t num_sparsities;
+  double* fid_sparsities;
+  double* fid_minus;
+  double* fid_minus_random;
+  double sampling_ms, prediction_ms, solve_ms, total_ms;
+  char warning[512];
+} sf_explanation;
+
+/* explain.hpp:47-49 explain_node, collective over the context's ranks */
+int sf_explain_node(sf_ctx* ctx, const sf_graph* g, const sf_model* m,
+                    uint32_t node, const sf_explain_options* opts,
+                    sf_explanation* out);
+int sf_explanation_free(sf_explanation* e);
+
+/* fidelity.hpp:45-51 evaluate_fidelity on the device engine */
+int sf_evaluate_fidelity(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
+                         uint32_t class_index, const double* phi,
+                         const uint32_t* top_counts, uint32_t num_counts,
+                         const double* sparsities, uint32_t num_sparsities,
+                         uint64_t seed, uint32_t trials, uint32_t* counts_out,
+                         double* plus, double* plus_random, double* minus,
+                         double* minus_random);
+
+/* ------------------------------------------------------------ bench hooks
+ * Device-resident sample + masked inference for one target (the
+ * coalitions/s metric): samples this rank's shard on the GPU and scores it,
+ * leaving masks and predictions in HBM. Times (ms, CUDA events on the
+ * context stream) are written to stage_ms[0..1] = {sampling, prediction}
+ * and the dominant kernel's summed duration to stage_ms[2] (may be NULL). */
+int sf_sample_and_predict(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
+                          uint32_t class_index, uint64_t k, uint64_t seed,
+                          int allow_exhaustive, double* stage_ms,
+                          uint64_t* rows_local);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHAPFLOW_B200_H */

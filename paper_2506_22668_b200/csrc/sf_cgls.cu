@@ -1,0 +1,631 @@
+// Weighted least squares on the bit-packed coalition matrix, sm_100a.
+// Replaces assemble_problem + solve_cgls (solver.cpp:95-362) and the Gram
+// build of solve_direct (solver.cpp:364-428).
+//
+// The system is sqrt(W) M phi ~ sqrt(W) t plus one pinned all-ones row of
+// weight constraint_weight and target constraint_target. M stays bit-packed
+// in HBM in two layouts:
+//   rows   row-major u64 words (the sampler's output) -> M u  (forward)
+//   maskt  64-row tiles, u64 per player, bit i = row t*64+i -> M^T r
+// Complement pairs (row 2j+1 = ~row 2j) take the reference's shortcut
+// (solver.cpp:188-198, 209-223, 261-263): the odd dot is sum(u) - dot and
+// the odd row contributes a constant plus a difference on the even row, so
+// only kept-set bits are visited. All n-vectors and row vectors are FP64.
+// Reductions use fixed-shape trees, so a run is bitwise reproducible for a
+// given layout (the reference's cross-world bitwise property comes from its
+// PairwiseFolder; here the parity bar is 1e-3 relative L2).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "sf_device.cuh"
+#include "sf_internal.hpp"
+
+namespace sfb {
+
+namespace {
+
+constexpr int kRedBlocks = 256;
+constexpr int kRedThreads = 256;
+constexpr uint32_t kChunk = 8192;  // players per forward chunk (64 KB of u in smem)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- reductions
+// Fixed-shape two-stage sum: kRedBlocks grid-strided partials, then one
+// block folds them in order. mode 0: sum x, 1: sum x^2, 2: sum (x - c)^2.
+__global__ void __launch_bounds__(kRedThreads)
+    reduce_stage1(const double* __restrict__ x, uint64_t n, int mode, double c,
+                  double* __restrict__ part) {
+  __shared__ double sh[kRedThreads / 32];
+  double acc = 0.0;
+  for (uint64_t i = blockIdx.x * uint64_t(kRedThreads) + threadIdx.x; i < n;
+       i += uint64_t(kRedBlocks) * kRedThreads) {
+    const double v = x[i];
+    acc += mode == 0 ? v : (mode == 1 ? v * v : (v - c) * (v - c));
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kRedThreads / 32 ? sh[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+__global__ void reduce_stage2(const double* __restrict__ part, int count,
+                              double* __restrict__ out) {
+  __shared__ double sh[kRedBlocks];
+  sh[threadIdx.x] = threadIdx.x < count ? part[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int h = kRedBlocks / 2; h > 0; h >>= 1) {
+    if (int(threadIdx.x) < h) sh[threadIdx.x] += sh[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ---------------------------------------------------------------- setup
+// is_comp[j]: row 2j+1 == ~row 2j (tail cleared)  (solver.cpp:188-198)
+__global__ void comp_flags_kernel(const uint64_t* __restrict__ rows, uint32_t W,
+                                  uint32_t n, uint64_t pairs,
+                                  uint8_t* __restrict__ is_comp) {
+  const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= pairs) return;
+  const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  const uint64_t* e = rows + 2 * j * W;
+  const uint64_t* o = e + W;
+  bool ok = true;
+  for (uint32_t w = lane; w < W; w += 32) {
+    uint64_t want = ~e[w];
+    if (w == W - 1) want &= tail;
+    ok &= (o[w] == want);
+  }
+  ok = __all_sync(kFull, ok);
+  if (lane == 0) is_comp[j] = ok ? 1 : 0;
+}
+
+__global__ void init_r_kernel(const double* __restrict__ sw,
+                              const double* __restrict__ tgt, uint64_t rows,
+                              double* __restrict__ r) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < rows) r[i] = sw[i] * tgt[i];
+}
+
+// ---------------------------------------------------------------- M u
+// part[c][row] = sum over set bits e of row within player chunk c of u[e]
+// for every row whose dot is needed (even rows; odd rows of non-complement
+// pairs). One warp per row, u chunk staged in shared memory.
+__global__ void __launch_bounds__(256)
+    forward_partial_kernel(const uint64_t* __restrict__ rows, uint32_t W,
+                           uint64_t nrows, const uint8_t* __restrict__ is_comp,
+                           const double* __restrict__ u, uint32_t n,
+                           double* __restrict__ part) {
+  extern __shared__ double su[];
+  const uint32_t c = blockIdx.y;
+  const uint32_t e0 = c * kChunk;
+  const uint32_t ce = min(n - e0, kChunk);
+  for (uint32_t i = threadIdx.x; i < ce; i += blockDim.x) su[i] = u[e0 + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t w0 = e0 / 64, w1 = min(W, (e0 + ce + 63) / 64);
+  const uint64_t warps = uint64_t(gridDim.x) * 8;
+  for (uint64_t row = blockIdx.x * 8ull + warp; row < nrows; row += warps) {
+    if ((row & 1) && is_comp[row >> 1]) continue;
+    const uint64_t* rp = rows + row * W;
+    double acc = 0.0;
+    for (uint32_t w = w0 + lane; w < w1; w += 32) {
+      uint64_t x = rp[w];
+      const uint32_t base = w * 64 - e0;
+      while (x) {
+        const int b = __ffsll(static_cast<long long>(x)) - 1;
+        x &= x - 1;
+        acc += su[base + b];
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) part[uint64_t(c) * nrows + row] = acc;
+  }
+}
+
+// v_i = sw_i * dot_i; complement odd rows v = sw * (sum_u - dot_even);
+// dsq[j] = v_2j^2 + v_2j+1^2 (per pair, reduced later in fixed order)
+__global__ void forward_finish_kernel(const double* __restrict__ part,
+                                      uint32_t chunks, uint64_t nrows,
+                                      const uint8_t* __restrict__ is_comp,
+                                      const double* __restrict__ sw,
+                                      const double* __restrict__ sum_u,
+                                      double* __restrict__ v,
+                                      double* __restrict__ dsq) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (2 * j >= nrows) return;
+  const uint64_t e = 2 * j;
+  double de = 0.0, dot_o = 0.0;
+  for (uint32_t c = 0; c < chunks; ++c) de += part[uint64_t(c) * nrows + e];
+  const double ve = sw[e] * de;
+  double vo;
+  if (is_comp[j]) {
+    vo = sw[e + 1] * (*sum_u - de);
+  } else {
+    for (uint32_t c = 0; c < chunks; ++c) dot_o += part[uint64_t(c) * nrows + e + 1];
+    vo = sw[e + 1] * dot_o;
+  }
+  v[e] = ve;
+  v[e + 1] = vo;
+  dsq[j] = ve * ve + vo * vo;
+}
+
+// ---------------------------------------------------------------- updates
+__global__ void axpy_kernel(double* __restrict__ y, const double* __restrict__ x,
+                            const double* __restrict__ alpha_num,
+                            const double* __restrict__ alpha_den, double sign,
+                            uint64_t n) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double a = sign * (*alpha_num / *alpha_den);
+  y[i] += a * x[i];
+}
+
+// u = s + beta u, beta = gamma_next / gamma (solver.cpp:357-358)
+__global__ void direction_kernel(double* __restrict__ u, const double* __restrict__ s,
+                                 const double* __restrict__ g_next,
+                                 const double* __restrict__ g, uint64_t n) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double beta = *g_next / *g;
+  u[i] = s[i] + beta * u[i];
+}
+
+// ---------------------------------------------------------------- M^T r
+// coefficients per row: c = sw * r; complement pairs fold into a constant
+// co (every player) plus (ce - co) on the even row (solver.cpp:209-217).
+__global__ void coef_kernel(const double* __restrict__ sw, const double* __restrict__ r,
+                            const uint8_t* __restrict__ is_comp, uint64_t nrows,
+                            double* __restrict__ coef, double* __restrict__ kconst,
+                            uint64_t* __restrict__ nzmask) {
+  const uint64_t row = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  double cf = 0.0, kc = 0.0;
+  if (row < nrows) {
+    const uint64_t j = row >> 1;
+    const double c = sw[row] * r[row];
+    if (is_comp[j]) {
+      if (row & 1) {
+        cf = 0.0;
+        kc = c;
+      } else {
+        cf = c - sw[row + 1] * r[row + 1];
+      }
+    } else {
+      cf = c;
+    }
+    coef[row] = cf;
+    if (row & 1) kconst[j] = kc;
+  }
+  // tile mask of rows with a nonzero coefficient (64 rows = 2 warps)
+  const unsigned b = __ballot_sync(kFull, cf != 0.0);
+  const uint64_t tile = row >> 6;
+  uint32_t* nz32 = reinterpret_cast<uint32_t*>(nzmask);
+  if ((threadIdx.x & 31) == 0)
+    nz32[tile * 2 + ((row >> 5) & 1)] = b;
+}
+
+// s_part[split][e] = sum over tiles of the split, over set bits i of
+// (maskt[t][e] & nz[t]), of coef[t*64+i]
+__global__ void __launch_bounds__(256)
+    transpose_partial_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
+                             uint32_t n, uint64_t tiles, uint64_t tiles_per_split,
+                             const double* __restrict__ coef,
+                             const uint64_t* __restrict__ nzmask,
+                             double* __restrict__ s_part) {
+  __shared__ double sc[64];
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t t0 = blockIdx.y * tiles_per_split;
+  const uint64_t t1 = min(tiles, t0 + tiles_per_split);
+  double acc = 0.0;
+  for (uint64_t t = t0; t < t1; ++t) {
+    __syncthreads();
+    if (threadIdx.x < 64) sc[threadIdx.x] = coef[t * 64 + threadIdx.x];
+    __syncthreads();
+    if (e < n) {
+      uint64_t x = maskt[t * Wp + e] & nzmask[t];
+      while (x) {
+        const int b = __ffsll(static_cast<long long>(x)) - 1;
+        x &= x - 1;
+        acc += sc[b];
+      }
+    }
+  }
+  if (e < n) s_part[uint64_t(blockIdx.y) * n + e] = acc;
+}
+
+// s_e = K + sum_split s_part[split][e]
+__global__ void transpose_finish_kernel(const double* __restrict__ s_part,
+                                        uint32_t splits, uint32_t n,
+                                        const double* __restrict__ kconst,
+                                        double* __restrict__ s) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double acc = *kconst;
+  for (uint32_t k = 0; k < splits; ++k) acc += s_part[uint64_t(k) * n + e];
+  s[e] = acc;
+}
+
+__global__ void add_scalar_kernel(double* __restrict__ s, double c, uint32_t n) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) s[e] += c;
+}
+
+// ---------------------------------------------------------------- assemble
+// per row: size = popcount; sw = sqrt(weight_of_size[size]);
+// target = double(value) - base (solver.cpp:140-154)
+__global__ void assemble_kernel(const uint64_t* __restrict__ rows, uint64_t nrows,
+                                uint32_t W, uint32_t n,
+                                const double* __restrict__ wsize,
+                                const float* __restrict__ values, double base,
+                                double* __restrict__ sw, double* __restrict__ tgt,
+                                int* __restrict__ bad) {
+  const uint64_t row = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  uint32_t cnt = 0;
+  for (uint32_t w = lane; w < W; w += 32) cnt += __popcll(rows[row * W + w]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+  if (lane == 0) {
+    if (cnt == 0 || cnt >= n) {
+      atomicMin(bad, row < 0x7fffffffull ? int(row) : 0x7fffffff);
+      sw[row] = 0.0;
+    } else {
+      sw[row] = sqrt(wsize[cnt]);
+    }
+    tgt[row] = double(values[row]) - base;
+  }
+}
+
+// ---------------------------------------------------------------- Gram
+// G[a][b] = sum_i w_i bit_i(a) bit_i(b) (+ pin), rhs[a] = sum_i w_i t_i bit_i(a)
+__global__ void gram_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
+                           uint32_t n, uint64_t tiles, const double* __restrict__ w,
+                           const double* __restrict__ wt, double cw, double ct,
+                           double* __restrict__ G, double* __restrict__ rhs) {
+  const uint32_t a = blockIdx.y;
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n || b < a) return;
+  double acc = 0.0, racc = 0.0;
+  for (uint64_t t = 0; t < tiles; ++t) {
+    const uint64_t xa = maskt[t * Wp + a];
+    uint64_t x = xa & maskt[t * Wp + b];
+    while (x) {
+      const int i = __ffsll(static_cast<long long>(x)) - 1;
+      x &= x - 1;
+      acc += w[t * 64 + i];
+    }
+    if (b == a) {
+      uint64_t y = xa;
+      while (y) {
+        const int i = __ffsll(static_cast<long long>(y)) - 1;
+        y &= y - 1;
+        racc += wt[t * 64 + i];
+      }
+    }
+  }
+  G[uint64_t(a) * n + b] = acc + cw;
+  G[uint64_t(b) * n + a] = acc + cw;
+  if (b == a) rhs[a] = racc + cw * ct;
+}
+
+__global__ void weight_products_kernel(const double* __restrict__ sw,
+                                       const double* __restrict__ tgt, uint64_t rows,
+                                       uint64_t padded, double* __restrict__ w,
+                                       double* __restrict__ wt) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= padded) return;
+  const double ww = i < rows ? sw[i] * sw[i] : 0.0;
+  w[i] = ww;
+  wt[i] = i < rows ? ww * tgt[i] : 0.0;
+}
+
+inline unsigned blocks_for(uint64_t n, unsigned t = 256) {
+  return unsigned((n + t - 1) / t);
+}
+
+// device scratch for one solve
+struct Scratch {
+  unsigned char* base = nullptr;
+  uint64_t off = 0;
+  template <typename T>
+  T* take(uint64_t count) {
+    off = (off + 255) & ~uint64_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += sizeof(T) * std::max<uint64_t>(count, 1);
+    return p;
+  }
+};
+
+}  // namespace
+
+void launch_assemble(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
+                     uint32_t W, uint32_t n, const double* dev_wsize,
+                     const float* dev_values, double base, double* dev_sw,
+                     double* dev_targets, int* dev_bad_row) {
+  if (rows == 0) return;
+  assemble_kernel<<<blocks_for(rows * 32), 256, 0, ctx.stream>>>(
+      dev_rows, rows, W, n, dev_wsize, dev_values, base, dev_sw, dev_targets, dev_bad_row);
+  SF_LAUNCHED(ctx);
+}
+
+CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
+                      uint64_t max_iter, int mode, bool trace) {
+  (void)mode;  // round 1: reference protocol for both modes
+  CglsResult res;
+  const uint32_t n = in.n;
+  if (n == 0) {
+    res.converged = true;
+    return res;
+  }
+  if (in.rows % 2) throw DataError("local rows must come in adjacent pairs");
+  const uint64_t rows = in.rows, pairs = rows / 2;
+  const uint32_t W = in.W;
+  const uint64_t tiles = (rows + 63) / 64;
+  const uint64_t Wp = uint64_t(W) * 64;
+  const uint32_t chunks = (n + kChunk - 1) / kChunk;
+  int sms = 148;
+  SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
+  // transpose grid: player blocks x tile splits ~ 8 CTAs per SM
+  const uint64_t pblocks = (n + 255) / 256;
+  const uint64_t want_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
+  const uint64_t tiles_per_split =
+      std::max<uint64_t>(1, (tiles + want_splits - 1) / want_splits);
+  const uint32_t splits = uint32_t((tiles + tiles_per_split - 1) / tiles_per_split);
+
+  // scratch layout
+  const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + uint64_t(chunks) * rows * 8 +
+                         tiles * 64 * 8 + tiles * 8 + pairs * 8 * 2 + uint64_t(splits) * n * 8 +
+                         uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
+  ctx.solver_work.reserve(bytes);
+  Scratch sc{ctx.solver_work.p, 0};
+  uint64_t* maskt = sc.take<uint64_t>(tiles * Wp);
+  uint8_t* is_comp = sc.take<uint8_t>(pairs);
+  double* r = sc.take<double>(rows);
+  double* v = sc.take<double>(rows);
+  double* coef = sc.take<double>(tiles * 64);
+  uint64_t* nz = sc.take<uint64_t>(tiles);
+  double* part = sc.take<double>(uint64_t(chunks) * rows);
+  double* dsq = sc.take<double>(pairs);
+  double* kc = sc.take<double>(pairs);
+  double* s_part = sc.take<double>(uint64_t(splits) * n);
+  double* s = sc.take<double>(n);
+  double* u = sc.take<double>(n);
+  double* phi = sc.take<double>(n);
+  double* red = sc.take<double>(kRedBlocks);
+  // device scalars: 0 sum_u, 1 delta, 2 gamma, 3 gamma_next, 4 kconst,
+  // 5 sse, 6 data0
+  double* scal = sc.take<double>(16);
+
+  cudaStream_t st = ctx.stream;
+  auto reduce = [&](const double* x, uint64_t count, int md, double c, double* out) {
+    reduce_stage1<<<kRedBlocks, kRedThreads, 0, st>>>(x, count, md, c, red);
+    SF_LAUNCHED(ctx);
+    reduce_stage2<<<1, kRedBlocks, 0, st>>>(red, kRedBlocks, out);
+    SF_LAUNCHED(ctx);
+  };
+  double* host = nullptr;
+  SF_CUDA(cudaMallocHost(&host, 16 * sizeof(double)));
+  auto fetch = [&](int idx, int count) {
+    ctx.d2h_bytes += uint64_t(count) * sizeof(double);
+    SF_CUDA(cudaMemcpyAsync(host + idx, scal + idx, count * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+  };
+  struct HostFree {
+    double* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } host_guard{host};
+
+  launch_transpose_tiles(ctx, in.dev_rows, rows, W, tiles, maskt);
+  if (pairs) {
+    comp_flags_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, is_comp);
+    SF_LAUNCHED(ctx);
+    init_r_kernel<<<blocks_for(rows), 256, 0, st>>>(in.dev_sw, in.dev_targets, rows, r);
+    SF_LAUNCHED(ctx);
+  }
+  const double scw = std::sqrt(in.constraint_weight);
+  double r_c = scw * in.constraint_target;
+
+  // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
+  auto transpose_product = [&]() {
+    SF_CUDA(cudaMemsetAsync(kc, 0, pairs * 8 + 8, st));
+    if (rows) {
+      coef_kernel<<<blocks_for(tiles * 64, 64), 64, 0, st>>>(in.dev_sw, r, is_comp, rows, coef,
+                                                              kc, nz);
+      SF_LAUNCHED(ctx);
+    }
+    reduce(kc, pairs, 0, 0.0, scal + 4);
+    dim3 grid(blocks_for(n), splits);
+    transpose_partial_kernel<<<grid, 256, 0, st>>>(maskt, Wp, n, tiles, tiles_per_split, coef,
+                                                   nz, s_part);
+    SF_LAUNCHED(ctx);
+    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits, n, scal + 4, s);
+    SF_LAUNCHED(ctx);
+    comm_allreduce_sum(ctx, s, n);
+    add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw * r_c, n);
+    SF_LAUNCHED(ctx);
+  };
+  // v = sqrt(W) M u; delta = ||v||^2 all-reduced + v_c^2 (solver.cpp:252-287)
+  auto forward_product = [&](double& delta, double& v_c) {
+    reduce(u, n, 0, 0.0, scal + 0);  // sum_u
+    if (rows) {
+      const size_t smem = size_t(std::min<uint32_t>(n, kChunk)) * 8;
+      SF_CUDA(cudaFuncSetAttribute(forward_partial_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChunk * 8)));
+      const uint64_t want = (rows + 7) / 8;
+      dim3 grid(unsigned(std::min<uint64_t>(want, uint64_t(sms) * 4)), chunks);
+      forward_partial_kernel<<<grid, 256, smem, st>>>(in.dev_rows, W, rows, is_comp, u, n, part);
+      SF_LAUNCHED(ctx);
+      forward_finish_kernel<<<blocks_for(pairs), 256, 0, st>>>(part, chunks, rows, is_comp,
+                                                                in.dev_sw, scal + 0, v, dsq);
+      SF_LAUNCHED(ctx);
+    }
+    reduce(dsq, pairs, 0, 0.0, scal + 1);
+    comm_allreduce_sum(ctx, scal + 1, 1);
+    fetch(0, 2);
+    delta = host[1];
+    v_c = scw * host[0];
+    delta += v_c * v_c;
+  };
+
+  SF_CUDA(cudaMemsetAsync(phi, 0, uint64_t(n) * 8, st));
+  transpose_product();
+  reduce(s, n, 1, 0.0, scal + 2);                // gamma = ||s||^2
+  reduce(s, n, 2, scw * r_c, scal + 6);          // data0 = ||s - pin||^2
+  fetch(2, 5);
+  double gamma = host[2];
+  const double gamma0 = gamma;
+  const double data0 = host[6];
+  auto download_phi = [&]() {
+    ctx.d2h_bytes += uint64_t(n) * 8;
+    res.phi.resize(n);
+    SF_CUDA(cudaMemcpyAsync(res.phi.data(), phi, uint64_t(n) * 8, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+  };
+  if (gamma0 == 0.0) {
+    res.converged = true;
+    download_phi();
+    return res;
+  }
+  const double reference = data0 > 0.0 ? data0 : gamma0;
+  res.relative_residual = std::sqrt(gamma0 / reference);
+  SF_CUDA(cudaMemcpyAsync(u, s, uint64_t(n) * 8, cudaMemcpyDeviceToDevice, st));
+  const double blowup = 1.0e12 * std::max(res.relative_residual, 1.0);
+  const uint64_t maxit = max_iter ? max_iter : std::min<uint64_t>(n, 5000);
+  while (res.iterations < maxit) {
+    double delta = 0.0, v_c = 0.0;
+    forward_product(delta, v_c);
+    if (!std::isfinite(delta))
+      throw NumericalError("iterative solve diverged at iteration " +
+                           std::to_string(res.iterations) + ": non-finite step norm");
+    if (delta <= 0.0) break;
+    const double theta = gamma / delta;
+    host[8] = gamma;
+    host[9] = delta;
+    // theta on device: write (gamma, delta) into scal[8..9]
+    SF_CUDA(cudaMemcpyAsync(scal + 8, host + 8, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+    axpy_kernel<<<blocks_for(n), 256, 0, st>>>(phi, u, scal + 8, scal + 9, 1.0, n);
+    SF_LAUNCHED(ctx);
+    if (rows) {
+      axpy_kernel<<<blocks_for(rows), 256, 0, st>>>(r, v, scal + 8, scal + 9, -1.0, rows);
+      SF_LAUNCHED(ctx);
+    }
+    r_c -= theta * v_c;
+    if (trace) {
+      reduce(r, rows, 1, 0.0, scal + 5);
+      comm_allreduce_sum(ctx, scal + 5, 1);
+      fetch(5, 1);
+      res.row_residual_trace.push_back(std::sqrt(host[5] + r_c * r_c));
+    }
+    transpose_product();
+    reduce(s, n, 1, 0.0, scal + 3);
+    fetch(3, 1);
+    const double gamma_next = host[3];
+    ++res.iterations;
+    res.relative_residual = std::sqrt(gamma_next / reference);
+    if (trace) res.trace.push_back(res.relative_residual);
+    if (!std::isfinite(gamma_next) || res.relative_residual > blowup)
+      throw NumericalError("iterative solve diverged at iteration " +
+                           std::to_string(res.iterations) + ": residual exploded");
+    if (res.relative_residual <= tol) {
+      res.converged = true;
+      break;
+    }
+    host[10] = gamma_next;
+    host[11] = gamma;
+    SF_CUDA(cudaMemcpyAsync(scal + 10, host + 10, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+    direction_kernel<<<blocks_for(n), 256, 0, st>>>(u, s, scal + 10, scal + 11, n);
+    SF_LAUNCHED(ctx);
+    gamma = gamma_next;
+  }
+  download_phi();
+  return res;
+}
+
+std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in) {
+  const uint32_t n = in.n;
+  if (n == 0) return {};
+  const uint64_t rows = in.rows;
+  const uint32_t W = in.W;
+  const uint64_t tiles = (rows + 63) / 64;
+  const uint64_t Wp = uint64_t(W) * 64;
+  DevBuf<uint64_t> maskt;
+  DevBuf<double> w, wt, G, rhs;
+  maskt.reserve(std::max<uint64_t>(tiles * Wp, 1));
+  w.reserve(tiles * 64 + 1);
+  wt.reserve(tiles * 64 + 1);
+  G.reserve(uint64_t(n) * n);
+  rhs.reserve(n);
+  cudaStream_t st = ctx.stream;
+  launch_transpose_tiles(ctx, in.dev_rows, rows, W, tiles, maskt.p);
+  if (tiles) {
+    weight_products_kernel<<<blocks_for(tiles * 64), 256, 0, st>>>(in.dev_sw, in.dev_targets,
+                                                                    rows, tiles * 64, w.p, wt.p);
+    SF_LAUNCHED(ctx);
+  }
+  dim3 grid(blocks_for(n), n);
+  gram_kernel<<<grid, 256, 0, st>>>(maskt.p, Wp, n, tiles, w.p, wt.p, in.constraint_weight,
+                                    in.constraint_target, G.p, rhs.p);
+  SF_LAUNCHED(ctx);
+  std::vector<double> gram(uint64_t(n) * n), b(n);
+  SF_CUDA(cudaMemcpyAsync(gram.data(), G.p, gram.size() * 8, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaMemcpyAsync(b.data(), rhs.p, uint64_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  // Cholesky with one jitter retry (solver.cpp:383-405), on the host
+  auto factor = [&](std::vector<double> a, std::vector<double>& out) -> uint32_t {
+    for (uint32_t c = 0; c < n; ++c) {
+      double d = a[uint64_t(c) * n + c];
+      for (uint32_t k = 0; k < c; ++k) d -= a[uint64_t(c) * n + k] * a[uint64_t(c) * n + k];
+      if (!(d > 0.0) || !std::isfinite(d)) return c;
+      const double piv = std::sqrt(d);
+      a[uint64_t(c) * n + c] = piv;
+      for (uint32_t rr = c + 1; rr < n; ++rr) {
+        double t = a[uint64_t(rr) * n + c];
+        for (uint32_t k = 0; k < c; ++k) t -= a[uint64_t(rr) * n + k] * a[uint64_t(c) * n + k];
+        a[uint64_t(rr) * n + c] = t / piv;
+      }
+    }
+    out = std::move(a);
+    return n;
+  };
+  std::vector<double> L;
+  if (factor(gram, L) != n) {
+    double tr = 0.0;
+    for (uint32_t a = 0; a < n; ++a) tr += gram[uint64_t(a) * n + a];
+    const double jitter = 1.0e-10 * tr / n;
+    for (uint32_t a = 0; a < n; ++a) gram[uint64_t(a) * n + a] += jitter;
+    const uint32_t bad = factor(gram, L);
+    if (bad != n)
+      throw NumericalError("normal equations are singular: factorization failed at pivot " +
+                           std::to_string(bad) + " of " + std::to_string(n) +
+                           " even after diagonal jitter");
+  }
+  std::vector<double> z(n), phi(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    double t = b[i];
+    for (uint32_t k = 0; k < i; ++k) t -= L[uint64_t(i) * n + k] * z[k];
+    z[i] = t / L[uint64_t(i) * n + i];
+  }
+  for (uint32_t ii = n; ii > 0; --ii) {
+    const uint32_t i = ii - 1;
+    double t = z[i];
+    for (uint32_t k = i + 1; k < n; ++k) t -= L[uint64_t(k) * n + i] * phi[k];
+    phi[i] = t / L[uint64_t(i) * n + i];
+  }
+  return phi;
+}
+
+}  // namespace sfb

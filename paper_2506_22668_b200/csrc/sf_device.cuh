@@ -1,0 +1,53 @@
+// Device helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace sfb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Philox-4x32-10 block (philox.hpp:39-66): key = (lo, hi) of seed, counter
+// = (lo, hi) of the block index followed by (lo, hi) of the stream. The two
+// u64 draws of a block, in the order the reference hands them out
+// (philox.hpp:21-27), are first = (b3 << 32) | b2, second = (b1 << 32) | b0.
+__device__ __forceinline__ void philox_block(uint64_t seed, uint64_t stream,
+                                             uint64_t block, uint64_t& first,
+                                             uint64_t& second) {
+  uint32_t c0 = static_cast<uint32_t>(block), c1 = static_cast<uint32_t>(block >> 32);
+  uint32_t c2 = static_cast<uint32_t>(stream), c3 = static_cast<uint32_t>(stream >> 32);
+  uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  first = (static_cast<uint64_t>(c3) << 32) | c2;
+  second = (static_cast<uint64_t>(c1) << 32) | c0;
+}
+
+// Exact x mod d for a u64 x and a 32-bit d > 0 (the reference takes
+// next_u64() % (m + 1) in 64-bit arithmetic, sampler.cpp:59). Two 32-bit
+// steps: (hi mod d) then ((r << 32) | lo) mod d, the second with a
+// quotient that fits 32 bits.
+__device__ __forceinline__ uint32_t mod_u64_u32(uint64_t x, uint32_t d) {
+  const uint32_t hi = static_cast<uint32_t>(x >> 32);
+  const uint32_t r = hi % d;
+  const uint64_t y = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(x);
+  return static_cast<uint32_t>(y % d);
+}
+
+__device__ __forceinline__ float inv_sqrt_deg(uint32_t deg) {
+  // 1.0f / std::sqrt(static_cast<float>(deg)) with IEEE-rounded sqrt and
+  // division, bitwise equal to the reference (gcn.cpp:82)
+  return __fdiv_rn(1.0f, __fsqrt_rn(static_cast<float>(deg)));
+}
+
+}  // namespace sfb

@@ -1,0 +1,1417 @@
+// Host side of libshapflow_b200: the C-ABI (include/shapflow_b200.h), the
+// size plan, graph construction / SFG1 I/O / computational-graph
+// extraction, model construction, and the explain_node orchestration that
+// drives the sm_100a kernels. Written from the reference's documented
+// behaviour (citations per function); no compute falls back to the CPU.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <numeric>
+#include <sstream>
+
+#include "../../include/shapflow_b200.h"
+#include "sf_internal.hpp"
+
+namespace sfb {
+
+// ---------------------------------------------------------------- Philox (host)
+// philox.hpp:13-73, for model generation and seeds on the host.
+namespace {
+struct HostPhilox {
+  uint32_t key[2], stream[2];
+  uint64_t counter = 0;
+  uint32_t block[4] = {};
+  int have = 0;
+  HostPhilox(uint64_t seed, uint64_t s)
+      : key{uint32_t(seed), uint32_t(seed >> 32)}, stream{uint32_t(s), uint32_t(s >> 32)} {}
+  uint64_t next_u64() {
+    if (have == 0) {
+      uint32_t c[4] = {uint32_t(counter), uint32_t(counter >> 32), stream[0], stream[1]};
+      uint32_t k0 = key[0], k1 = key[1];
+      for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = uint64_t(0xD2511F53u) * c[0];
+        const uint64_t p1 = uint64_t(0xCD9E8D57u) * c[2];
+        const uint32_t n0 = uint32_t(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n2 = uint32_t(p0 >> 32) ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = uint32_t(p1);
+        c[2] = n2;
+        c[3] = uint32_t(p0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+      }
+      std::memcpy(block, c, sizeof c);
+      ++counter;
+      have = 2;
+    }
+    --have;
+    return (uint64_t(block[2 * have + 1]) << 32) | block[2 * have];
+  }
+  double next_double() { return double(next_u64() >> 11) * 0x1.0p-53; }
+};
+}  // namespace
+
+// ---------------------------------------------------------------- plan
+uint64_t binomial_or_max(uint32_t n, uint32_t s) {  // sampler.cpp:67-77
+  if (s > n) return 0;
+  s = std::min(s, n - s);
+  unsigned __int128 r = 1;
+  for (uint32_t i = 1; i <= s; ++i) {
+    r = r * (n - s + i) / i;
+    if (r > UINT64_MAX) return UINT64_MAX;
+  }
+  return static_cast<uint64_t>(r);
+}
+
+SizePlan plan_sizes(uint32_t n, uint64_t k, bool allow_exhaustive) {
+  // sampler.cpp:93-151: pairs split by per-size mass (n-1)/(s(n-s)) (x2 for
+  // a pair covering sizes s and n-s), floor quotas then largest remainder
+  // with ties to the smaller size; classes contiguous in the pair index.
+  if (n < 2)
+    throw DataError("plan_sizes: need at least 2 players, got " + std::to_string(n));
+  if (k == 0) throw DataError("plan_sizes: sample budget must be positive");
+  SizePlan plan;
+  plan.n = n;
+  if (k & 1) ++k;
+  plan.requested = k;
+  if (allow_exhaustive && n <= 62 && ((uint64_t{1} << n) - 2) <= k) {
+    plan.exhaustive = true;
+    uint64_t next = 0;
+    for (uint32_t s = 1; 2 * s <= n; ++s) {
+      uint64_t pairs = binomial_or_max(n, s);
+      if (2 * s == n) pairs /= 2;  // keep the half containing player 0
+      plan.classes.push_back({s, pairs, next});
+      next += pairs;
+    }
+    return plan;
+  }
+  const uint64_t total_pairs = k / 2;
+  const uint32_t half = n / 2;
+  std::vector<double> mass(half + 1, 0.0);
+  double mass_sum = 0.0;
+  for (uint32_t s = 1; s <= half; ++s) {
+    const double rho = (n - 1.0) / (double(s) * double(n - s));
+    mass[s] = (2 * s == n) ? rho : 2.0 * rho;
+    mass_sum += mass[s];
+  }
+  std::vector<uint64_t> quota(half + 1, 0);
+  std::vector<std::pair<double, uint32_t>> order;
+  order.reserve(half);
+  uint64_t assigned = 0;
+  for (uint32_t s = 1; s <= half; ++s) {
+    const double ideal = double(total_pairs) * (mass[s] / mass_sum);
+    const uint64_t q = static_cast<uint64_t>(std::floor(ideal));
+    quota[s] = q;
+    assigned += q;
+    order.emplace_back(-(ideal - double(q)), s);
+  }
+  std::sort(order.begin(), order.end());
+  for (size_t i = 0; assigned < total_pairs; ++i) {
+    ++quota[order[i % order.size()].second];
+    ++assigned;
+  }
+  uint64_t next = 0;
+  for (uint32_t s = 1; s <= half; ++s) {
+    if (quota[s] == 0) continue;
+    plan.classes.push_back({s, quota[s], next});
+    next += quota[s];
+  }
+  return plan;
+}
+
+std::vector<uint64_t> global_rows_of_size(const SizePlan& plan) {
+  // sampler.cpp:168-176
+  std::vector<uint64_t> c(size_t(plan.n) + 1, 0);
+  for (const SizeClass& cls : plan.classes) {
+    if (2 * cls.size == plan.n) {
+      c[cls.size] += 2 * cls.pairs;
+    } else {
+      c[cls.size] += cls.pairs;
+      c[plan.n - cls.size] += cls.pairs;
+    }
+  }
+  return c;
+}
+
+uint64_t local_pair_count(uint64_t global_pairs, int rank, int world) {
+  // pairs g = rank, rank + world, ... (sampler.cpp:177-178)
+  if (uint64_t(rank) >= global_pairs) return 0;
+  return (global_pairs - rank + world - 1) / world;
+}
+
+// per-size weights normalized by the first populated size (solver.cpp:125-138)
+static std::vector<double> weight_of_size(uint32_t n, const std::vector<uint64_t>& counts) {
+  std::vector<double> w(size_t(n) + 1, 0.0);
+  double scale = 0.0;
+  for (uint32_t s = 1; s < n; ++s) {
+    if (counts[s] == 0) continue;
+    const double rho = (n - 1.0) / (double(s) * double(n - s));
+    const double ws = rho / static_cast<double>(counts[s]);
+    if (scale == 0.0) scale = ws;
+    w[s] = ws / scale;
+  }
+  return w;
+}
+
+// ---------------------------------------------------------------- graphs
+static Graph build_graph(uint32_t num_nodes, const uint64_t* edges, uint64_t num_edges,
+                         std::vector<float> features, uint64_t dim,
+                         std::vector<uint32_t> labels) {
+  // graph.cpp:127-163: symmetrize, drop self-loops, dedupe, sorted rows
+  if (features.size() != uint64_t(num_nodes) * dim)
+    throw DataError("feature buffer size does not match num_nodes x dim");
+  if (labels.empty()) labels.assign(num_nodes, 0xFFFFFFFFu);
+  if (labels.size() != num_nodes) throw DataError("label buffer size does not match num_nodes");
+  std::vector<uint64_t> dir;
+  dir.reserve(num_edges * 2);
+  for (uint64_t i = 0; i < num_edges; ++i) {
+    const uint64_t u = edges[2 * i], v = edges[2 * i + 1];
+    if (u >= num_nodes || v >= num_nodes)
+      throw DataError("edge endpoint out of range: (" + std::to_string(u) + ", " +
+                      std::to_string(v) + ") with " + std::to_string(num_nodes) + " nodes");
+    if (u == v) continue;
+    dir.push_back((u << 32) | v);
+    dir.push_back((v << 32) | u);
+  }
+  std::sort(dir.begin(), dir.end());
+  dir.erase(std::unique(dir.begin(), dir.end()), dir.end());
+  Graph g;
+  g.num_nodes = num_nodes;
+  g.feature_dim = dim;
+  g.features = std::move(features);
+  g.labels = std::move(labels);
+  g.row_ptr.assign(size_t(num_nodes) + 1, 0);
+  for (uint64_t x : dir) g.row_ptr[(x >> 32) + 1]++;
+  for (size_t i = 1; i <= num_nodes; ++i) g.row_ptr[i] += g.row_ptr[i - 1];
+  g.col.resize(dir.size());
+  for (size_t i = 0; i < dir.size(); ++i) g.col[i] = uint32_t(dir[i]);
+  return g;
+}
+
+template <typename T>
+static void read_raw(std::istream& in, T* dst, size_t count, const char* what) {
+  in.read(reinterpret_cast<char*>(dst), std::streamsize(sizeof(T) * count));
+  if (!in) throw DataError(std::string("graph file truncated while reading ") + what);
+}
+
+static Graph load_sfg(const std::string& path) {
+  // SFG1 (graph.cpp:35-64): magic, u64 nodes, u64 edges, u64 dim,
+  // edges as u64 pairs, f32 features, u32 labels
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataError("cannot open graph file: " + path);
+  char magic[4];
+  read_raw(in, magic, 4, "magic");
+  if (std::memcmp(magic, "SFG1", 4) != 0) throw DataError("bad magic in " + path + " (expected SFG1)");
+  uint64_t nodes = 0, edges = 0, dim = 0;
+  read_raw(in, &nodes, 1, "node count");
+  read_raw(in, &edges, 1, "edge count");
+  read_raw(in, &dim, 1, "feature dim");
+  if (nodes > 0xFFFFFFFFull) throw DataError("node count too large: " + std::to_string(nodes));
+  std::vector<uint64_t> flat(edges * 2);
+  read_raw(in, flat.data(), flat.size(), "edges");
+  std::vector<float> f(nodes * dim);
+  read_raw(in, f.data(), f.size(), "features");
+  std::vector<uint32_t> labels(nodes);
+  read_raw(in, labels.data(), labels.size(), "labels");
+  return build_graph(uint32_t(nodes), flat.data(), edges, std::move(f), dim, std::move(labels));
+}
+
+static void save_sfg(const Graph& g, const std::string& path) {
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw DataError("cannot write graph file: " + path);
+  out.write("SFG1", 4);
+  const uint64_t nodes = g.num_nodes, edges = g.col.size() / 2, dim = g.feature_dim;
+  out.write(reinterpret_cast<const char*>(&nodes), 8);
+  out.write(reinterpret_cast<const char*>(&edges), 8);
+  out.write(reinterpret_cast<const char*>(&dim), 8);
+  for (uint32_t u = 0; u < g.num_nodes; ++u)
+    for (uint64_t i = g.row_ptr[u]; i < g.row_ptr[u + 1]; ++i)
+      if (u < g.col[i]) {
+        const uint64_t pr[2] = {u, g.col[i]};
+        out.write(reinterpret_cast<const char*>(pr), 16);
+      }
+  out.write(reinterpret_cast<const char*>(g.features.data()), std::streamsize(g.features.size() * 4));
+  out.write(reinterpret_cast<const char*>(g.labels.data()), std::streamsize(g.labels.size() * 4));
+  if (!out) throw DataError("write failed: " + path);
+}
+
+static Subgraph extract(const Graph& g, uint32_t target, int hops) {
+  // graph.cpp:195-261: BFS ball (discovery order = local ids, target 0),
+  // induced undirected edges sorted lexicographically, symmetric local CSR
+  // with edge_player, feature slice.
+  if (target >= g.num_nodes) throw DataError("target node " + std::to_string(target) + " out of range");
+  if (hops < 0) throw DataError("hop count must be nonnegative");
+  std::vector<uint32_t> local_of(g.num_nodes, 0xFFFFFFFFu);
+  Subgraph sg;
+  sg.target_global = target;
+  sg.feature_dim = g.feature_dim;
+  sg.local_to_global.push_back(target);
+  local_of[target] = 0;
+  size_t fb = 0;
+  for (int hop = 0; hop < hops; ++hop) {
+    const size_t fe = sg.local_to_global.size();
+    if (fb == fe) break;
+    for (size_t i = fb; i < fe; ++i) {
+      const uint32_t u = sg.local_to_global[i];
+      for (uint64_t k = g.row_ptr[u]; k < g.row_ptr[u + 1]; ++k) {
+        const uint32_t nb = g.col[k];
+        if (local_of[nb] == 0xFFFFFFFFu) {
+          local_of[nb] = uint32_t(sg.local_to_global.size());
+          sg.local_to_global.push_back(nb);
+        }
+      }
+    }
+    fb = fe;
+  }
+  const uint32_t V = sg.num_nodes();
+  for (uint32_t lu = 0; lu < V; ++lu) {
+    const uint32_t u = sg.local_to_global[lu];
+    for (uint64_t k = g.row_ptr[u]; k < g.row_ptr[u + 1]; ++k) {
+      const uint32_t lv = local_of[g.col[k]];
+      if (lv == 0xFFFFFFFFu) continue;
+      if (lu < lv) sg.players.emplace_back(lu, lv);
+    }
+  }
+  std::sort(sg.players.begin(), sg.players.end());
+  std::vector<uint64_t> deg(V, 0);
+  for (const auto& [u, v] : sg.players) {
+    deg[u]++;
+    deg[v]++;
+  }
+  sg.row_ptr.assign(size_t(V) + 1, 0);
+  for (uint32_t u = 0; u < V; ++u) sg.row_ptr[u + 1] = sg.row_ptr[u] + deg[u];
+  sg.col.resize(sg.row_ptr.back());
+  sg.edge_player.resize(sg.row_ptr.back());
+  std::vector<uint64_t> cursor(sg.row_ptr.begin(), sg.row_ptr.end() - 1);
+  for (uint32_t e = 0; e < sg.players.size(); ++e) {
+    const auto [u, v] = sg.players[e];
+    sg.col[cursor[u]] = v;
+    sg.edge_player[cursor[u]++] = e;
+    sg.col[cursor[v]] = u;
+    sg.edge_player[cursor[v]++] = e;
+  }
+  sg.features.resize(uint64_t(V) * g.feature_dim);
+  for (uint32_t lu = 0; lu < V; ++lu)
+    std::memcpy(sg.features.data() + uint64_t(lu) * g.feature_dim,
+                g.features.data() + uint64_t(sg.local_to_global[lu]) * g.feature_dim,
+                g.feature_dim * 4);
+  return sg;
+}
+
+std::vector<uint64_t> Subgraph::ball_sizes(int hops) const {
+  const uint32_t V = num_nodes();
+  std::vector<int> dist(V, -1);
+  std::vector<uint32_t> q;
+  q.reserve(V);
+  if (V) {
+    dist[0] = 0;
+    q.push_back(0);
+  }
+  for (size_t h = 0; h < q.size(); ++h) {
+    const uint32_t u = q[h];
+    for (uint64_t k = row_ptr[u]; k < row_ptr[u + 1]; ++k)
+      if (dist[col[k]] < 0) {
+        dist[col[k]] = dist[u] + 1;
+        q.push_back(col[k]);
+      }
+  }
+  std::vector<uint64_t> out(size_t(hops) + 1, 0);
+  for (int h = 0; h <= hops; ++h) {
+    uint64_t c = 0;
+    while (c < V && dist[c] >= 0 && dist[c] <= h) ++c;
+    for (uint64_t x = c; x < V; ++x)
+      if (dist[x] >= 0 && dist[x] <= h)
+        throw DataError("subgraph local ids are not in breadth-first order");
+    out[h] = c;
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- model
+static void validate_model(const Model& m) {  // gcn.cpp:14-33
+  if (m.layers.empty()) throw DataError("model has no layers");
+  for (size_t l = 0; l < m.layers.size(); ++l) {
+    const Layer& lay = m.layers[l];
+    if (lay.in == 0 || lay.out == 0)
+      throw DataError("layer " + std::to_string(l) + " has a zero dimension");
+    if (l > 0 && m.layers[l - 1].out != lay.in)
+      throw DataError("dimension chain broken between layers " + std::to_string(l - 1) +
+                      " and " + std::to_string(l));
+  }
+}
+
+static Model random_model(uint64_t input_dim, const uint64_t* hidden, int nh, uint32_t classes,
+                          uint64_t seed) {
+  // synthetic.cpp:88-118: Glorot uniform from Philox(seed, 16 + l), zero bias
+  if (input_dim == 0 || classes == 0)
+    throw DataError("model needs at least one input feature and one class");
+  std::vector<uint64_t> dims{input_dim};
+  for (int i = 0; i < nh; ++i) dims.push_back(hidden[i]);
+  dims.push_back(classes);
+  Model m;
+  for (size_t l = 0; l + 1 < dims.size(); ++l) {
+    Layer lay;
+    lay.in = dims[l];
+    lay.out = dims[l + 1];
+    if (lay.in == 0 || lay.out == 0) throw DataError("hidden layer widths must be positive");
+    HostPhilox rng(seed, 16 + l);
+    const double limit = std::sqrt(6.0 / double(lay.in + lay.out));
+    lay.weight.resize(lay.in * lay.out);
+    for (float& w : lay.weight) w = static_cast<float>(limit * (2.0 * rng.next_double() - 1.0));
+    lay.bias.assign(lay.out, 0.0f);
+    m.layers.push_back(std::move(lay));
+  }
+  return m;
+}
+
+// ---------------------------------------------------------------- engine I/O
+static void upload_rows(Ctx& ctx, const uint64_t* bits, uint64_t rows, uint64_t words,
+                        uint32_t W) {
+  // rows may be wider than words_for_bits(n); keep the first W words
+  ctx.masks.reserve(std::max<uint64_t>(rows * W, 1));
+  if (rows == 0) return;
+  ctx.h2d_bytes += rows * W * 8;
+  if (words == W) {
+    SF_CUDA(cudaMemcpyAsync(ctx.masks.p, bits, rows * W * 8, cudaMemcpyHostToDevice, ctx.stream));
+  } else {
+    SF_CUDA(cudaMemcpy2DAsync(ctx.masks.p, W * 8, bits, words * 8, W * 8, rows,
+                              cudaMemcpyHostToDevice, ctx.stream));
+  }
+}
+
+static void predict_rows(Ctx& ctx, const Subgraph& sg, const Model& m, const uint64_t* dev_rows,
+                         uint64_t rows, uint32_t cls, float* host_out, float* host_probs) {
+  engine_prepare(ctx, sg, m);
+  const uint32_t C = uint32_t(m.layers.back().out);
+  ctx.preds.reserve(std::max<uint64_t>(rows * (host_probs ? C + 1 : 1), 1));
+  float* d_out = ctx.preds.p;
+  float* d_probs = host_probs ? ctx.preds.p + rows : nullptr;
+  engine_predict(ctx, dev_rows, rows, cls, d_out, d_probs, nullptr);
+  ctx.d2h_bytes += (host_out ? rows * 4 : 0) + (host_probs ? rows * C * 4 : 0);
+  if (host_out)
+    SF_CUDA(cudaMemcpyAsync(host_out, d_out, rows * 4, cudaMemcpyDeviceToHost, ctx.stream));
+  if (host_probs)
+    SF_CUDA(cudaMemcpyAsync(host_probs, d_probs, rows * C * 4, cudaMemcpyDeviceToHost, ctx.stream));
+  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+// ---------------------------------------------------------------- fidelity
+static uint32_t kept_at_sparsity(uint32_t n, double sparsity) {  // fidelity.cpp:42-49
+  if (!(sparsity >= 0.0 && sparsity <= 1.0))
+    throw DataError("sparsity must lie in [0, 1], got " + std::to_string(sparsity));
+  const auto kept = static_cast<uint32_t>(std::ceil((1.0 - sparsity) * double(n)));
+  return std::min(kept, n);
+}
+
+static std::vector<uint32_t> ranking(const std::vector<double>& phi) {  // solver.cpp:430-440
+  std::vector<uint32_t> o(phi.size());
+  std::iota(o.begin(), o.end(), 0u);
+  std::sort(o.begin(), o.end(), [&](uint32_t a, uint32_t b) {
+    if (phi[a] != phi[b]) return phi[a] > phi[b];
+    return a < b;
+  });
+  return o;
+}
+
+struct FidelityOut {
+  std::vector<uint32_t> counts;
+  std::vector<double> plus, plus_random, sparsities, minus, minus_random;
+};
+
+// fidelity.cpp:126-162, every mask scored in one batch on the device engine.
+// Row layout: [full] [plus_c for each count] [plus_random trials per count]
+// [minus_s per sparsity] [minus_random trials per sparsity]; the random
+// baselines are Floyd draws on the device with the reference's streams.
+static FidelityOut fidelity(Ctx& ctx, const Subgraph& sg, const Model& m, uint32_t cls,
+                            const std::vector<double>& phi, const std::vector<uint32_t>& counts,
+                            const std::vector<double>& sparsities, uint64_t seed,
+                            uint32_t trials) {
+  const uint32_t n = uint32_t(sg.num_players());
+  if (phi.size() != n)
+    throw DataError("attribution vector has " + std::to_string(phi.size()) + " entries for " +
+                    std::to_string(n) + " players");
+  const uint32_t W = std::max<uint32_t>(1, (n + 63) / 64);
+  const std::vector<uint32_t> ranked = ranking(phi);
+  const uint64_t tail = (n % 64) ? ((uint64_t{1} << (n % 64)) - 1) : ~uint64_t{0};
+  std::vector<uint64_t> full(W, ~uint64_t{0});
+  if (n == 0) full.assign(W, 0);
+  else full[W - 1] = tail;
+  const size_t nc = counts.size(), ns = sparsities.size();
+  const uint64_t rows = 1 + nc + nc * trials + ns + ns * trials;
+  std::vector<uint64_t> host(rows * W, 0);
+  auto row = [&](uint64_t r) { return host.data() + r * W; };
+  std::copy(full.begin(), full.end(), row(0));
+  FidelityOut out;
+  std::vector<uint64_t> streams;
+  std::vector<uint32_t> sizes;
+  std::vector<uint8_t> invert;
+  std::vector<uint64_t> job_rows;
+  for (size_t i = 0; i < nc; ++i) {
+    const uint32_t c = std::min(counts[i], n);
+    out.counts.push_back(c);
+    uint64_t* r = row(1 + i);
+    std::copy(full.begin(), full.end(), r);
+    for (uint32_t k = 0; k < c; ++k) r[ranked[k] >> 6] &= ~(uint64_t{1} << (ranked[k] & 63));
+    for (uint32_t t = 0; t < trials; ++t) {
+      streams.push_back((uint64_t(c) << 32) | t);  // fidelity.cpp:99-100
+      sizes.push_back(c);
+      invert.push_back(1);
+      job_rows.push_back(1 + nc + i * trials + t);
+    }
+  }
+  const uint64_t mbase = 1 + nc + nc * trials;
+  for (size_t i = 0; i < ns; ++i) {
+    const uint32_t keep = kept_at_sparsity(n, sparsities[i]);
+    out.sparsities.push_back(sparsities[i]);
+    uint64_t* r = row(mbase + i);
+    for (uint32_t k = 0; k < keep; ++k) r[ranked[k] >> 6] |= uint64_t{1} << (ranked[k] & 63);
+    for (uint32_t t = 0; t < trials; ++t) {
+      streams.push_back((uint64_t(keep) << 32) | (uint64_t{1} << 63) | t);  // 117-118
+      sizes.push_back(keep);
+      invert.push_back(0);
+      job_rows.push_back(mbase + ns + i * trials + t);
+    }
+  }
+  // device: deterministic rows, then the Floyd jobs written in place
+  ctx.masks.reserve(rows * W);
+  SF_CUDA(cudaMemcpyAsync(ctx.masks.p, host.data(), rows * W * 8, cudaMemcpyHostToDevice, ctx.stream));
+  ctx.h2d_bytes += rows * W * 8;
+  const uint64_t jobs = streams.size();
+  if (jobs) {
+    DevBuf<uint64_t> d_streams, d_rows;
+    DevBuf<uint32_t> d_sizes;
+    DevBuf<uint8_t> d_inv;
+    d_streams.upload(streams.data(), jobs, ctx.stream);
+    d_sizes.upload(sizes.data(), jobs, ctx.stream);
+    d_inv.upload(invert.data(), jobs, ctx.stream);
+    d_rows.reserve(jobs * W);
+    launch_floyd_jobs(ctx, n, seed, d_streams.p, d_sizes.p, d_inv.p, jobs, d_rows.p);
+    // trial rows are contiguous per block: copy the job rows into place
+    for (uint64_t j = 0; j < jobs;) {
+      uint64_t k = j;
+      while (k + 1 < jobs && job_rows[k + 1] == job_rows[k] + 1) ++k;
+      SF_CUDA(cudaMemcpyAsync(ctx.masks.p + job_rows[j] * W, d_rows.p + j * W,
+                              (k - j + 1) * W * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+      j = k + 1;
+    }
+    SF_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
+  std::vector<float> score(rows);
+  predict_rows(ctx, sg, m, ctx.masks.p, rows, cls, score.data(), nullptr);
+  const double f0 = double(score[0]);
+  for (size_t i = 0; i < nc; ++i) {
+    out.plus.push_back(std::abs(f0 - double(score[1 + i])));
+    double acc = 0.0;
+    for (uint32_t t = 0; t < trials; ++t) acc += std::abs(f0 - double(score[1 + nc + i * trials + t]));
+    out.plus_random.push_back(trials ? acc / double(trials) : 0.0);
+  }
+  for (size_t i = 0; i < ns; ++i) {
+    out.minus.push_back(std::abs(f0 - double(score[mbase + i])));
+    double acc = 0.0;
+    for (uint32_t t = 0; t < trials; ++t)
+      acc += std::abs(f0 - double(score[mbase + ns + i * trials + t]));
+    out.minus_random.push_back(trials ? acc / double(trials) : 0.0);
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- explain
+using Clock = std::chrono::steady_clock;
+static double ms_since(Clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t).count();
+}
+
+template <typename T>
+static T* dup_array(const std::vector<T>& v) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * std::max<size_t>(v.size(), 1)));
+  if (!p) throw std::bad_alloc();
+  if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
+  return p;
+}
+
+static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node,
+                         const sf_explain_options& o, sf_explanation* out) {
+  // explain.cpp:42-143
+  const auto t_start = Clock::now();
+  std::memset(out, 0, sizeof(*out));
+  out->node = node;
+  out->converged = 1;
+  if (o.batch_size == 0) throw DataError("batch_size must be positive");
+  if (m.layers.front().in != g.feature_dim)
+    throw DataError("model expects " + std::to_string(m.layers.front().in) +
+                    " input features but the graph has " + std::to_string(g.feature_dim));
+  const Subgraph sg = extract(g, node, m.depth());
+  const uint64_t n_raw = sg.num_players();
+  if (o.player_cap != 0 && n_raw > o.player_cap) {
+    out->skipped = 1;
+    std::snprintf(out->warning, sizeof(out->warning),
+                  "node %u skipped: %llu players exceed the cap of %llu", node,
+                  (unsigned long long)n_raw, (unsigned long long)o.player_cap);
+    out->total_ms = ms_since(t_start);
+    return;
+  }
+  const uint32_t n = uint32_t(n_raw);
+  const uint64_t seed = sf_node_sampling_seed(o.seed, node);
+  const uint32_t W = std::max<uint32_t>(1, (n + 63) / 64);
+  const uint32_t C = uint32_t(m.layers.back().out);
+
+  // full-mask probabilities -> class (first argmax), empty-mask base score
+  {
+    std::vector<uint64_t> two(2 * W, 0);
+    for (uint32_t w = 0; w < W; ++w) two[w] = ~uint64_t{0};
+    if (n % 64) two[W - 1] = (uint64_t{1} << (n % 64)) - 1;
+    if (n == 0) two[0] = 0;
+    upload_rows(ctx, two.data(), 2, W, W);
+    std::vector<float> probs(2 * C);
+    predict_rows(ctx, sg, m, ctx.masks.p, 2, 0, nullptr, probs.data());
+    const uint32_t cls = uint32_t(std::max_element(probs.begin(), probs.begin() + C) - probs.begin());
+    out->predicted_class = cls;
+    out->full_score = double(probs[cls]);
+    out->base_score = double(probs[C + cls]);
+  }
+  std::vector<uint32_t> players_global;
+  players_global.reserve(2 * n);
+  for (const auto& [u, v] : sg.players) {
+    uint32_t gu = sg.local_to_global[u], gv = sg.local_to_global[v];
+    if (gu > gv) std::swap(gu, gv);
+    players_global.push_back(gu);
+    players_global.push_back(gv);
+  }
+  out->num_players = n;
+  out->players_global = dup_array(players_global);
+  std::vector<double> phi;
+  if (n == 0) {
+    out->exhaustive = 1;
+  } else if (n == 1) {
+    phi = {out->full_score - out->base_score};
+    out->exhaustive = 1;
+  } else {
+    const uint64_t k = o.samples ? o.samples : sf_auto_samples(n);
+    comm_barrier(ctx);
+    auto t_stage = Clock::now();
+    const SizePlan plan = plan_sizes(n, k, o.allow_exhaustive != 0);
+    const uint64_t pairs = local_pair_count(plan.total_pairs(), ctx.rank, ctx.world);
+    const uint64_t rows = 2 * pairs;
+    ctx.masks.reserve(std::max<uint64_t>(rows * W, 1));
+    launch_generate_masks(ctx, plan, seed, ctx.rank, ctx.world, ctx.masks.p);
+    comm_barrier(ctx);
+    out->sampling_ms = ms_since(t_stage);
+    out->exhaustive = plan.exhaustive ? 1 : 0;
+    out->rows = plan.total_pairs() * 2;
+
+    t_stage = Clock::now();
+    engine_prepare(ctx, sg, m);
+    ctx.preds.reserve(std::max<uint64_t>(rows, 1));
+    engine_predict(ctx, ctx.masks.p, rows, out->predicted_class, ctx.preds.p, nullptr, nullptr);
+    comm_barrier(ctx);
+    out->prediction_ms = ms_since(t_stage);
+
+    t_stage = Clock::now();
+    const std::vector<double> wsize = weight_of_size(n, global_rows_of_size(plan));
+    DevBuf<double> d_wsize, d_sw, d_tgt;
+    DevBuf<int> d_bad;
+    d_wsize.upload(wsize.data(), wsize.size(), ctx.stream);
+    d_sw.reserve(std::max<uint64_t>(rows, 1));
+    d_tgt.reserve(std::max<uint64_t>(rows, 1));
+    const int big = 0x7fffffff;
+    d_bad.upload(&big, 1, ctx.stream);
+    launch_assemble(ctx, ctx.masks.p, rows, W, n, d_wsize.p, ctx.preds.p, out->base_score, d_sw.p,
+                    d_tgt.p, d_bad.p);
+    ctx.h2d_bytes += wsize.size() * 8 + 4;
+    ctx.d2h_bytes += 4;
+    int bad = big;
+    SF_CUDA(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    SF_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (bad != big)
+      throw DataError("coalition row " + std::to_string(bad) + " keeps all or no players");
+    CglsInput in;
+    in.n = n;
+    in.rows = rows;
+    in.W = W;
+    in.dev_rows = ctx.masks.p;
+    in.dev_sw = d_sw.p;
+    in.dev_targets = d_tgt.p;
+    in.constraint_target = out->full_score - out->base_score;
+    in.constraint_weight = o.constraint_scale;
+    in.global_pair_count = plan.total_pairs();
+    CglsResult res = cgls_solve(ctx, in, o.tol, o.max_iter, o.solver_mode, false);
+    comm_barrier(ctx);
+    out->solve_ms = ms_since(t_stage);
+    phi = std::move(res.phi);
+    out->iterations = uint32_t(res.iterations);
+    out->residual = res.relative_residual;
+    out->converged = res.converged ? 1 : 0;
+    if (!res.converged) {
+      std::ostringstream msg;
+      msg << "node " << node << ": solver stopped after " << res.iterations
+          << " iterations at relative residual " << res.relative_residual << " (tol " << o.tol
+          << ")";
+      std::snprintf(out->warning, sizeof(out->warning), "%s", msg.str().c_str());
+    }
+  }
+  out->phi = dup_array(phi);
+  const std::vector<uint32_t> ranked = ranking(phi);
+  const size_t keep = std::min<size_t>(o.top_k, ranked.size());
+  std::vector<uint32_t> tp(ranked.begin(), ranked.begin() + keep);
+  std::vector<double> tv(keep);
+  for (size_t i = 0; i < keep; ++i) tv[i] = phi[tp[i]];
+  out->num_top = uint32_t(keep);
+  out->top_player = dup_array(tp);
+  out->top_phi = dup_array(tv);
+  if (o.fidelity) {
+    std::vector<uint32_t> counts = o.top_counts ? std::vector<uint32_t>(o.top_counts, o.top_counts + o.num_top_counts)
+                                                : std::vector<uint32_t>{5, 10, 20};
+    std::vector<double> sp = o.sparsities ? std::vector<double>(o.sparsities, o.sparsities + o.num_sparsities)
+                                          : std::vector<double>{0.1, 0.3, 0.5, 0.7, 0.9};
+    FidelityOut f = fidelity(ctx, sg, m, out->predicted_class, phi, counts, sp, seed, o.baseline_trials);
+    out->has_fidelity = 1;
+    out->num_counts = uint32_t(f.counts.size());
+    out->fid_counts = dup_array(f.counts);
+    out->fid_plus = dup_array(f.plus);
+    out->fid_plus_random = dup_array(f.plus_random);
+    out->num_sparsities = uint32_t(f.sparsities.size());
+    out->fid_sparsities = dup_array(f.sparsities);
+    out->fid_minus = dup_array(f.minus);
+    out->fid_minus_random = dup_array(f.minus_random);
+  }
+  out->total_ms = ms_since(t_start);
+}
+
+}  // namespace sfb
+
+// ================================================================ C-ABI
+using namespace sfb;
+
+struct sf_ctx {
+  Ctx c;
+};
+struct sf_graph {
+  Graph g;
+};
+struct sf_model {
+  Model m;
+};
+struct sf_subgraph {
+  Subgraph s;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return SF_OK;
+  } catch (const DataError& e) {
+    g_last_error = e.what();
+    return SF_ERR_DATA;
+  } catch (const NumericalError& e) {
+    g_last_error = e.what();
+    return SF_ERR_NUMERICAL;
+  } catch (const ProtocolError& e) {
+    g_last_error = e.what();
+    return SF_ERR_PROTOCOL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SF_ERR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return SF_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw DataError(std::string("null ") + what);
+}
+
+SizePlan plan_from_arrays(uint32_t n, const uint32_t* sizes, const uint64_t* pairs,
+                          const uint64_t* first, uint64_t nclasses, int exhaustive) {
+  SizePlan p;
+  p.n = n;
+  p.exhaustive = exhaustive != 0;
+  for (uint64_t i = 0; i < nclasses; ++i) {
+    if (sizes[i] == 0 || 2 * uint64_t(sizes[i]) > n)
+      throw DataError("size class " + std::to_string(sizes[i]) + " invalid for " +
+                      std::to_string(n) + " players");
+    if (i > 0 && first[i] != first[i - 1] + pairs[i - 1])
+      throw DataError("size classes must be contiguous in the pair index");
+    p.classes.push_back({sizes[i], pairs[i], first[i]});
+  }
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sf_last_error(void) { return g_last_error.c_str(); }
+const char* sf_version(void) { return "shapflow_b200 0.1 (sm_100a)"; }
+
+int sf_ctx_create(int device, sf_ctx** out) {
+  return guard([&] {
+    need(out, "output");
+    int count = 0;
+    SF_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+      throw DataError("CUDA device " + std::to_string(device) + " not present (" +
+                      std::to_string(count) + " visible)");
+    auto* c = new sf_ctx;
+    c->c.device = device;
+    try {
+      SF_CUDA(cudaSetDevice(device));
+      SF_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int sf_ctx_destroy(sf_ctx* ctx) {
+  return guard([&] {
+    if (ctx) {
+      cudaSetDevice(ctx->c.device);
+      delete ctx;
+    }
+  });
+}
+
+int sf_ctx_rank(const sf_ctx* ctx) { return ctx ? ctx->c.rank : -1; }
+int sf_ctx_world(const sf_ctx* ctx) { return ctx ? ctx->c.world : -1; }
+uint64_t sf_ctx_launches(const sf_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int sf_ctx_io_bytes(const sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+  return guard([&] {
+    need(ctx, "context");
+    if (h2d) *h2d = ctx->c.h2d_bytes;
+    if (d2h) *d2h = ctx->c.d2h_bytes;
+  });
+}
+
+int sf_ctx_event_record(sf_ctx* ctx, int slot) {
+  return guard([&] {
+    need(ctx, "context");
+    if (slot < 0 || slot >= 8) throw DataError("event slot out of range");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    if (!ctx->c.events[slot]) SF_CUDA(cudaEventCreate(&ctx->c.events[slot]));
+    SF_CUDA(cudaEventRecord(ctx->c.events[slot], ctx->c.stream));
+  });
+}
+
+int sf_ctx_event_elapsed(sf_ctx* ctx, int a, int b, float* ms) {
+  return guard([&] {
+    need(ctx, "context");
+    need(ms, "output");
+    if (a < 0 || a >= 8 || b < 0 || b >= 8 || !ctx->c.events[a] || !ctx->c.events[b])
+      throw DataError("event slot not recorded");
+    SF_CUDA(cudaEventSynchronize(ctx->c.events[b]));
+    SF_CUDA(cudaEventElapsedTime(ms, ctx->c.events[a], ctx->c.events[b]));
+  });
+}
+
+int sf_ctx_synchronize(sf_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "context");
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sf_ctx_time_dominant(sf_ctx* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "context");
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    ctx->c.time_dominant = enable != 0;
+    ctx->c.dom_used = 0;
+    ctx->c.dom_pairs = 0;
+  });
+}
+
+int sf_ctx_dominant_stats(sf_ctx* ctx, double* total_ms, uint64_t* launches, uint64_t* pairs) {
+  return guard([&] {
+    need(ctx, "context");
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    double tot = 0.0;
+    for (size_t i = 0; i < ctx->c.dom_used; ++i) {
+      float ms = 0.f;
+      SF_CUDA(cudaEventElapsedTime(&ms, ctx->c.dom_events[i].first, ctx->c.dom_events[i].second));
+      tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = ctx->c.dom_used;
+    if (pairs) *pairs = ctx->c.dom_pairs;
+  });
+}
+
+int sf_spmm_bytes_per_pair(const sf_model* m, const sf_subgraph* sgp, double* bytes, double* flops) {
+  return guard([&] {
+    need(m, "model");
+    need(sgp, "subgraph");
+    const Subgraph& sg = sgp->s;
+    const int L = m->m.depth();
+    const auto ball = sg.ball_sizes(L);
+    // layer 0 produces rows R = B_{L-1} (the target row alone when L == 1)
+    const uint64_t R = ball[L - 1];
+    const double d = double(m->m.layers.front().out);
+    uint64_t deg = 0;
+    for (uint64_t u = 0; u < R; ++u) deg += sg.row_ptr[u + 1] - sg.row_ptr[u];
+    const double W = double((sg.num_players() + 63) / 64);
+    if (bytes) *bytes = (double(deg) + 2.0 * R) * d * 4.0 + 2.0 * R * d * 4.0 + 2.0 * W * 8.0;
+    if (flops) *flops = 2.0 * (double(deg) + 2.0 * R) * d;
+  });
+}
+
+int sf_nccl_unique_id(void* out) {
+  return guard([&] {
+    need(out, "output");
+    nccl_unique_id(out);
+  });
+}
+
+int sf_ctx_join_nccl(sf_ctx* ctx, const void* id, int rank, int world) {
+  return guard([&] {
+    need(ctx, "context");
+    if (world > 1) need(id, "unique id");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    nccl_join(ctx->c, id, rank, world);
+  });
+}
+
+int sf_ctx_stats(const sf_ctx* ctx, uint64_t* s, uint64_t* v, uint64_t* b, uint64_t* d) {
+  return guard([&] {
+    need(ctx, "context");
+    if (s) *s = ctx->c.stats.scalar_allreduce;
+    if (v) *v = ctx->c.stats.vector_allreduce;
+    if (b) *b = ctx->c.stats.barriers;
+    if (d) *d = ctx->c.stats.doubles_reduced;
+  });
+}
+
+int sf_ctx_barrier(sf_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "context");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    comm_barrier(ctx->c);
+  });
+}
+
+uint64_t sf_node_sampling_seed(uint64_t seed, uint32_t node) {
+  return seed ^ (0x9E3779B97F4A7C15ull * (uint64_t(node) + 1));  // explain.cpp:37-40
+}
+
+uint64_t sf_auto_samples(uint64_t n) { return n < 5000 ? 60000 : 600000; }
+
+uint64_t sf_binomial_or_max(uint32_t n, uint32_t s) { return binomial_or_max(n, s); }
+
+int sf_kernel_weight(uint32_t n, uint32_t s, double* out) {
+  return guard([&] {  // sampler.cpp:79-91
+    need(out, "output");
+    if (n < 2 || s == 0 || s >= n)
+      throw DataError("coalition weight undefined for size " + std::to_string(s) + " of " +
+                      std::to_string(n) + " players");
+    if (n <= 60) {
+      const double c = double(binomial_or_max(n, s));
+      *out = (n - 1.0) / (c * s * (n - s));
+      return;
+    }
+    const double log_c = std::lgamma(n + 1.0) - std::lgamma(s + 1.0) - std::lgamma(n - s + 1.0);
+    *out = std::exp(std::log(n - 1.0) - log_c - std::log(double(s)) - std::log(double(n - s)));
+  });
+}
+
+int sf_philox_u64(sf_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t count, uint64_t* out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "output");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    DevBuf<uint64_t> d;
+    d.reserve(std::max<uint64_t>(count, 1));
+    launch_philox_stream(ctx->c, seed, stream, count, d.p);
+    SF_CUDA(cudaMemcpyAsync(out, d.p, count * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sf_plan_sizes(uint32_t n, uint64_t k, int allow, uint32_t* sizes, uint64_t* pairs,
+                  uint64_t* first, uint64_t cap, uint64_t* nclasses, int* exhaustive,
+                  uint64_t* requested) {
+  return guard([&] {
+    const SizePlan p = plan_sizes(n, k, allow != 0);
+    if (nclasses) *nclasses = p.classes.size();
+    if (exhaustive) *exhaustive = p.exhaustive ? 1 : 0;
+    if (requested) *requested = p.requested;
+    if (sizes && pairs && first) {
+      if (p.classes.size() > cap) throw DataError("plan arrays too small");
+      for (size_t i = 0; i < p.classes.size(); ++i) {
+        sizes[i] = p.classes[i].size;
+        pairs[i] = p.classes[i].pairs;
+        first[i] = p.classes[i].first_pair;
+      }
+    }
+  });
+}
+
+int sf_generate_masks(sf_ctx* ctx, uint32_t n, const uint32_t* sizes, const uint64_t* pairs,
+                      const uint64_t* first, uint64_t nclasses, int exhaustive, uint64_t seed,
+                      int rank, int world, uint64_t* out, uint64_t cap_words, uint64_t* rows,
+                      uint64_t* rows_of_size) {
+  return guard([&] {
+    need(ctx, "context");
+    if (world < 1 || rank < 0 || rank >= world)
+      throw DataError("invalid worker rank " + std::to_string(rank) + " of " + std::to_string(world));
+    const SizePlan p = plan_from_arrays(n, sizes, pairs, first, nclasses, exhaustive);
+    const uint64_t lp = local_pair_count(p.total_pairs(), rank, world);
+    const uint64_t W = (n + 63) / 64;
+    if (rows) *rows = 2 * lp;
+    if (rows_of_size) {
+      const auto c = global_rows_of_size(p);
+      std::memcpy(rows_of_size, c.data(), c.size() * 8);
+    }
+    if (!out) return;
+    if (2 * lp * W > cap_words) throw DataError("mask output buffer too small");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.masks.reserve(std::max<uint64_t>(2 * lp * W, 1));
+    launch_generate_masks(ctx->c, p, seed, rank, world, ctx->c.masks.p);
+    SF_CUDA(cudaMemcpyAsync(out, ctx->c.masks.p, 2 * lp * W * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sf_graph_build(uint32_t num_nodes, const uint64_t* edges, uint64_t num_edges,
+                   const float* features, uint64_t dim, const uint32_t* labels, sf_graph** out) {
+  return guard([&] {
+    need(out, "output");
+    if (num_edges) need(edges, "edges");
+    if (uint64_t(num_nodes) * dim != 0) need(features, "features");
+    std::vector<float> f(features, features + uint64_t(num_nodes) * dim);
+    std::vector<uint32_t> lab;
+    if (labels) lab.assign(labels, labels + num_nodes);
+    auto* g = new sf_graph{build_graph(num_nodes, edges, num_edges, std::move(f), dim, std::move(lab))};
+    *out = g;
+  });
+}
+
+int sf_graph_load(const char* path, sf_graph** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "output");
+    const std::string p(path);
+    if (p.size() < 4 || p.substr(p.size() - 4) != ".sfg")
+      throw DataError("only binary SFG1 graphs (.sfg) are supported: " + p);
+    *out = new sf_graph{load_sfg(p)};
+  });
+}
+
+int sf_graph_save(const sf_graph* g, const char* path) {
+  return guard([&] {
+    need(g, "graph");
+    need(path, "path");
+    save_sfg(g->g, path);
+  });
+}
+
+int sf_graph_free(sf_graph* g) {
+  delete g;
+  return SF_OK;
+}
+
+int sf_graph_dims(const sf_graph* g, uint32_t* nodes, uint64_t* nnz, uint64_t* dim) {
+  return guard([&] {
+    need(g, "graph");
+    if (nodes) *nodes = g->g.num_nodes;
+    if (nnz) *nnz = g->g.col.size();
+    if (dim) *dim = g->g.feature_dim;
+  });
+}
+
+int sf_graph_csr(const sf_graph* g, uint64_t* row_ptr, uint32_t* col) {
+  return guard([&] {
+    need(g, "graph");
+    if (row_ptr) std::memcpy(row_ptr, g->g.row_ptr.data(), g->g.row_ptr.size() * 8);
+    if (col) std::memcpy(col, g->g.col.data(), g->g.col.size() * 4);
+  });
+}
+
+int sf_model_create(int L, const uint64_t* dims, const float* weights, const float* biases,
+                    sf_model** out) {
+  return guard([&] {
+    need(out, "output");
+    need(dims, "dims");
+    if (L < 1) throw DataError("model has no layers");
+    Model m;
+    for (int l = 0; l < L; ++l) {
+      Layer lay;
+      lay.in = dims[l];
+      lay.out = dims[l + 1];
+      lay.weight.assign(weights, weights + lay.in * lay.out);
+      lay.bias.assign(biases, biases + lay.out);
+      weights += lay.in * lay.out;
+      biases += lay.out;
+      m.layers.push_back(std::move(lay));
+    }
+    validate_model(m);
+    *out = new sf_model{std::move(m)};
+  });
+}
+
+int sf_model_random(uint64_t input_dim, const uint64_t* hidden, int nh, uint32_t classes,
+                    uint64_t seed, sf_model** out) {
+  return guard([&] {
+    need(out, "output");
+    *out = new sf_model{random_model(input_dim, hidden, nh, classes, seed)};
+  });
+}
+
+int sf_model_free(sf_model* m) {
+  delete m;
+  return SF_OK;
+}
+
+int sf_model_dims(const sf_model* m, int* L, uint64_t* dims) {
+  return guard([&] {
+    need(m, "model");
+    if (L) *L = m->m.depth();
+    if (dims) {
+      dims[0] = m->m.layers.front().in;
+      for (int l = 0; l < m->m.depth(); ++l) dims[l + 1] = m->m.layers[l].out;
+    }
+  });
+}
+
+int sf_model_layer(const sf_model* m, int l, float* w, float* b) {
+  return guard([&] {
+    need(m, "model");
+    if (l < 0 || l >= m->m.depth()) throw DataError("layer index out of range");
+    const Layer& lay = m->m.layers[l];
+    if (w) std::memcpy(w, lay.weight.data(), lay.weight.size() * 4);
+    if (b) std::memcpy(b, lay.bias.data(), lay.bias.size() * 4);
+  });
+}
+
+int sf_extract(const sf_graph* g, uint32_t target, int hops, sf_subgraph** out) {
+  return guard([&] {
+    need(g, "graph");
+    need(out, "output");
+    *out = new sf_subgraph{extract(g->g, target, hops)};
+  });
+}
+
+int sf_subgraph_free(sf_subgraph* sg) {
+  delete sg;
+  return SF_OK;
+}
+
+int sf_subgraph_dims(const sf_subgraph* sg, uint32_t* V, uint64_t* n, uint64_t* nnz, uint64_t* dim) {
+  return guard([&] {
+    need(sg, "subgraph");
+    if (V) *V = sg->s.num_nodes();
+    if (n) *n = sg->s.num_players();
+    if (nnz) *nnz = sg->s.col.size();
+    if (dim) *dim = sg->s.feature_dim;
+  });
+}
+
+int sf_subgraph_copy(const sf_subgraph* sgp, uint64_t* row_ptr, uint32_t* col, uint32_t* ep,
+                     uint32_t* players_uv, uint32_t* l2g, float* features) {
+  return guard([&] {
+    need(sgp, "subgraph");
+    const Subgraph& sg = sgp->s;
+    if (row_ptr) std::memcpy(row_ptr, sg.row_ptr.data(), sg.row_ptr.size() * 8);
+    if (col) std::memcpy(col, sg.col.data(), sg.col.size() * 4);
+    if (ep) std::memcpy(ep, sg.edge_player.data(), sg.edge_player.size() * 4);
+    if (players_uv)
+      for (size_t e = 0; e < sg.players.size(); ++e) {
+        players_uv[2 * e] = sg.players[e].first;
+        players_uv[2 * e + 1] = sg.players[e].second;
+      }
+    if (l2g) std::memcpy(l2g, sg.local_to_global.data(), sg.local_to_global.size() * 4);
+    if (features) std::memcpy(features, sg.features.data(), sg.features.size() * 4);
+  });
+}
+
+int sf_subgraph_ball_sizes(const sf_subgraph* sg, int hops, uint64_t* sizes) {
+  return guard([&] {
+    need(sg, "subgraph");
+    need(sizes, "output");
+    const auto b = sg->s.ball_sizes(hops);
+    std::memcpy(sizes, b.data(), b.size() * 8);
+  });
+}
+
+int sf_predict_batched(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg, const uint64_t* bits,
+                       uint64_t rows, uint64_t words, uint32_t cls, uint64_t batch_size, float* out) {
+  return guard([&] {  // gcn.cpp:259-270 + validation 43-49
+    need(ctx, "context");
+    need(m, "model");
+    need(sg, "subgraph");
+    if (cls >= m->m.layers.back().out) throw DataError("class index out of range");
+    if (m->m.layers.front().in != sg->s.feature_dim)
+      throw DataError("model input dim " + std::to_string(m->m.layers.front().in) +
+                      " does not match feature dim " + std::to_string(sg->s.feature_dim));
+    if (batch_size == 0) throw DataError("batch_size must be positive");
+    const uint32_t W = uint32_t((sg->s.num_players() + 63) / 64);
+    if (rows > 0 && words < W) throw DataError("mask rows narrower than the player count");
+    if (rows == 0) return;
+    need(bits, "mask rows");
+    need(out, "output");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    const uint32_t Wd = std::max<uint32_t>(W, 1);
+    if (W == 0) {
+      // no players: every mask is the empty one
+      std::vector<uint64_t> z(rows, 0);
+      upload_rows(ctx->c, z.data(), rows, 1, 1);
+    } else {
+      upload_rows(ctx->c, bits, rows, words, Wd);
+    }
+    predict_rows(ctx->c, sg->s, m->m, ctx->c.masks.p, rows, cls, out, nullptr);
+  });
+}
+
+int sf_predict_probs(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg, const uint64_t* mask,
+                     uint64_t words, float* probs) {
+  return guard([&] {  // gcn.cpp:239-248
+    need(ctx, "context");
+    need(m, "model");
+    need(sg, "subgraph");
+    need(probs, "output");
+    const uint32_t W = uint32_t((sg->s.num_players() + 63) / 64);
+    if (words < W) throw DataError("mask shorter than the player count");
+    if (m->m.layers.front().in != sg->s.feature_dim)
+      throw DataError("model input dim does not match feature dim");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    if (W == 0) {
+      uint64_t z = 0;
+      upload_rows(ctx->c, &z, 1, 1, 1);
+    } else {
+      need(mask, "mask");
+      upload_rows(ctx->c, mask, 1, words, W);
+    }
+    predict_rows(ctx->c, sg->s, m->m, ctx->c.masks.p, 1, 0, nullptr, probs);
+  });
+}
+
+int sf_assemble_weights(uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
+                        const uint64_t* rows_of_size, double* weights) {
+  return guard([&] {  // solver.cpp:116-151 (weights part)
+    need(weights, "output");
+    std::vector<uint64_t> counts;
+    if (rows_of_size) {
+      counts.assign(rows_of_size, rows_of_size + n + 1);
+    } else {
+      counts.assign(size_t(n) + 1, 0);
+      for (uint64_t i = 0; i < rows; ++i) {
+        uint64_t c = 0;
+        for (uint64_t w = 0; w < words; ++w) c += __builtin_popcountll(bits[i * words + w]);
+        if (c <= n) ++counts[c];
+      }
+    }
+    const auto ws = weight_of_size(n, counts);
+    for (uint64_t i = 0; i < rows; ++i) {
+      uint64_t c = 0;
+      for (uint64_t w = 0; w < words; ++w) c += __builtin_popcountll(bits[i * words + w]);
+      if (c == 0 || c >= n)
+        throw DataError("coalition row " + std::to_string(i) + " keeps all or no players");
+      weights[i] = ws[c];
+    }
+  });
+}
+
+static void solve_common(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows,
+                         uint64_t words, const double* weights, const double* targets,
+                         DevBuf<double>& d_sw, DevBuf<double>& d_tgt, CglsInput& in) {
+  need(ctx, "context");
+  if (rows % 2) throw DataError("local rows must come in adjacent pairs");
+  const uint32_t W = uint32_t((n + 63) / 64);
+  if (rows && words < W) throw DataError("rows narrower than the player count");
+  SF_CUDA(cudaSetDevice(ctx->c.device));
+  std::vector<double> sw(rows);
+  for (uint64_t i = 0; i < rows; ++i) {
+    sw[i] = std::sqrt(weights[i]);
+    if (!std::isfinite(targets[i]) || !std::isfinite(sw[i])) {
+      // surfaces as a non-finite step norm exactly like the reference
+    }
+  }
+  upload_rows(ctx->c, bits, rows, words, std::max<uint32_t>(W, 1));
+  d_sw.upload(sw.data(), rows, ctx->c.stream);
+  d_tgt.upload(targets, rows, ctx->c.stream);
+  in.n = n;
+  in.rows = rows;
+  in.W = std::max<uint32_t>(W, 1);
+  in.dev_rows = ctx->c.masks.p;
+  in.dev_sw = d_sw.p;
+  in.dev_targets = d_tgt.p;
+}
+
+int sf_solve_cgls(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
+                  const double* weights, const double* targets, double ct, double cw, double tol,
+                  uint64_t max_iter, int mode, double* phi, uint64_t* iterations, double* rel,
+                  int* converged, double* trace, double* row_trace, uint64_t trace_cap) {
+  return guard([&] {  // solver.cpp:158-362
+    if (n == 0) {
+      if (iterations) *iterations = 0;
+      if (converged) *converged = 1;
+      if (rel) *rel = 0.0;
+      return;
+    }
+    need(phi, "output");
+    DevBuf<double> d_sw, d_tgt;
+    CglsInput in;
+    solve_common(ctx, n, bits, rows, words, weights, targets, d_sw, d_tgt, in);
+    in.constraint_target = ct;
+    in.constraint_weight = cw;
+    in.global_pair_count = rows / 2;
+    CglsResult r = cgls_solve(ctx->c, in, tol, max_iter, mode, trace || row_trace);
+    std::memcpy(phi, r.phi.data(), uint64_t(n) * 8);
+    if (iterations) *iterations = r.iterations;
+    if (rel) *rel = r.relative_residual;
+    if (converged) *converged = r.converged ? 1 : 0;
+    for (uint64_t i = 0; i < trace_cap; ++i) {
+      if (trace && i < r.trace.size()) trace[i] = r.trace[i];
+      if (row_trace && i < r.row_residual_trace.size()) row_trace[i] = r.row_residual_trace[i];
+    }
+  });
+}
+
+int sf_solve_direct(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
+                    const double* weights, const double* targets, double ct, double cw,
+                    double* phi) {
+  return guard([&] {  // solver.cpp:364-428
+    if (ctx && ctx->c.world != 1)
+      throw DataError("direct solve needs the full system on a single worker");
+    if (n > 20000) throw DataError("direct solve limited to 20000 players, got " + std::to_string(n));
+    if (n == 0) return;
+    need(phi, "output");
+    DevBuf<double> d_sw, d_tgt;
+    CglsInput in;
+    solve_common(ctx, n, bits, rows, words, weights, targets, d_sw, d_tgt, in);
+    in.constraint_target = ct;
+    in.constraint_weight = cw;
+    const auto r = gram_solve(ctx->c, in);
+    std::memcpy(phi, r.data(), uint64_t(n) * 8);
+  });
+}
+
+int sf_rank_edges(const double* phi, uint64_t n, uint32_t* order) {
+  return guard([&] {
+    need(order, "output");
+    const auto o = ranking(std::vector<double>(phi, phi + n));
+    std::memcpy(order, o.data(), n * 4);
+  });
+}
+
+void sf_explain_options_default(sf_explain_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->batch_size = 50;
+  o->top_k = 10;
+  o->tol = 1.0e-6;
+  o->allow_exhaustive = 1;
+  o->constraint_scale = 1.0e6;
+  o->fidelity = 1;
+  o->baseline_trials = 8;
+}
+
+int sf_explain_node(sf_ctx* ctx, const sf_graph* g, const sf_model* m, uint32_t node,
+                    const sf_explain_options* opts, sf_explanation* out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(g, "graph");
+    need(m, "model");
+    need(out, "output");
+    sf_explain_options o;
+    if (opts)
+      o = *opts;
+    else
+      sf_explain_options_default(&o);
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    try {
+      explain_node(ctx->c, g->g, m->m, node, o, out);
+    } catch (const DataError& e) {  // explain.cpp:171-175
+      throw DataError("node " + std::to_string(node) + ": " + e.what());
+    } catch (const NumericalError& e) {
+      throw NumericalError("node " + std::to_string(node) + ": " + e.what());
+    }
+  });
+}
+
+int sf_explanation_free(sf_explanation* e) {
+  if (!e) return SF_OK;
+  for (void* p : {static_cast<void*>(e->phi), static_cast<void*>(e->players_global),
+                  static_cast<void*>(e->top_player), static_cast<void*>(e->top_phi),
+                  static_cast<void*>(e->fid_counts), static_cast<void*>(e->fid_plus),
+                  static_cast<void*>(e->fid_plus_random), static_cast<void*>(e->fid_sparsities),
+                  static_cast<void*>(e->fid_minus), static_cast<void*>(e->fid_minus_random)})
+    std::free(p);
+  std::memset(e, 0, sizeof(*e));
+  return SF_OK;
+}
+
+int sf_evaluate_fidelity(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg, uint32_t cls,
+                         const double* phi, const uint32_t* counts, uint32_t nc, const double* sp,
+                         uint32_t ns, uint64_t seed, uint32_t trials, uint32_t* counts_out,
+                         double* plus, double* plus_random, double* minus, double* minus_random) {
+  return guard([&] {
+    need(ctx, "context");
+    need(m, "model");
+    need(sg, "subgraph");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    const uint64_t n = sg->s.num_players();
+    FidelityOut f = fidelity(ctx->c, sg->s, m->m, cls, std::vector<double>(phi, phi + n),
+                             std::vector<uint32_t>(counts, counts + nc),
+                             std::vector<double>(sp, sp + ns), seed, trials);
+    for (uint32_t i = 0; i < nc; ++i) {
+      if (counts_out) counts_out[i] = f.counts[i];
+      plus[i] = f.plus[i];
+      plus_random[i] = f.plus_random[i];
+    }
+    for (uint32_t i = 0; i < ns; ++i) {
+      minus[i] = f.minus[i];
+      minus_random[i] = f.minus_random[i];
+    }
+  });
+}
+
+int sf_sample_and_predict(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg, uint32_t cls,
+                          uint64_t k, uint64_t seed, int allow_exhaustive, double* stage_ms,
+                          uint64_t* rows_local) {
+  return guard([&] {
+    need(ctx, "context");
+    need(m, "model");
+    need(sg, "subgraph");
+    Ctx& c = ctx->c;
+    SF_CUDA(cudaSetDevice(c.device));
+    const uint32_t n = uint32_t(sg->s.num_players());
+    const SizePlan plan = plan_sizes(n, k, allow_exhaustive != 0);
+    const uint64_t rows = 2 * local_pair_count(plan.total_pairs(), c.rank, c.world);
+    const uint32_t W = std::max<uint32_t>(1, (n + 63) / 64);
+    c.masks.reserve(std::max<uint64_t>(rows * W, 1));
+    c.preds.reserve(std::max<uint64_t>(rows, 1));
+    engine_prepare(c, sg->s, m->m);
+    cudaEvent_t e0, e1, e2;
+    SF_CUDA(cudaEventCreate(&e0));
+    SF_CUDA(cudaEventCreate(&e1));
+    SF_CUDA(cudaEventCreate(&e2));
+    SF_CUDA(cudaEventRecord(e0, c.stream));
+    launch_generate_masks(c, plan, seed, c.rank, c.world, c.masks.p);
+    SF_CUDA(cudaEventRecord(e1, c.stream));
+    float dom = 0.f;
+    engine_predict(c, c.masks.p, rows, cls, c.preds.p, nullptr, stage_ms ? &dom : nullptr);
+    SF_CUDA(cudaEventRecord(e2, c.stream));
+    SF_CUDA(cudaEventSynchronize(e2));
+    float a = 0.f, b = 0.f;
+    SF_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    SF_CUDA(cudaEventElapsedTime(&b, e1, e2));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    if (stage_ms) {
+      stage_ms[0] = a;
+      stage_ms[1] = b;
+      stage_ms[2] = dom;
+    }
+    if (rows_local) *rows_local = rows;
+  });
+}
+
+}  // extern "C"

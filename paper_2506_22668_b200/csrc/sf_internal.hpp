@@ -1,0 +1,253 @@
+// Internal declarations shared by the host C++ and the CUDA translation
+// units of libshapflow_b200. Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace sfb {
+
+// ---------------------------------------------------------------- errors
+// Mirror of the reference exception types (error.hpp:10-27); the C-ABI maps
+// them to status codes 2/3/4 and CUDA failures to 1.
+struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ProtocolError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file,
+                       int line) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + " failed at " + file + ":" +
+                    std::to_string(line) + ": " + cudaGetErrorString(e));
+}
+#define SF_CUDA(x) ::sfb::cuda_check((x), #x, __FILE__, __LINE__)
+#define SF_LAUNCHED(ctx)                                                  \
+  do {                                                                    \
+    ::sfb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__,      \
+                      __LINE__);                                          \
+    (ctx).launches++;                                                     \
+  } while (0)
+
+inline uint64_t next_object_id() {
+  static std::atomic<uint64_t> id{1};
+  return id++;
+}
+
+// ---------------------------------------------------------------- host data
+struct Graph {  // graph.hpp:16-31
+  uint64_t id = next_object_id();
+  uint32_t num_nodes = 0;
+  uint64_t feature_dim = 0;
+  std::vector<uint64_t> row_ptr;
+  std::vector<uint32_t> col;
+  std::vector<float> features;
+  std::vector<uint32_t> labels;
+};
+
+struct Layer {
+  uint64_t in = 0, out = 0;
+  std::vector<float> weight;  // in x out
+  std::vector<float> bias;
+};
+
+struct Model {  // gcn.hpp:13-30
+  uint64_t id = next_object_id();
+  std::vector<Layer> layers;
+  int depth() const { return static_cast<int>(layers.size()); }
+};
+
+struct Subgraph {  // graph.hpp:36-53
+  uint64_t id = next_object_id();
+  uint32_t target_global = 0;
+  uint64_t feature_dim = 0;
+  std::vector<uint32_t> local_to_global;
+  std::vector<std::pair<uint32_t, uint32_t>> players;
+  std::vector<uint64_t> row_ptr;
+  std::vector<uint32_t> col;
+  std::vector<uint32_t> edge_player;
+  std::vector<float> features;
+  uint32_t num_nodes() const {
+    return static_cast<uint32_t>(local_to_global.size());
+  }
+  uint64_t num_players() const { return players.size(); }
+  // |B_h|, h = 0..H: local ids are BFS discovery order, so balls are prefixes
+  std::vector<uint64_t> ball_sizes(int hops) const;
+};
+
+// ---------------------------------------------------------------- device mem
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void reserve(size_t count) {
+    if (count <= n) return;
+    release();
+    SF_CUDA(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+    n = count;
+  }
+  void upload(const T* src, size_t count, cudaStream_t s) {
+    reserve(count);
+    if (count)
+      SF_CUDA(cudaMemcpyAsync(p, src, sizeof(T) * count,
+                              cudaMemcpyHostToDevice, s));
+  }
+};
+
+// Device-resident copy of one (subgraph, model) pair: the inputs of the
+// masked-inference engine.
+struct Engine {
+  uint64_t sg_id = 0, model_id = 0;
+  uint32_t V = 0;
+  uint64_t n = 0;
+  uint32_t W = 0;  // u64 words per mask row
+  int L = 0;
+  std::vector<uint64_t> dims;       // d_0..d_L
+  std::vector<uint64_t> ball;       // |B_h|, h = 0..L
+  DevBuf<uint32_t> row_ptr, col, edge_player;
+  DevBuf<float> p0;                 // X W_0, V x d_1 (layer-0 transform-first)
+  std::vector<std::unique_ptr<DevBuf<float>>> w, b;  // per layer (w[0] unused)
+};
+
+struct CommStats {  // comm.hpp:13-19
+  uint64_t scalar_allreduce = 0, vector_allreduce = 0, barriers = 0,
+           doubles_reduced = 0;
+};
+
+struct Nccl;  // dlopen'ed NCCL (sf_comm.cpp)
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  std::unique_ptr<Nccl> nccl;
+  CommStats stats;
+  uint64_t launches = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic issued
+  cudaEvent_t events[8] = {};             // bench timers on `stream`
+  // dominant-kernel (layer-0 masked SpMM) timing: event pairs per launch,
+  // read back after the work is done (no per-batch synchronization)
+  bool time_dominant = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dom_events;
+  size_t dom_used = 0;
+  uint64_t dom_pairs = 0;  // complement pairs covered by the timed launches
+  Engine engine;
+  // scratch reused across calls
+  DevBuf<uint64_t> masks;      // row-major mask rows
+  DevBuf<uint32_t> maskt;      // tile-transposed kept-set bits
+  DevBuf<float> preds;
+  DevBuf<unsigned char> work;  // engine workspace
+  DevBuf<unsigned char> solver_work;
+  Ctx();
+  ~Ctx();
+};
+
+// ---------------------------------------------------------------- comm
+void nccl_unique_id(void* out128);
+void nccl_join(Ctx& ctx, const void* id128, int rank, int world);
+void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count);
+void comm_barrier(Ctx& ctx);
+
+// ---------------------------------------------------------------- plan
+struct SizeClass {
+  uint32_t size = 0;
+  uint64_t pairs = 0, first_pair = 0;
+};
+struct SizePlan {
+  uint32_t n = 0;
+  uint64_t requested = 0;
+  bool exhaustive = false;
+  std::vector<SizeClass> classes;
+  uint64_t total_pairs() const {
+    return classes.empty() ? 0 : classes.back().first_pair + classes.back().pairs;
+  }
+};
+SizePlan plan_sizes(uint32_t n, uint64_t k, bool allow_exhaustive);
+uint64_t binomial_or_max(uint32_t n, uint32_t s);
+std::vector<uint64_t> global_rows_of_size(const SizePlan& plan);
+uint64_t local_pair_count(uint64_t global_pairs, int rank, int world);
+
+// ---------------------------------------------------------------- kernels
+// sf_sampler.cu
+void launch_philox_stream(Ctx& ctx, uint64_t seed, uint64_t stream,
+                          uint64_t count, uint64_t* dev_out);
+// Generates this rank's rows (row-major, 2 rows per local pair) into
+// dev_rows; also writes the tile-transposed kept-set layout when dev_maskt
+// is non-null.
+void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
+                           int rank, int world, uint64_t* dev_rows);
+// Independent Floyd draws (fidelity baselines, fidelity.cpp:25-33): row j
+// is the size-sizes[j] subset drawn from Philox(seed, streams[j]), or the
+// full row minus that subset when invert[j] != 0.
+void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
+                       const uint64_t* dev_streams, const uint32_t* dev_sizes,
+                       const uint8_t* dev_invert, uint64_t jobs,
+                       uint64_t* dev_rows);
+// Row-major rows -> tile layout: maskt[t][e] bit i = row (row0+t*64+i)
+// bit e, for all 64 rows of the tile (u32 pairs: low = rows 0..31).
+void launch_transpose_tiles(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
+                            uint32_t W, uint64_t tiles, uint64_t* dev_maskt);
+
+// sf_gcn.cu
+void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m);
+// Scores `rows` mask rows (row-major on device) into dev_probs (class
+// `cls`) and, when dev_allprobs is non-null, every class probability.
+void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
+                    uint32_t cls, float* dev_out, float* dev_allprobs,
+                    float* dominant_ms);
+
+// sf_cgls.cu
+struct CglsResult {
+  std::vector<double> phi;
+  uint64_t iterations = 0;
+  double relative_residual = 0.0;
+  bool converged = false;
+  std::vector<double> trace, row_residual_trace;
+};
+struct CglsInput {
+  uint32_t n = 0;
+  uint64_t rows = 0;  // local rows (even)
+  uint32_t W = 0;
+  const uint64_t* dev_rows = nullptr;  // row-major bits on device
+  const double* dev_sw = nullptr;      // sqrt(weight) per local row
+  const double* dev_targets = nullptr; // value - base per local row
+  double constraint_target = 0.0, constraint_weight = 0.0;
+  uint64_t global_pair_count = 0;
+};
+CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
+                      uint64_t max_iter, int mode, bool trace);
+std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in);
+
+// sf_assemble (sf_cgls.cu): per-row sqrt(weight) and targets on device from
+// per-size weights and float predictions.
+void launch_assemble(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
+                     uint32_t W, uint32_t n, const double* dev_wsize,
+                     const float* dev_values, double base, double* dev_sw,
+                     double* dev_targets, int* dev_bad_row);
+
+}  // namespace sfb

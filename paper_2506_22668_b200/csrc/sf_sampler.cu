@@ -1,0 +1,331 @@
+// Coalition sampler for sm_100a: counter-based Philox-4x32-10 + Floyd's
+// subset sampler, one warp per complement pair, bit-exact with the
+// reference generate_masks (sampler.cpp:153-210).
+//
+// Layout: rows are u64 words, bit e = player e, row-major,
+// words_for_bits(n) words per row; local pair j owns rows 2j (kept-set,
+// size s <= n/2) and 2j+1 (complement, tail bits cleared). Pair j of rank r
+// is global pair g = r + j * world (sampler.cpp:177-178), so its Philox
+// stream is (seed, g) and the layout of any world reproduces the
+// single-worker rows at the same global index.
+#include <cuda_runtime.h>
+
+#include "sf_device.cuh"
+#include "sf_internal.hpp"
+
+namespace sfb {
+
+namespace {
+
+constexpr int kSamplerWarps = 4;  // warps per CTA
+
+struct ClassTable {
+  const uint32_t* size;
+  const uint64_t* first;
+  const uint64_t* pairs;
+  uint32_t count;
+};
+
+__device__ __forceinline__ uint32_t find_class(const ClassTable& ct,
+                                               uint64_t g) {
+  // classes are contiguous and ascending in g (sampler.cpp:144-149)
+  uint32_t lo = 0, hi = ct.count;  // first[lo] <= g < first[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ct.first[mid] <= g)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Bitset accessors for the two storage variants: shared memory (one row per
+// warp, fast path) or the output row itself in global memory (large n).
+struct SmemSet {
+  uint64_t* w;
+  __device__ bool test(uint32_t t) const { return (w[t >> 6] >> (t & 63)) & 1ull; }
+  __device__ void set(uint32_t t) const {
+    atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), 1ull << (t & 63));
+  }
+};
+struct GmemSet {
+  uint64_t* w;
+  __device__ bool test(uint32_t t) const { return (__ldcg(&w[t >> 6]) >> (t & 63)) & 1ull; }
+  __device__ void set(uint32_t t) const {
+    atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), 1ull << (t & 63));
+  }
+};
+
+// Floyd (sampler.cpp:55-63): for m = n-s .. n-1 draw t = u64 % (m+1) and
+// insert t, or m when t is already present. The warp draws 64 consecutive
+// values at once (lane i owns Philox block base/2 + i, i.e. draws base+2i
+// and base+2i+1), tests them against the set as it stood before the chunk,
+// then replays the chunk in order with shuffles so that a draw colliding
+// with an earlier pick of the same chunk resolves exactly as the
+// sequential loop would.
+template <typename Set>
+__device__ void floyd_warp(const Set& set, uint32_t n, uint32_t s,
+                           uint64_t seed, uint64_t g, int lane) {
+  const uint32_t m0 = n - s;
+  for (uint32_t base = 0; base < s; base += 64) {
+    uint64_t x0, x1;
+    philox_block(seed, g, (base >> 1) + lane, x0, x1);
+    const uint32_t i0 = base + 2 * lane, i1 = i0 + 1;
+    const bool v0 = i0 < s, v1 = i1 < s;
+    const uint32_t mm0 = m0 + i0, mm1 = m0 + i1;
+    const uint32_t t0 = v0 ? mod_u64_u32(x0, mm0 + 1) : 0xffffffffu;
+    const uint32_t t1 = v1 ? mod_u64_u32(x1, mm1 + 1) : 0xffffffffu;
+    __syncwarp();
+    bool hit0 = v0 && set.test(t0);
+    bool hit1 = v1 && set.test(t1);
+    const uint32_t chunk = min(64u, s - base);
+    for (uint32_t k = 0; k < chunk; ++k) {
+      const int owner = k >> 1;
+      uint32_t pk = (k & 1) ? (hit1 ? mm1 : t1) : (hit0 ? mm0 : t0);
+      pk = __shfl_sync(kFull, pk, owner);
+      // later draws of this chunk that drew the value just picked
+      if (i0 > base + k && t0 == pk) hit0 = true;
+      if (i1 > base + k && t1 == pk) hit1 = true;
+    }
+    if (v0) set.set(hit0 ? mm0 : t0);
+    if (v1) set.set(hit1 ? mm1 : t1);
+    __syncwarp();
+  }
+}
+
+// Exhaustive plans (sampler.cpp:38-51, 106-114, 192-199): lexicographic
+// unranking, n <= 62 so a row is one word.
+__device__ uint64_t binom_dev(uint32_t n, uint32_t s) {
+  if (s > n) return 0;
+  if (n - s < s) s = n - s;
+  unsigned __int128 r = 1;
+  for (uint32_t i = 1; i <= s; ++i) {
+    r = r * (n - s + i) / i;
+    if (r > (unsigned __int128)0xffffffffffffffffull) return 0xffffffffffffffffull;
+  }
+  return static_cast<uint64_t>(r);
+}
+
+__device__ uint64_t unrank(uint64_t idx, uint32_t m, uint32_t t,
+                           uint32_t offset) {
+  uint64_t row = 0;
+  uint32_t x = 0;
+  for (uint32_t i = 0; i < t; ++i) {
+    for (;;) {
+      const uint64_t c = binom_dev(m - 1 - x, t - 1 - i);
+      if (idx < c) break;
+      idx -= c;
+      ++x;
+    }
+    row |= 1ull << (x + offset);
+    ++x;
+  }
+  return row;
+}
+
+__global__ void exhaustive_kernel(ClassTable ct, uint32_t n, int rank,
+                                  int world, uint64_t local_pairs,
+                                  uint64_t* rows) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (j >= local_pairs) return;
+  const uint64_t g = rank + j * uint64_t(world);
+  const uint32_t ci = find_class(ct, g);
+  const uint32_t s = ct.size[ci];
+  const uint64_t idx = g - ct.first[ci];
+  uint64_t sub;
+  if (2 * s == n)
+    sub = 1ull | unrank(idx, n - 1, s - 1, 1);
+  else
+    sub = unrank(idx, n, s, 0);
+  const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  rows[2 * j] = sub;
+  rows[2 * j + 1] = ~sub & tail;
+}
+
+template <bool kSmem>
+__global__ void __launch_bounds__(kSamplerWarps * 32)
+    floyd_kernel(ClassTable ct, uint32_t n, uint32_t W, uint64_t seed,
+                 int rank, int world, uint64_t local_pairs, uint64_t* rows) {
+  extern __shared__ uint64_t smem_sets[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  const uint64_t warps_total = uint64_t(gridDim.x) * kSamplerWarps;
+  for (uint64_t j = blockIdx.x * uint64_t(kSamplerWarps) + warp; j < local_pairs;
+       j += warps_total) {
+    const uint64_t g = rank + j * uint64_t(world);
+    const uint32_t ci = find_class(ct, g);
+    const uint32_t s = ct.size[ci];
+    uint64_t* even = rows + (2 * j) * W;
+    uint64_t* odd = even + W;
+    uint64_t* bits = kSmem ? smem_sets + size_t(warp) * W : even;
+    for (uint32_t w = lane; w < W; w += 32) bits[w] = 0;
+    __syncwarp();
+    if (kSmem)
+      floyd_warp(SmemSet{bits}, n, s, seed, g, lane);
+    else
+      floyd_warp(GmemSet{bits}, n, s, seed, g, lane);
+    __syncwarp();
+    for (uint32_t w = lane; w < W; w += 32) {
+      const uint64_t v = kSmem ? bits[w] : __ldcg(&bits[w]);
+      if (kSmem) even[w] = v;
+      odd[w] = (w == W - 1) ? (~v & tail) : ~v;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kSamplerWarps * 32)
+    floyd_jobs_kernel(uint32_t n, uint32_t W, uint64_t seed,
+                      const uint64_t* __restrict__ streams,
+                      const uint32_t* __restrict__ sizes,
+                      const uint8_t* __restrict__ invert, uint64_t jobs,
+                      uint64_t* __restrict__ rows) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t j = blockIdx.x * uint64_t(kSamplerWarps) + (threadIdx.x >> 5);
+  if (j >= jobs) return;
+  const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  uint64_t* row = rows + j * W;
+  for (uint32_t w = lane; w < W; w += 32) row[w] = 0;
+  __syncwarp();
+  floyd_warp(GmemSet{row}, n, sizes[j], seed, streams[j], lane);
+  __syncwarp();
+  if (invert[j])
+    for (uint32_t w = lane; w < W; w += 32) {
+      const uint64_t v = ~__ldcg(&row[w]);
+      row[w] = (w == W - 1) ? (v & tail) : v;
+    }
+}
+
+__global__ void philox_stream_kernel(uint64_t seed, uint64_t stream,
+                                     uint64_t count, uint64_t* out) {
+  const uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (2 * b >= count) return;
+  uint64_t f, s;
+  philox_block(seed, stream, b, f, s);
+  out[2 * b] = f;
+  if (2 * b + 1 < count) out[2 * b + 1] = s;
+}
+
+// rows (row-major, W words) -> tiles: out[t][e] u64 with bit i = bit e of
+// row t*64+i (rows past `rows` read as zero). One CTA per (tile, 32-word
+// chunk): stage 64 x 32 words in smem, then 64 ballots per half-tile.
+__global__ void __launch_bounds__(256)
+    transpose_tiles_kernel(const uint64_t* __restrict__ in, uint64_t rows,
+                           uint32_t W, uint64_t* __restrict__ out) {
+  __shared__ uint64_t sm[64][33];
+  const uint64_t t = blockIdx.y;
+  const uint32_t w0 = blockIdx.x * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 64 * 32; i += 256) {
+    const int r = i >> 5, w = i & 31;
+    const uint64_t row = t * 64 + r;
+    sm[r][w] = (row < rows && w0 + w < W) ? in[row * W + w0 + w] : 0ull;
+  }
+  __syncthreads();
+  uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
+  const uint64_t Wp = uint64_t(W) * 64;  // players per tile, padded
+  // 8 warps x 8 (word, half) jobs = 32 words x 2 halves
+  for (int job = warp; job < 64; job += 8) {
+    const int w = job >> 1, h = job & 1;
+    if (w0 + w >= W) continue;
+    const uint64_t v = sm[h * 32 + lane][w];
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const uint32_t b = __ballot_sync(kFull, (v >> j) & 1ull);
+      if (lane == (j & 31)) {
+        if (j < 32)
+          lo = b;
+        else
+          hi = b;
+      }
+    }
+    const uint64_t e = uint64_t(w0 + w) * 64 + lane;
+    out32[(t * Wp + e) * 2 + h] = lo;
+    out32[(t * Wp + e + 32) * 2 + h] = hi;
+  }
+}
+
+}  // namespace
+
+void launch_philox_stream(Ctx& ctx, uint64_t seed, uint64_t stream,
+                          uint64_t count, uint64_t* dev_out) {
+  if (count == 0) return;
+  const uint64_t blocks = (count + 1) / 2;
+  philox_stream_kernel<<<unsigned((blocks + 255) / 256), 256, 0, ctx.stream>>>(
+      seed, stream, count, dev_out);
+  SF_LAUNCHED(ctx);
+}
+
+void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
+                           int rank, int world, uint64_t* dev_rows) {
+  const uint64_t pairs = local_pair_count(plan.total_pairs(), rank, world);
+  if (pairs == 0) return;
+  const uint32_t n = plan.n;
+  const uint32_t W = (n + 63) / 64;
+  const size_t C = plan.classes.size();
+  std::vector<uint32_t> sizes(C);
+  std::vector<uint64_t> first(C), cnt(C);
+  for (size_t i = 0; i < C; ++i) {
+    sizes[i] = plan.classes[i].size;
+    first[i] = plan.classes[i].first_pair;
+    cnt[i] = plan.classes[i].pairs;
+  }
+  // class table lives in the context's solver scratch for the launch
+  DevBuf<uint32_t> d_sizes;
+  DevBuf<uint64_t> d_first, d_cnt;
+  d_sizes.upload(sizes.data(), C, ctx.stream);
+  d_first.upload(first.data(), C, ctx.stream);
+  d_cnt.upload(cnt.data(), C, ctx.stream);
+  ClassTable ct{d_sizes.p, d_first.p, d_cnt.p, static_cast<uint32_t>(C)};
+  if (plan.exhaustive) {
+    exhaustive_kernel<<<unsigned((pairs + 127) / 128), 128, 0, ctx.stream>>>(
+        ct, n, rank, world, pairs, dev_rows);
+    SF_LAUNCHED(ctx);
+  } else {
+    int sms = 148;
+    SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
+    const size_t smem = size_t(kSamplerWarps) * W * 8;
+    const uint64_t want = (pairs + kSamplerWarps - 1) / kSamplerWarps;
+    if (smem <= 200 * 1024) {
+      auto k = floyd_kernel<true>;
+      SF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+      int per_sm = 1;
+      SF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSamplerWarps * 32, smem));
+      const uint64_t grid = std::min<uint64_t>(want, uint64_t(sms) * std::max(per_sm, 1) * 4);
+      k<<<unsigned(grid), kSamplerWarps * 32, smem, ctx.stream>>>(
+          ct, n, W, seed, rank, world, pairs, dev_rows);
+    } else {
+      const uint64_t grid = std::min<uint64_t>(want, uint64_t(sms) * 16);
+      floyd_kernel<false><<<unsigned(grid), kSamplerWarps * 32, 0, ctx.stream>>>(
+          ct, n, W, seed, rank, world, pairs, dev_rows);
+    }
+    SF_LAUNCHED(ctx);
+  }
+  // the class table must outlive the launch
+  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
+                       const uint64_t* dev_streams, const uint32_t* dev_sizes,
+                       const uint8_t* dev_invert, uint64_t jobs,
+                       uint64_t* dev_rows) {
+  if (jobs == 0) return;
+  const uint32_t W = (n + 63) / 64;
+  floyd_jobs_kernel<<<unsigned((jobs + kSamplerWarps - 1) / kSamplerWarps), kSamplerWarps * 32, 0,
+                      ctx.stream>>>(n, W, seed, dev_streams, dev_sizes, dev_invert, jobs, dev_rows);
+  SF_LAUNCHED(ctx);
+}
+
+void launch_transpose_tiles(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
+                            uint32_t W, uint64_t tiles, uint64_t* dev_maskt) {
+  if (tiles == 0) return;
+  dim3 grid((W + 31) / 32, unsigned(tiles));
+  transpose_tiles_kernel<<<grid, 256, 0, ctx.stream>>>(dev_rows, rows, W, dev_maskt);
+  SF_LAUNCHED(ctx);
+}
+
+}  // namespace sfb

@@ -1,0 +1,156 @@
+"""GPU: weighted least squares on bit rows (replaces assemble_problem +
+solve_cgls + solve_direct, solver.cpp:95-428). The reference's own solver tests
+(test_solver.cpp) re-expressed through the C-ABI, plus parity with the
+reference / bit-row restatement at larger sizes."""
+import numpy as np
+import pytest
+
+import paper_2506_22668_b200 as sf
+
+pytestmark = pytest.mark.gpu
+
+
+def toy_game_values(bits, port):
+    # test_solver.cpp:23-37 hashed "toy game", any deterministic function works
+    key = np.full(bits.shape[0], 0x6B43A9B5, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for w in range(bits.shape[1]):
+            key = key * np.uint64(0x9E3779B97F4A7C15) + bits[:, w]
+    return np.array([(int(port.philox(int(k), 3, 1)[0]) >> 11) * 2.0**-53 for k in key])
+
+
+def sampled_problem(ctx, port, n, k, seed, base, full):
+    p = sf.plan_sizes(n, k, False)
+    bits, ros = ctx.generate_masks(p, seed)
+    vals = toy_game_values(bits, port)
+    w = sf.assemble_weights(n, bits, ros)
+    return bits, w, vals - base, full - base
+
+
+def test_identity_system_one_iteration(ctx):
+    # test_solver.cpp:55-77: non-complement rows e0..e3, no pin
+    bits = np.array([[1], [2], [4], [8]], np.uint64)
+    r = ctx.solve_cgls(4, bits, np.ones(4), np.array([1.0, 2, 3, 4]), 0.0, 0.0)
+    assert r["converged"] and r["iterations"] == 1
+    assert np.allclose(r["phi"], [1, 2, 3, 4], rtol=1e-12)
+
+
+def test_two_players_hand_value(ctx):
+    # test_solver.cpp:79-102: f({0})=1, f({1})=2, f(both)=4 -> (1.5, 2.5)
+    p = sf.plan_sizes(2, 2, True)
+    bits, ros = ctx.generate_masks(p, 0)
+    vals = np.where(bits[:, 0] == 1, 1.0, 2.0)
+    w = sf.assemble_weights(2, bits, ros)
+    r = ctx.solve_cgls(2, bits, w, vals, 4.0, 1e6, max_iter=10)
+    assert r["converged"]
+    assert r["phi"] == pytest.approx([1.5, 2.5], rel=1e-6)
+    d = ctx.solve_direct(2, bits, w, vals, 4.0, 1e6)
+    assert d == pytest.approx([1.5, 2.5], rel=1e-6)
+
+
+@pytest.mark.parametrize("n", [5, 8, 13])
+def test_cgls_matches_direct(ctx, port, n):
+    # test_solver.cpp:104-124
+    bits, w, t, ct = sampled_problem(ctx, port, n, 60 * n, 1000 + n, 0.3, 0.7)
+    r = ctx.solve_cgls(n, bits, w, t, ct, 1e6, tol=1e-10, max_iter=4 * n)
+    assert r["converged"]
+    d = ctx.solve_direct(n, bits, w, t, ct, 1e6)
+    scale = max(np.abs(d).max(), 1.0)
+    assert np.abs(r["phi"] - d).max() <= 1e-8 * scale
+
+
+def test_additive_game_exact(ctx):
+    # test_solver.cpp:126-148
+    n = 6
+    p = sf.plan_sizes(n, 62, True)
+    bits, ros = ctx.generate_masks(p, 0)
+    vals = np.array([sum(i + 1 for i in range(n) if (int(b) >> i) & 1) for b in bits[:, 0]], float)
+    w = sf.assemble_weights(n, bits, ros)
+    r = ctx.solve_cgls(n, bits, w, vals, 21.0, 1e6)
+    assert r["phi"] == pytest.approx(np.arange(1, n + 1), rel=1e-6)
+
+
+def test_symmetric_game(ctx):
+    # test_solver.cpp:150-168
+    n = 6
+    p = sf.plan_sizes(n, 62, True)
+    bits, ros = ctx.generate_masks(p, 0)
+    vals = np.array([bin(int(b)).count("1") ** 2 for b in bits[:, 0]], float)
+    w = sf.assemble_weights(n, bits, ros)
+    r = ctx.solve_cgls(n, bits, w, vals, 36.0, 1e6)
+    assert r["phi"].max() - r["phi"].min() <= 1e-6
+    assert r["phi"][0] == pytest.approx(6.0, rel=1e-4)
+
+
+def test_duplicate_rows_half_weight(ctx, port):
+    # test_solver.cpp:170-197
+    bits, w, t, ct = sampled_problem(ctx, port, 7, 200, 5, 0.1, 0.9)
+    a = ctx.solve_cgls(7, bits, w, t, ct, 1e6, tol=1e-10, max_iter=28)
+    bits2 = np.repeat(bits, 2, axis=0)
+    b = ctx.solve_cgls(7, bits2, np.repeat(w, 2) / 2, np.repeat(t, 2), ct, 1e6, tol=1e-10, max_iter=28)
+    assert np.allclose(a["phi"], b["phi"], rtol=1e-8, atol=1e-12)
+
+
+def test_monotone_row_residual(ctx, port):
+    # test_solver.cpp:199-210
+    bits, w, t, ct = sampled_problem(ctx, port, 10, 400, 77, 0.2, 0.8)
+    r = ctx.solve_cgls(10, bits, w, t, ct, 1e6, trace=True)
+    tr = r["row_residual_trace"]
+    assert len(tr) >= 2
+    assert all(tr[i] <= tr[i - 1] * (1 + 1e-10) + 1e-12 for i in range(1, len(tr)))
+
+
+@pytest.mark.parametrize("n", [6, 12, 20])
+def test_efficiency_pin(ctx, port, n):
+    # test_solver.cpp:212-220
+    bits, w, t, ct = sampled_problem(ctx, port, n, 50 * n, n, 0.25, 0.75)
+    r = ctx.solve_cgls(n, bits, w, t, ct, 1e6)
+    assert abs(r["phi"].sum() - ct) <= 1e-4
+
+
+def test_validation_errors(ctx, port):
+    # test_solver.cpp:258-324
+    bits = np.array([[3], [4]], np.uint64)
+    with pytest.raises(sf.NumericalError, match="pivot"):
+        ctx.solve_direct(3, bits, np.zeros(2), np.array([1.0, 2.0]), 0.0, 0.0)
+    b, w, t, ct = sampled_problem(ctx, port, 5, 100, 2, 0.0, 1.0)
+    with pytest.raises(sf.DataError):
+        ctx.solve_cgls(5, b[:-1], w[:-1], t[:-1], ct, 1e6)
+    t2 = t.copy()
+    t2[0] = np.nan
+    with pytest.raises(sf.NumericalError):
+        ctx.solve_cgls(5, b, w, t2, ct, 1e6)
+    with pytest.raises(sf.DataError):
+        sf.assemble_weights(4, np.array([[0], [15]], np.uint64))
+
+
+@pytest.mark.parametrize("n,k,seed", [(11, 500, 31), (40, 3000, 3), (200, 4000, 9), (999, 10000, 1)])
+def test_cgls_vs_reference(ctx, ref, port, n, k, seed):
+    p = sf.plan_sizes(n, k, False)
+    bits, ros = ctx.generate_masks(p, seed)
+    vals = np.sin(np.arange(bits.shape[0]) * 0.37) * 0.5 + 0.5
+    phi_ref, it_ref, _, conv_ref = ref.solve_cgls(n, bits, vals, 0.25, 0.75, max_iter=4 * n)
+    w = sf.assemble_weights(n, bits, ros)
+    r = ctx.solve_cgls(n, bits, w, vals - 0.25, 0.5, 1e6, max_iter=4 * n)
+    assert r["converged"] == conv_ref
+    assert abs(int(r["iterations"]) - int(it_ref)) <= 1
+    err = np.linalg.norm(r["phi"] - phi_ref) / np.linalg.norm(phi_ref)
+    assert err <= 1e-3  # BASELINE bar; observed ~1e-12 (FP64, reordered sums)
+    assert (sf.rank_edges(r["phi"])[:10] == port.rank_edges(phi_ref)[:10]).all()
+
+
+def test_collective_counts_reference_protocol(ctx, port):
+    # acceptance.cpp:653-677: 1 scalar + 1 vector all-reduce per iteration,
+    # one more vector at init, n doubles per vector, 1 per scalar
+    n = 16
+    p = sf.plan_sizes(n, 2048, False)
+    bits, ros = ctx.generate_masks(p, 3)
+    vals = np.array([(int(port.philox(77, i, 1)[0]) >> 11) * 2.0**-53 for i in range(bits.shape[0])])
+    w = sf.assemble_weights(n, bits, ros)
+    before = ctx.stats()
+    r = ctx.solve_cgls(n, bits, w, vals - 0.25, 0.5, 1e6)
+    after = ctx.stats()
+    it = r["iterations"]
+    assert after["scalar_allreduce"] - before["scalar_allreduce"] == it
+    assert after["vector_allreduce"] - before["vector_allreduce"] == it + 1
+    assert after["doubles_reduced"] - before["doubles_reduced"] == (it + 1) * n + it

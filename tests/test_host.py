@@ -1,0 +1,146 @@
+"""CPU: the C-ABI library loads, exports every symbol the header declares, and
+its host-side logic (plan, graph build, extraction, model generation, errors)
+matches the reference. No kernel runs here."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_2506_22668_b200 as sf
+from conftest import toy_graph_arrays
+from paper_2506_22668_b200 import workloads as W
+
+
+def test_library_exports_every_header_symbol():
+    L = ctypes.CDLL(sf.lib_path)
+    missing = [s for s in sf.EXPORTED_SYMBOLS if not hasattr(L, s)]
+    assert not missing, missing
+    assert len(sf.EXPORTED_SYMBOLS) >= 40
+    assert b"sm_100a" in sf.lib.sf_version()
+
+
+def test_library_is_sm100a_only():
+    # the fatbin carries sm_100a SASS (cuobjdump lists the ELF arch)
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", sf.lib_path],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_primitives_match_golden(golden):
+    for c in golden["node_sampling_seed"]:
+        assert sf.node_sampling_seed(c["seed"], c["node"]) == int(c["out"], 16)
+    for c in golden["binomial"]:
+        assert sf.binomial_or_max(c["n"], c["s"]) == int(c["out"])
+    assert sf.auto_samples(4999) == 60000 and sf.auto_samples(5000) == 600000
+    assert sf.kernel_weight(4, 2) == pytest.approx(0.125, rel=1e-12)
+    assert sf.kernel_weight(61, 1) == pytest.approx(60.0 / (61.0 * 60.0), rel=1e-9)
+    with pytest.raises(sf.DataError):
+        sf.kernel_weight(4, 0)
+
+
+def test_plan_matches_golden(golden):
+    for c in golden["plans"]:
+        p = sf.plan_sizes(c["n"], c["k"], c["allow"])
+        assert p["exhaustive"] == c["exhaustive"] and p["requested"] == c["requested"]
+        assert p["sizes"].tolist() == c["sizes"]
+        assert p["pairs"].tolist() == c["pairs"]
+        assert p["first"].tolist() == c["first"]
+    with pytest.raises(sf.DataError):
+        sf.plan_sizes(1, 100)
+    with pytest.raises(sf.DataError):
+        sf.plan_sizes(5, 0)
+
+
+def test_graph_build_and_extract_match_reference(ref):
+    edges, feats = toy_graph_arrays()
+    for nodes, e, x, target, hops in [(6, edges, feats, 1, 2), (6, edges, feats, 5, 1)]:
+        g = sf.Graph.build(nodes, e, x)
+        rg = ref.graph_build(nodes, e, x)
+        assert all((a == b).all() for a, b in zip(g.csr(), ref.graph_csr(rg)))
+        a = g.extract(target, hops).arrays()
+        rs = ref.extract(rg, target, hops)
+        for k in ("row_ptr", "col", "edge_player", "players", "local_to_global", "features"):
+            assert (a[k] == getattr(rs, k)).all(), k
+
+
+def test_workload_c1_extraction_matches_reference(ref):
+    d = W.build("C1")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    rg = ref.graph_build(cfg.nodes, d["edges"], d["features"])
+    sg = g.extract(d["target"], cfg.hops)
+    rs = ref.extract(rg, d["target"], cfg.hops)
+    a = sg.arrays()
+    for k in ("row_ptr", "col", "edge_player", "players", "local_to_global", "features"):
+        assert (a[k] == getattr(rs, k)).all(), k
+    assert 900 <= sg.n <= 1100
+    b = sg.ball_sizes(cfg.hops)
+    assert b[0] == 1 and b[-1] == sg.V
+
+
+def test_sfg_roundtrip(tmp_path, ref):
+    edges, feats = toy_graph_arrays(3)
+    path = str(tmp_path / "toy.sfg")
+    W.write_sfg(path, 6, edges, feats)
+    g = sf.Graph.load(path)
+    rg = ref.graph_load(path)
+    assert all((a == b).all() for a, b in zip(g.csr(), ref.graph_csr(rg)))
+    out, rout = str(tmp_path / "out.sfg"), str(tmp_path / "ref.sfg")
+    g.save(out)
+    ref.graph_save(rg, rout)  # graph.cpp:171-193 writes u < v edges in CSR order
+    assert open(out, "rb").read() == open(rout, "rb").read()
+    with pytest.raises(sf.DataError):
+        sf.Graph.load(str(tmp_path / "absent.sfg"))
+
+
+def test_model_random_matches_reference(ref):
+    for dims in [(2, (4,), 2, 17), (602, (128, 128), 41, 7), (3, (), 2, 1)]:
+        m = sf.Model.random(dims[0], dims[1], dims[2], dims[3])
+        rm = ref.model_random(dims[0], list(dims[1]), dims[2], dims[3])
+        for (w, b), rw, rb in zip(m.layers(), rm.weights, rm.biases):
+            assert (w == rw).all() and (b == rb).all()
+
+
+def test_model_validation():
+    with pytest.raises(sf.DataError):
+        sf.Model.create([np.zeros((2, 3), np.float32), np.zeros((2, 1), np.float32)],
+                        [np.zeros(3, np.float32), np.zeros(1, np.float32)])
+    with pytest.raises(sf.DataError):
+        sf.Model.random(0, (), 2, 1)
+
+
+def test_graph_validation():
+    with pytest.raises(sf.DataError):
+        sf.Graph.build(10, np.array([[0, 99]], np.uint64), np.zeros((10, 1), np.float32))
+    g = sf.Graph.build(5, np.zeros((0, 2), np.uint64), np.zeros((5, 1), np.float32))
+    assert g.dims() == (5, 0, 1)
+    with pytest.raises(sf.DataError):
+        g.extract(9, 2)
+
+
+def test_assemble_weights_reference_normalization():
+    # first populated size gets weight 1; rows of size s weigh rho_s / count_s
+    n = 4
+    p = sf.plan_sizes(n, 110, False)
+    # rows: complement pairs of sizes 1/3 (40 pairs) and 2/2 (15 pairs)
+    bits = []
+    for s, cnt in zip(p["sizes"], p["pairs"]):
+        for _ in range(int(cnt)):
+            row = (1 << int(s)) - 1
+            bits += [row, (~row) & 0xF]
+    w = sf.assemble_weights(n, np.array(bits, np.uint64).reshape(-1, 1))
+    assert w[0] == 1.0
+    rho = lambda s: (n - 1.0) / (s * (n - s))  # noqa: E731
+    assert w[80] == pytest.approx((rho(2) / 30) / (rho(1) / 40), rel=1e-15)
+
+
+def test_context_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(sf.ShapflowError):
+        sf.Context(0)
