@@ -88,7 +88,7 @@ class Clocks:
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[5 + i]})
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].strip() == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
                 "samples": len(self.rows)}
 
@@ -228,7 +228,7 @@ def run_ours(args):
     probs = ctx.predict_probs(m, sg, full)
     cls = int(np.argmax(probs))
     seed = sf.node_sampling_seed(cfg.explain_seed, d["target"])
-    k = cfg.samples
+    k = args.samples or cfg.samples
 
     # ---------------------------------------------------------------- value
     for _ in range(args.warmup):
@@ -279,8 +279,8 @@ def run_ours(args):
     from paper_2506_22668_b200.api import ExplainOptions
 
     opts = ExplainOptions(samples=k, seed=cfg.explain_seed)
-    e2e_steps = max(1, min(args.steps, 3))
-    ctx.explain_node(g, m, d["target"], opts)  # warm (allocations)
+    e2e_steps = 0 if args.no_e2e else max(1, min(args.steps, 3))
+    ex = ctx.explain_node(g, m, d["target"], opts) if e2e_steps else None  # warm (allocations)
     h2d0, d2h0 = C.c_uint64(), C.c_uint64()
     sf.lib.sf_ctx_io_bytes(ctx.h, C.byref(h2d0), C.byref(d2h0))
     barrier()
@@ -288,7 +288,7 @@ def run_ours(args):
     for _ in range(e2e_steps):
         ex = ctx.explain_node(g, m, d["target"], opts)
     barrier()
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / max(e2e_steps, 1))
     h2d1, d2h1 = C.c_uint64(), C.c_uint64()
     sf.lib.sf_ctx_io_bytes(ctx.h, C.byref(h2d1), C.byref(d2h1))
 
@@ -316,10 +316,11 @@ def run_ours(args):
                 "accuracy_mode": "FP32 SIMT (CUDA cores), FP64 solver",
             },
             "stage_ms_per_step": {"sampling": stage[0] / args.steps, "prediction": stage[1] / args.steps},
-            "e2e": {"value": k / e2e_s, "unit": "coalitions/s", "s_per_node": e2e_s,
-                    "h2d_bytes_per_step": int((h2d1.value - h2d0.value) / e2e_steps),
-                    "d2h_bytes_per_step": int((d2h1.value - d2h0.value) / e2e_steps),
-                    "cgls_iterations": ex.iterations, "timings_ms": ex.timings},
+            "e2e": None if not e2e_steps else {
+                "value": k / e2e_s, "unit": "coalitions/s", "s_per_node": e2e_s,
+                "h2d_bytes_per_step": int((h2d1.value - h2d0.value) / e2e_steps),
+                "d2h_bytes_per_step": int((d2h1.value - d2h0.value) / e2e_steps),
+                "cgls_iterations": ex.iterations, "timings_ms": ex.timings},
             "gpu_launches": int(launches),
             "roofline": roof,
             "clocks": clk,
@@ -345,6 +346,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the explain_node e2e leg (profiling runs)")
+    ap.add_argument("--samples", type=int, default=0, help="override k (profiling runs only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -58,99 +58,274 @@ __global__ void __launch_bounds__(256)
   out[lane + 32] = inv_sqrt_deg(d1);
 }
 
-// ---------------------------------------------------------------- layer 0
-// H[t][r][i][f] = relu(isd_i(r) * sum_{v in {r} u kept N(r)} isd_i(v) P[v][f]
-//                     + bias[f])        (P = X W0, shared by all coalitions)
-// One CTA per (tile, row r). Thread (cg, fg) owns features 4fg..4fg+3 of
-// CB coalitions; the per-(neighbor, coalition) coefficients
-// bit_i(e) * isd_i(v) are staged in shared memory 32 neighbors at a time,
-// so each P row is fetched once per tile and reused by 64 coalitions.
+// ---------------------------------------------------------------- fused
+// Layer 0 evaluated on the fly and aggregated straight into the next layer
+// (DESIGN.md "fused engine"). For a work item (u, segments v_a..v_b of
+// {u} u N(u)) and the 64 coalitions i of tile t:
+//   h_i(v)   = relu(isd_i(v) * sum_{x in {v} u kept N(v)} isd_i(x) P[x] + b0)
+//   Apart_i  = sum_v m_i(e_uv) isd_i(v) h_i(v)       (isd_i(u) applied later)
+// P = X W0 is shared by all coalitions: each gathered P row is read once per
+// tile and reused by the 64 coalitions; layer-0 rows never reach memory.
+//
+// Pipeline (per CTA = one item x one tile): warp 8 is a producer that
+// streams, 32 entries per chunk, the entry records, the P rows, the isd rows
+// and the mask words of the chunk into a kStages-deep shared-memory ring
+// with cp.async.bulk (TMA bulk copies completing on an mbarrier). Warps 0-7
+// consume: they turn (mask bit, isd) into coefficients in shared memory,
+// then run the rank-1 updates h += coef (x) P from shared memory only.
+// Thread (cg, fg) of the consumers owns features 4fg..4fg+3 of CB
+// coalitions. Segment state (h, isd_i(v), m_i(e_uv) isd_i(v)) stays in
+// registers across chunks.
+constexpr uint32_t kSelf = 0xFFFFFFFFu;
+constexpr int kChunkEntries = 32;
+constexpr int kConsumers = 256;
+
 template <int D>
-struct L0Cfg {
-  static constexpr int FG = D / 4;               // float4 lanes per row
-  static constexpr int THREADS = 256;
-  static constexpr int CGS = THREADS / FG;        // coalition groups
-  static constexpr int CB = kTile / CGS;          // coalitions per thread
-  static_assert(D % 4 == 0 && FG <= THREADS && kTile % CGS == 0, "shape");
+struct FusedCfg {
+  static constexpr int FG = D / 4;            // float4 lanes per row
+  static constexpr int CGS = kConsumers / FG;  // coalition groups
+  static constexpr int CB = kTile / CGS;       // coalitions per thread
+  static constexpr int STAGES = D >= 256 ? 2 : 3;
+  // stage layout (bytes): records | P rows | isd rows | mask words | coef
+  static constexpr int OFF_P = kChunkEntries * 16;
+  static constexpr int OFF_ISD = OFF_P + kChunkEntries * D * 4;
+  static constexpr int OFF_W = OFF_ISD + kChunkEntries * kTile * 4;
+  static constexpr int OFF_COEF = OFF_W + kChunkEntries * 32;
+  static constexpr int STAGE_BYTES = OFF_COEF + kChunkEntries * kTile * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8;
+  static_assert(D % 4 == 0 && FG <= kConsumers && kTile % CGS == 0, "shape");
 };
 
-template <int D, bool kRelu>
-__global__ void __launch_bounds__(256)
-    layer0_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
-                  const uint32_t* __restrict__ row_ptr,
-                  const uint32_t* __restrict__ col,
-                  const uint32_t* __restrict__ ep,
-                  const float* __restrict__ isd, uint32_t V,
-                  const float* __restrict__ P, const float* __restrict__ bias,
-                  uint32_t R, float* __restrict__ H) {
-  using Cfg = L0Cfg<D>;
-  constexpr int KC = 32;
-  __shared__ __align__(16) float coef[KC][kTile];
-  __shared__ uint32_t nbr[KC];
-  const uint32_t r = blockIdx.x;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+// entry record: x (P / isd row), e (mask player of the (v, x) edge or kSelf),
+// euv (mask player of the (u, v) edge, self entries only), flags bit0 =
+// first entry of a segment (x = v), bit1 = last entry of a segment
+template <int D>
+__global__ void __launch_bounds__(kConsumers + 32, D >= 256 ? 1 : 2)
+    fused_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
+                 const float* __restrict__ isd, uint32_t V,
+                 const float* __restrict__ P, const float* __restrict__ bias,
+                 const uint4* __restrict__ ent, const uint32_t* __restrict__ item_ent,
+                 const uint32_t* __restrict__ item_order, uint32_t items,
+                 float* __restrict__ Apart) {
+  using Cfg = FusedCfg<D>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  const uint32_t item = item_order[blockIdx.x];
   const uint64_t t = blockIdx.y;
   const int tid = threadIdx.x;
-  const int fg = tid % Cfg::FG, cg = tid / Cfg::FG;
-  const uint64_t* mt = maskt + t * Wp;
-  const float* isd_t = isd + t * uint64_t(V) * kTile;
-
-  float4 acc[Cfg::CB];
-#pragma unroll
-  for (int j = 0; j < Cfg::CB; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-
-  const uint32_t beg = row_ptr[r], end = row_ptr[r + 1];
-  // entry -1 is the self-loop (always kept)
-  for (int64_t c0 = int64_t(beg) - 1; c0 < int64_t(end); c0 += KC) {
-    const int64_t left = int64_t(end) - c0;
-    const int cnt = left < KC ? int(left) : KC;
-    __syncthreads();
-    for (int idx = tid; idx < cnt * kTile; idx += Cfg::THREADS) {
-      const int k = idx / kTile, i = idx % kTile;
-      const int64_t e = c0 + k;
-      float c;
-      uint32_t v;
-      if (e < int64_t(beg)) {
-        v = r;
-        c = isd_t[uint64_t(r) * kTile + i];
-      } else {
-        v = col[e];
-        const uint64_t w = mt[ep[e]];
-        c = ((w >> i) & 1ull) ? isd_t[uint64_t(v) * kTile + i] : 0.f;
-      }
-      coef[k][i] = c;
-      if (i == 0) nbr[k] = v;
+  const uint32_t e0 = item_ent[item], e1 = item_ent[item + 1];
+  const uint32_t nchunks = (e1 - e0 + kChunkEntries - 1) / kChunkEntries;
+  if (tid == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
     }
-    __syncthreads();
-    for (int k = 0; k < cnt; ++k) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(P + uint64_t(nbr[k]) * D) + fg);
-      const float* ck = &coef[k][cg * Cfg::CB];
-#pragma unroll
-      for (int j = 0; j < Cfg::CB; ++j) {
-        const float c = ck[j];
-        acc[j].x = fmaf(c, x.x, acc[j].x);
-        acc[j].y = fmaf(c, x.y, acc[j].y);
-        acc[j].z = fmaf(c, x.z, acc[j].z);
-        acc[j].w = fmaf(c, x.w, acc[j].w);
-      }
-    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
+
+  if (tid >= kConsumers) {
+    // ------------------------------------------------------------ producer
+    const int lane = tid - kConsumers;
+    const uint64_t* mt = maskt + t * Wp;
+    const float* isd_t = isd + t * uint64_t(V) * kTile;
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      const int s = c % Cfg::STAGES;
+      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
+      unsigned char* st = smem + s * Cfg::STAGE_BYTES;
+      const uint32_t base = e0 + c * kChunkEntries;
+      const bool on = base + lane < e1;
+      uint4 rec = make_uint4(0, kSelf, kSelf, 0);
+      uint32_t bytes = 0;
+      if (on) {
+        rec = ent[base + lane];
+        bytes = D * 4 + kTile * 4 + (rec.y != kSelf ? 16 : 0) + (rec.z != kSelf ? 16 : 0);
+        reinterpret_cast<uint4*>(st)[lane] = rec;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+      __syncwarp();
+      if (on) {
+        bulk_g2s(st + Cfg::OFF_P + lane * D * 4, P + uint64_t(rec.x) * D, D * 4, &full[s]);
+        bulk_g2s(st + Cfg::OFF_ISD + lane * kTile * 4, isd_t + uint64_t(rec.x) * kTile, kTile * 4, &full[s]);
+        if (rec.y != kSelf)
+          bulk_g2s(st + Cfg::OFF_W + lane * 32, mt + (rec.y & ~1u), 16, &full[s]);
+        if (rec.z != kSelf)
+          bulk_g2s(st + Cfg::OFF_W + lane * 32 + 16, mt + (rec.z & ~1u), 16, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int fg = tid % Cfg::FG, cg = tid / Cfg::FG;
+  const int ci = tid & (kTile - 1), ck = tid >> 6;  // coefficient pass: coalition ci, entries ck + 4r
   const float4 bv = reinterpret_cast<const float4*>(bias)[fg];
+  float4 h[Cfg::CB], acc[Cfg::CB];
+  float sv[Cfg::CB];
+  uint32_t dmask = 0;  // bit j: m_i(e_uv) for coalition cg*CB+j of the open segment
 #pragma unroll
   for (int j = 0; j < Cfg::CB; ++j) {
-    const int i = cg * Cfg::CB + j;
-    const float s = isd_t[uint64_t(r) * kTile + i];
-    float4 h;
-    h.x = fmaf(s, acc[j].x, bv.x);
-    h.y = fmaf(s, acc[j].y, bv.y);
-    h.z = fmaf(s, acc[j].z, bv.z);
-    h.w = fmaf(s, acc[j].w, bv.w);
-    if (kRelu) {
-      h.x = fmaxf(h.x, 0.f);
-      h.y = fmaxf(h.y, 0.f);
-      h.z = fmaxf(h.z, 0.f);
-      h.w = fmaxf(h.w, 0.f);
+    h[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sv[j] = 0.f;
+  }
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    const int s = c % Cfg::STAGES;
+    mbar_wait(&full[s], (c / Cfg::STAGES) & 1);
+    unsigned char* st = smem + s * Cfg::STAGE_BYTES;
+    const uint4* recs = reinterpret_cast<const uint4*>(st);
+    const float* Ps = reinterpret_cast<const float*>(st + Cfg::OFF_P);
+    const float* isds = reinterpret_cast<const float*>(st + Cfg::OFF_ISD);
+    const uint64_t* ws = reinterpret_cast<const uint64_t*>(st + Cfg::OFF_W);
+    float* coef = reinterpret_cast<float*>(st + Cfg::OFF_COEF);
+    const int cnt = int(min(uint32_t(kChunkEntries), e1 - (e0 + c * kChunkEntries)));
+    // coefficients m_i(e) isd_i(x); self entries additionally carry
+    // m_i(e_uv) in the sign-free slot dv (kept as the raw bit below)
+#pragma unroll
+    for (int r = 0; r < kChunkEntries / 4; ++r) {
+      const int k = ck + 4 * r;
+      if (k < cnt) {
+        const uint4 rec = recs[k];
+        const bool kept = rec.y == kSelf || ((ws[k * 4 + (rec.y & 1u)] >> ci) & 1ull);
+        coef[k * kTile + ci] = kept ? isds[k * kTile + ci] : 0.f;
+      }
     }
-    reinterpret_cast<float4*>(H + ((t * R + r) * kTile + i) * D)[fg] = h;
+    consumer_sync();
+    for (int k = 0; k < cnt; ++k) {
+      const uint4 rec = recs[k];
+      if (rec.w & 1u) {  // segment start: x = v, remember isd_i(v) and m_i(e_uv)
+        const uint64_t wv = rec.z == kSelf ? ~0ull : ws[k * 4 + 2 + (rec.z & 1u)];
+        dmask = uint32_t(wv >> (cg * Cfg::CB));
+#pragma unroll
+        for (int j = 0; j < Cfg::CB; ++j) sv[j] = isds[k * kTile + cg * Cfg::CB + j];
+      }
+      const float4 x = reinterpret_cast<const float4*>(Ps + k * D)[fg];
+      const float* ckp = coef + k * kTile + cg * Cfg::CB;
+#pragma unroll
+      for (int j = 0; j < Cfg::CB; ++j) {
+        const float cc = ckp[j];
+        h[j].x = fmaf(cc, x.x, h[j].x);
+        h[j].y = fmaf(cc, x.y, h[j].y);
+        h[j].z = fmaf(cc, x.z, h[j].z);
+        h[j].w = fmaf(cc, x.w, h[j].w);
+      }
+      if (rec.w & 2u) {  // segment end: h_i(v) = relu(isd_i(v) h + b0); A += m isd_i(v) h_i(v)
+#pragma unroll
+        for (int j = 0; j < Cfg::CB; ++j) {
+          const float dv = ((dmask >> j) & 1u) ? sv[j] : 0.f;
+          acc[j].x = fmaf(dv, fmaxf(fmaf(sv[j], h[j].x, bv.x), 0.f), acc[j].x);
+          acc[j].y = fmaf(dv, fmaxf(fmaf(sv[j], h[j].y, bv.y), 0.f), acc[j].y);
+          acc[j].z = fmaf(dv, fmaxf(fmaf(sv[j], h[j].z, bv.z), 0.f), acc[j].z);
+          acc[j].w = fmaf(dv, fmaxf(fmaf(sv[j], h[j].w, bv.w), 0.f), acc[j].w);
+          h[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  float* out = Apart + (t * items + item) * uint64_t(kTile) * D;
+#pragma unroll
+  for (int j = 0; j < Cfg::CB; ++j)
+    reinterpret_cast<float4*>(out + uint64_t(cg * Cfg::CB + j) * D)[fg] = acc[j];
+}
+
+// Softmax of z (float, max subtraction, sequential sum) as gcn.cpp:143-152.
+__device__ __forceinline__ void softmax_row(float* zi, uint32_t C) {
+  float mx = zi[0];
+  for (uint32_t c = 1; c < C; ++c) mx = fmaxf(mx, zi[c]);
+  float sum = 0.f;
+  for (uint32_t c = 0; c < C; ++c) {
+    zi[c] = expf(zi[c] - mx);
+    sum += zi[c];
+  }
+  for (uint32_t c = 0; c < C; ++c) zi[c] = zi[c] / sum;
+}
+
+// Per (u in U, tile): A_i = isd_i(u) sum_items Apart (fixed item order),
+// z_i = bias + A_i W (K x N); mode 0: H[t][u][i] = relu(z_i) (hidden layer),
+// mode 1 (U = {target}, last layer): softmax(z_i) -> out / allprobs.
+__global__ void __launch_bounds__(256)
+    reduce_gemm_kernel(const float* __restrict__ Apart, uint32_t items,
+                       const uint32_t* __restrict__ u_items,
+                       const float* __restrict__ isd, uint32_t V,
+                       const float* __restrict__ Wt, const float* __restrict__ bias,
+                       uint32_t K, uint32_t N, uint32_t U, int mode,
+                       float* __restrict__ H, uint32_t cls, uint64_t row0,
+                       uint64_t rows, float* __restrict__ out,
+                       float* __restrict__ allprobs) {
+  extern __shared__ float sm[];
+  float* a = sm;               // [64][K]
+  float* z = sm + kTile * K;   // [64][N] (mode 1)
+  const uint32_t u = blockIdx.x;
+  const uint64_t t = blockIdx.y;
+  const float* isd_t = isd + t * uint64_t(V) * kTile;
+  const uint32_t ib = u_items[u], ie = u_items[u + 1];
+  for (uint32_t idx = threadIdx.x; idx < kTile * K; idx += blockDim.x) {
+    float s = 0.f;
+    for (uint32_t it = ib; it < ie; ++it) s += Apart[(t * items + it) * uint64_t(kTile) * K + idx];
+    a[idx] = isd_t[uint64_t(u) * kTile + idx / K] * s;
+  }
+  __syncthreads();
+  for (uint32_t idx = threadIdx.x; idx < kTile * N; idx += blockDim.x) {
+    const uint32_t i = idx / N, j = idx % N;
+    float v = bias[j];
+    const float* ai = a + i * K;
+    for (uint32_t k = 0; k < K; ++k) v = fmaf(ai[k], Wt[uint64_t(k) * N + j], v);
+    if (mode == 0)
+      H[((t * U + u) * kTile + i) * N + j] = fmaxf(v, 0.f);
+    else
+      z[idx] = v;
+  }
+  if (mode == 0) return;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = warp; i < kTile; i += int(blockDim.x >> 5)) {
+    const uint64_t row = row0 + t * kTile + i;
+    if (row >= rows) continue;
+    if (lane == 0) {
+      softmax_row(z + i * N, N);
+      out[row] = z[i * N + cls];
+    }
+    __syncwarp();
+    if (allprobs)
+      for (uint32_t c = lane; c < N; c += 32) allprobs[row * N + c] = z[i * N + c];
   }
 }
 
@@ -304,16 +479,8 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
     const uint64_t row = row0 + t * kTile + i;
     if (row >= rows) continue;
     if (lane == 0) {
-      float* zi = z + i * C;
-      float mx = zi[0];
-      for (uint32_t c = 1; c < C; ++c) mx = fmaxf(mx, zi[c]);
-      float sum = 0.f;
-      for (uint32_t c = 0; c < C; ++c) {
-        zi[c] = expf(zi[c] - mx);
-        sum += zi[c];
-      }
-      for (uint32_t c = 0; c < C; ++c) zi[c] = zi[c] / sum;
-      out[row] = zi[cls];
+      softmax_row(z + i * C, C);
+      out[row] = z[i * C + cls];
     }
     __syncwarp();
     if (allprobs)
@@ -330,22 +497,79 @@ void gemm(Ctx& ctx, const float* A, const float* B, const float* bias, float* Cm
   SF_LAUNCHED(ctx);
 }
 
+}  // namespace
+
+namespace {
+constexpr uint32_t kItemEntries = 512;  // target staged entries per work item
+
+bool fused_width(uint64_t d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256; }
+
 template <int D>
-bool try_layer0(Ctx& ctx, const uint64_t* maskt, uint64_t Wp, const Engine& e,
-                const float* isd, const float* bias, uint32_t R, uint64_t T,
-                float* H, bool relu) {
+bool try_fused(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
+               uint64_t nt, float* apart) {
   if (e.dims[1] != uint64_t(D)) return false;
-  dim3 grid(R, unsigned(T));
-  if (relu)
-    layer0_kernel<D, true><<<grid, 256, 0, ctx.stream>>>(
-        maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, e.p0.p, bias, R, H);
-  else
-    layer0_kernel<D, false><<<grid, 256, 0, ctx.stream>>>(
-        maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, e.p0.p, bias, R, H);
+  using Cfg = FusedCfg<D>;
+  static bool configured = false;
+  if (!configured) {
+    SF_CUDA(cudaFuncSetAttribute(fused_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    configured = true;
+  }
+  dim3 grid(e.items, unsigned(nt));
+  fused_kernel<D><<<grid, kConsumers + 32, Cfg::SMEM, ctx.stream>>>(
+      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint4*>(e.ent.p), e.item_ent.p,
+      e.item_order.p, e.items, apart);
   SF_LAUNCHED(ctx);
   return true;
 }
 
+// Entry records and work items of the fused plan (see Engine / fused_kernel).
+void build_fused_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
+  const uint32_t U = uint32_t(e.ball[e.L - 2]);
+  std::vector<uint32_t> ent;  // 4 words per entry: x, e, euv, flags
+  std::vector<uint32_t> item_ent{0}, u_items{0};
+  std::vector<uint64_t> item_work;
+  auto entries = [&]() { return uint64_t(ent.size() / 4); };
+  for (uint32_t u = 0; u < U; ++u) {
+    uint64_t open_entries = 0;
+    auto close_item = [&]() {
+      if (entries() > item_ent.back()) {
+        item_ent.push_back(uint32_t(entries()));
+        item_work.push_back(open_entries);
+        open_entries = 0;
+      }
+    };
+    auto segment = [&](uint32_t v, uint32_t euv) {
+      const uint64_t w = sg.row_ptr[v + 1] - sg.row_ptr[v] + 1;
+      if (open_entries && open_entries + w > kItemEntries) close_item();
+      ent.insert(ent.end(), {v, kSelf, euv, w == 1 ? 3u : 1u});
+      for (uint64_t k = sg.row_ptr[v]; k < sg.row_ptr[v + 1]; ++k) {
+        const bool last = (k + 1 == sg.row_ptr[v + 1]);
+        ent.insert(ent.end(), {sg.col[k], sg.edge_player[k], kSelf, last ? 2u : 0u});
+      }
+      open_entries += w;
+    };
+    segment(u, kSelf);
+    for (uint64_t k = sg.row_ptr[u]; k < sg.row_ptr[u + 1]; ++k) segment(sg.col[k], sg.edge_player[k]);
+    close_item();
+    u_items.push_back(uint32_t(item_ent.size() - 1));
+  }
+  if (entries() >= (1ull << 32)) throw DataError("fused plan too large");
+  // heaviest items first (LPT); partial sums keep the item index, so the
+  // reduction order stays fixed
+  std::vector<uint32_t> order(item_work.size());
+  for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t a, uint32_t b) { return item_work[a] > item_work[b]; });
+  e.U = U;
+  e.items = uint32_t(item_work.size());
+  e.entries = entries();
+  e.ent.upload(ent.data(), ent.size(), ctx.stream);
+  e.item_ent.upload(item_ent.data(), item_ent.size(), ctx.stream);
+  e.item_order.upload(order.data(), order.size(), ctx.stream);
+  e.u_items.upload(u_items.data(), u_items.size(), ctx.stream);
+  ctx.h2d_bytes += (ent.size() + item_ent.size() + order.size() + u_items.size()) * 4;
+  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+}
 }  // namespace
 
 void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
@@ -358,7 +582,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   e.sg_id = 0;
   e.V = sg.num_nodes();
   e.n = sg.num_players();
-  e.W = static_cast<uint32_t>((e.n + 63) / 64);
+  e.W = std::max<uint32_t>(1, static_cast<uint32_t>((e.n + 63) / 64));  // n = 0: one zero word
   e.L = m.depth();
   e.dims.assign(1, m.layers.front().in);
   for (const Layer& l : m.layers) e.dims.push_back(l.out);
@@ -385,6 +609,8 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   ctx.h2d_bytes += (rp.size() + sg.col.size() + sg.edge_player.size()) * 4 + sg.features.size() * 4;
   for (const Layer& l : m.layers) ctx.h2d_bytes += (l.weight.size() + l.bias.size()) * 4;
   SF_CUDA(cudaStreamSynchronize(ctx.stream));  // temporaries x, w0 die here
+  e.fused = e.L >= 2 && fused_width(e.dims[1]) && e.n > 0;
+  if (e.fused) build_fused_plan(ctx, e, sg);
   e.sg_id = sg.id;
   e.model_id = m.id;
 }
@@ -392,6 +618,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
 void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                     uint32_t cls, float* dev_out, float* dev_allprobs,
                     float* dominant_ms) {
+  (void)dominant_ms;
   Engine& e = ctx.engine;
   if (rows == 0) return;
   const uint64_t tiles = (rows + kTile - 1) / kTile;
@@ -401,11 +628,17 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   // rows each layer produces: R_l = |B_{L-1-l}|
   std::vector<uint64_t> R(L);
   for (int l = 0; l < L; ++l) R[l] = e.ball[L - 1 - l];
-  // per-tile bytes: masks + isd + two activation buffers + aggregation
-  uint64_t hmax = 0, amax = 0;
-  for (int l = 0; l + 1 < L; ++l) hmax = std::max(hmax, R[l] * kTile * e.dims[l + 1]);
-  for (int l = 1; l + 1 < L; ++l) amax = std::max(amax, R[l] * kTile * e.dims[l]);
-  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * 4 + (2 * hmax + amax) * 4;
+  // per-tile bytes: masks + isd + activations. Fused: item partials and the
+  // layer-1 outputs at U; generic: two activation buffers + aggregation.
+  uint64_t hmax = 0, amax = 0, apart = 0;
+  const int first_generic = e.fused ? 2 : 0;  // first layer the generic path runs
+  if (e.fused) {
+    apart = uint64_t(e.items) * kTile * e.dims[1];
+    if (L >= 3) hmax = uint64_t(e.U) * kTile * e.dims[2];
+  }
+  for (int l = first_generic; l + 1 < L; ++l) hmax = std::max(hmax, R[l] * kTile * e.dims[l + 1]);
+  for (int l = std::max(1, first_generic); l + 1 < L; ++l) amax = std::max(amax, R[l] * kTile * e.dims[l]);
+  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * 4 + (2 * hmax + amax + apart) * 4;
   const uint64_t budget = 96ull << 20;  // keep a batch's intermediates L2-sized
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
@@ -414,14 +647,15 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   const uint64_t off_h0 = off_isd + T * uint64_t(e.V) * kTile * 4;
   const uint64_t off_h1 = off_h0 + T * hmax * 4;
   const uint64_t off_a = off_h1 + T * hmax * 4;
-  ctx.work.reserve(off_a + T * amax * 4 + 256);
+  const uint64_t off_p = off_a + T * amax * 4;
+  ctx.work.reserve(off_p + T * apart * 4 + 256);
   unsigned char* base = ctx.work.p;
   uint64_t* maskt = reinterpret_cast<uint64_t*>(base);
   float* isd = reinterpret_cast<float*>(base + off_isd);
   float* hbuf[2] = {reinterpret_cast<float*>(base + off_h0), reinterpret_cast<float*>(base + off_h1)};
   float* abuf = reinterpret_cast<float*>(base + off_a);
+  float* pbuf = reinterpret_cast<float*>(base + off_p);
 
-  (void)dominant_ms;
   for (uint64_t t0 = 0; t0 < tiles; t0 += T) {
     const uint64_t nt = std::min(T, tiles - t0);
     const uint64_t row0 = t0 * kTile;
@@ -432,46 +666,63 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       isd_kernel<<<grid, 256, 0, ctx.stream>>>(maskt, Wp, e.row_ptr.p, e.edge_player.p, e.V, isd);
       SF_LAUNCHED(ctx);
     }
-    const float* X = e.p0.p;  // layer input: P0 (shared) or per-coalition H
+    const float* X = e.p0.p;  // current layer input: P0 (shared) or per-coalition H
     bool shared_x = true;
     uint64_t Rin = e.V;
     int cur = 0;
-    for (int l = 0; l + 1 < L; ++l) {
+    int l = 0;
+    if (e.fused) {
+      std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+      if (ctx.time_dominant) {
+        if (ctx.dom_used == ctx.dom_events.size()) {
+          std::pair<cudaEvent_t, cudaEvent_t> pr;
+          SF_CUDA(cudaEventCreate(&pr.first));
+          SF_CUDA(cudaEventCreate(&pr.second));
+          ctx.dom_events.push_back(pr);
+        }
+        ev = &ctx.dom_events[ctx.dom_used++];
+        ctx.dom_pairs += nrows / 2;
+        SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
+      }
+      const bool ok = try_fused<128>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
+                      try_fused<64>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
+                      try_fused<32>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
+                      try_fused<16>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
+                      try_fused<256>(ctx, e, maskt, Wp, isd, nt, pbuf);
+      if (!ok) throw std::logic_error("fused width not instantiated");
+      if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
+      const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
+      const int mode = (L == 2) ? 1 : 0;
+      const size_t smem = size_t(kTile) * (K + (mode ? N : 0)) * 4;
+      if (smem > 48 * 1024)
+        SF_CUDA(cudaFuncSetAttribute(reduce_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(std::min<size_t>(smem, 227 * 1024))));
+      dim3 grid(e.U, unsigned(nt));
+      reduce_gemm_kernel<<<grid, 256, smem, ctx.stream>>>(
+          pbuf, e.items, e.u_items.p, isd, e.V, e.w[1]->p, e.b[1]->p, K, N, e.U, mode, hbuf[0], cls,
+          row0, rows, dev_out, dev_allprobs);
+      SF_LAUNCHED(ctx);
+      if (L == 2) continue;
+      X = hbuf[0];
+      shared_x = false;
+      Rin = e.U;
+      cur = 1;
+      l = 2;
+    }
+    for (; l + 1 < L; ++l) {
       float* out = hbuf[cur];
       const uint32_t Rl = uint32_t(R[l]);
-      if (l == 0) {
-        std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
-        if (ctx.time_dominant) {
-          if (ctx.dom_used == ctx.dom_events.size()) {
-            std::pair<cudaEvent_t, cudaEvent_t> pr;
-            SF_CUDA(cudaEventCreate(&pr.first));
-            SF_CUDA(cudaEventCreate(&pr.second));
-            ctx.dom_events.push_back(pr);
-          }
-          ev = &ctx.dom_events[ctx.dom_used++];
-          ctx.dom_pairs += nrows / 2;
-          SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
-        }
-        const float* b0 = e.b[0]->p;
-        bool done = try_layer0<128>(ctx, maskt, Wp, e, isd, b0, Rl, nt, out, true) ||
-                    try_layer0<64>(ctx, maskt, Wp, e, isd, b0, Rl, nt, out, true) ||
-                    try_layer0<32>(ctx, maskt, Wp, e, isd, b0, Rl, nt, out, true) ||
-                    try_layer0<16>(ctx, maskt, Wp, e, isd, b0, Rl, nt, out, true) ||
-                    try_layer0<256>(ctx, maskt, Wp, e, isd, b0, Rl, nt, out, true);
-        if (!done) {
-          dim3 grid(Rl, unsigned(nt));
-          agg_generic_kernel<<<grid, 256, 0, ctx.stream>>>(
-              maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, e.p0.p, 1, 0,
-              uint32_t(e.dims[1]), b0, 1, Rl, out);
-          SF_LAUNCHED(ctx);
-        }
-        if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
-      } else {
-        const uint32_t Din = uint32_t(e.dims[l]), Dout = uint32_t(e.dims[l + 1]);
-        dim3 grid(Rl, unsigned(nt));
+      const uint32_t Din = uint32_t(e.dims[l]), Dout = uint32_t(e.dims[l + 1]);
+      dim3 grid(Rl, unsigned(nt));
+      if (l == 0) {  // generic layer 0 (unsupported widths): aggregate P0, bias, ReLU
         agg_generic_kernel<<<grid, 256, 0, ctx.stream>>>(
-            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, 0, uint32_t(Rin), Din,
-            nullptr, 0, Rl, abuf);
+            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, e.p0.p, 1, 0, Dout,
+            e.b[0]->p, 1, Rl, out);
+        SF_LAUNCHED(ctx);
+      } else {
+        agg_generic_kernel<<<grid, 256, 0, ctx.stream>>>(
+            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, shared_x ? 1 : 0,
+            uint32_t(Rin), Din, nullptr, 0, Rl, abuf);
         SF_LAUNCHED(ctx);
         gemm(ctx, abuf, e.w[l]->p, e.b[l]->p, out, nt * Rl * kTile, Dout, Din, true);
       }
@@ -489,8 +740,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                                      int(std::min<size_t>(smem, 227 * 1024))));
       last_kernel<<<unsigned(nt), 256, smem, ctx.stream>>>(
           maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, shared_x ? 1 : 0,
-          uint32_t(Rin), Din, Wt, e.b[L - 1]->p, C, cls, row0, rows, dev_out - row0 + row0,
-          dev_allprobs);
+          uint32_t(Rin), Din, Wt, e.b[L - 1]->p, C, cls, row0, rows, dev_out, dev_allprobs);
       SF_LAUNCHED(ctx);
     }
   }

@@ -132,6 +132,16 @@ struct Engine {
   DevBuf<uint32_t> row_ptr, col, edge_player;
   DevBuf<float> p0;                 // X W_0, V x d_1 (layer-0 transform-first)
   std::vector<std::unique_ptr<DevBuf<float>>> w, b;  // per layer (w[0] unused)
+  // Fused layer-0 + layer-1 aggregation plan:
+  // rows U = B_{L-2} (prefix of local ids); for each u in U the segments
+  // v in {u} u N(u) (self first, CSR order), each segment the entries
+  // {v} u N(v) whose P0 rows layer 0 gathers. Work items are contiguous
+  // segment ranges of one u, balanced by entry count.
+  bool fused = false;
+  uint32_t U = 0, items = 0;
+  uint64_t entries = 0;
+  DevBuf<uint32_t> ent;  // 4 words per entry: x, e, e_uv, flags
+  DevBuf<uint32_t> item_ent, item_order, u_items;
 };
 
 struct CommStats {  // comm.hpp:13-19
