@@ -230,6 +230,16 @@ def run_ours(args):
     seed = sf.node_sampling_seed(cfg.explain_seed, d["target"])
     k = args.samples or cfg.samples
 
+    if args.explain_only:  # profiling: one warm explain_node, then one more (ncu launch lists)
+        from paper_2506_22668_b200.api import ExplainOptions
+
+        for _ in range(2):
+            ex = ctx.explain_node(g, m, d["target"], ExplainOptions(samples=k, seed=cfg.explain_seed))
+        if rank == 0:
+            print(json.dumps({"explain_only": True, "iterations": ex.iterations, "timings_ms": ex.timings}))
+        ctx.close()
+        return 0
+
     # ---------------------------------------------------------------- value
     for _ in range(args.warmup):
         ctx.sample_and_predict(m, sg, cls, k, seed)
@@ -348,6 +358,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the explain_node e2e leg (profiling runs)")
     ap.add_argument("--samples", type=int, default=0, help="override k (profiling runs only)")
+    ap.add_argument("--explain-only", action="store_true", help="profiling: run explain_node twice and exit")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -91,7 +91,8 @@ struct FusedCfg {
   static constexpr int OFF_ISD = OFF_P + kChunkEntries * D * 4;
   static constexpr int OFF_W = OFF_ISD + kChunkEntries * kTile * 4;
   static constexpr int OFF_COEF = OFF_W + kChunkEntries * 32;
-  static constexpr int STAGE_BYTES = OFF_COEF + kChunkEntries * kTile * 4;
+  static constexpr int OFF_FLAGS = OFF_COEF + kChunkEntries * kTile * 4;  // start / end bitmasks
+  static constexpr int STAGE_BYTES = OFF_FLAGS + 16;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8;
   static_assert(D % 4 == 0 && FG <= kConsumers && kTile % CGS == 0, "shape");
 };
@@ -133,7 +134,7 @@ __device__ __forceinline__ void consumer_sync() {
 // euv (mask player of the (u, v) edge, self entries only), flags bit0 =
 // first entry of a segment (x = v), bit1 = last entry of a segment
 template <int D>
-__global__ void __launch_bounds__(kConsumers + 32, D >= 256 ? 1 : 2)
+__global__ void __launch_bounds__(kConsumers + 32) __maxnreg__(D >= 256 ? 224 : 112)
     fused_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
                  const float* __restrict__ isd, uint32_t V,
                  const float* __restrict__ P, const float* __restrict__ bias,
@@ -178,7 +179,13 @@ __global__ void __launch_bounds__(kConsumers + 32, D >= 256 ? 1 : 2)
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+      const uint32_t startm = __ballot_sync(kFull, on && (rec.w & 1u));
+      const uint32_t endm = __ballot_sync(kFull, on && (rec.w & 2u));
+      if (lane == 0) {
+        reinterpret_cast<uint32_t*>(st + Cfg::OFF_FLAGS)[0] = startm;
+        reinterpret_cast<uint32_t*>(st + Cfg::OFF_FLAGS)[1] = endm;
+        mbar_arrive_expect_tx(&full[s], bytes);
+      }
       __syncwarp();
       if (on) {
         bulk_g2s(st + Cfg::OFF_P + lane * D * 4, P + uint64_t(rec.x) * D, D * 4, &full[s]);
@@ -227,25 +234,36 @@ __global__ void __launch_bounds__(kConsumers + 32, D >= 256 ? 1 : 2)
       }
     }
     consumer_sync();
-    for (int k = 0; k < cnt; ++k) {
-      const uint4 rec = recs[k];
-      if (rec.w & 1u) {  // segment start: x = v, remember isd_i(v) and m_i(e_uv)
-        const uint64_t wv = rec.z == kSelf ? ~0ull : ws[k * 4 + 2 + (rec.z & 1u)];
+    // Runs of entries between segment boundaries: a segment starts at the
+    // first entry of a run (chunk start or right after an end) and the run
+    // stops at the next segment end, so the inner loop is branch-free.
+    const uint32_t startm = reinterpret_cast<const uint32_t*>(st + Cfg::OFF_FLAGS)[0];
+    const uint32_t endm = reinterpret_cast<const uint32_t*>(st + Cfg::OFF_FLAGS)[1];
+    int k = 0;
+    while (k < cnt) {
+      if ((startm >> k) & 1u) {  // segment start: x = v; keep isd_i(v) and m_i(e_uv)
+        const uint32_t z = recs[k].z;
+        const uint64_t wv = z == kSelf ? ~0ull : ws[k * 4 + 2 + (z & 1u)];
         dmask = uint32_t(wv >> (cg * Cfg::CB));
 #pragma unroll
         for (int j = 0; j < Cfg::CB; ++j) sv[j] = isds[k * kTile + cg * Cfg::CB + j];
       }
-      const float4 x = reinterpret_cast<const float4*>(Ps + k * D)[fg];
-      const float* ckp = coef + k * kTile + cg * Cfg::CB;
+      const uint32_t rest = endm >> k;
+      const int stop = rest ? k + __ffs(int(rest)) - 1 : cnt - 1;  // inclusive
+#pragma unroll 2
+      for (; k <= stop; ++k) {
+        const float4 x = reinterpret_cast<const float4*>(Ps + k * D)[fg];
+        const float* ckp = coef + k * kTile + cg * Cfg::CB;
 #pragma unroll
-      for (int j = 0; j < Cfg::CB; ++j) {
-        const float cc = ckp[j];
-        h[j].x = fmaf(cc, x.x, h[j].x);
-        h[j].y = fmaf(cc, x.y, h[j].y);
-        h[j].z = fmaf(cc, x.z, h[j].z);
-        h[j].w = fmaf(cc, x.w, h[j].w);
+        for (int j = 0; j < Cfg::CB; ++j) {
+          const float cc = ckp[j];
+          h[j].x = fmaf(cc, x.x, h[j].x);
+          h[j].y = fmaf(cc, x.y, h[j].y);
+          h[j].z = fmaf(cc, x.z, h[j].z);
+          h[j].w = fmaf(cc, x.w, h[j].w);
+        }
       }
-      if (rec.w & 2u) {  // segment end: h_i(v) = relu(isd_i(v) h + b0); A += m isd_i(v) h_i(v)
+      if (rest) {  // segment end: h_i(v) = relu(isd_i(v) h + b0); A += m isd_i(v) h_i(v)
 #pragma unroll
         for (int j = 0; j < Cfg::CB; ++j) {
           const float dv = ((dmask >> j) & 1u) ? sv[j] : 0.f;
@@ -278,55 +296,47 @@ __device__ __forceinline__ void softmax_row(float* zi, uint32_t C) {
   for (uint32_t c = 0; c < C; ++c) zi[c] = zi[c] / sum;
 }
 
-// Per (u in U, tile): A_i = isd_i(u) sum_items Apart (fixed item order),
-// z_i = bias + A_i W (K x N); mode 0: H[t][u][i] = relu(z_i) (hidden layer),
-// mode 1 (U = {target}, last layer): softmax(z_i) -> out / allprobs.
+// A[t][u][i][:] = isd_i(u) * sum over the items of u of Apart[t][item][i][:]
+// (fixed item order, deterministic), one float4 per thread.
 __global__ void __launch_bounds__(256)
-    reduce_gemm_kernel(const float* __restrict__ Apart, uint32_t items,
-                       const uint32_t* __restrict__ u_items,
-                       const float* __restrict__ isd, uint32_t V,
-                       const float* __restrict__ Wt, const float* __restrict__ bias,
-                       uint32_t K, uint32_t N, uint32_t U, int mode,
-                       float* __restrict__ H, uint32_t cls, uint64_t row0,
-                       uint64_t rows, float* __restrict__ out,
-                       float* __restrict__ allprobs) {
-  extern __shared__ float sm[];
-  float* a = sm;               // [64][K]
-  float* z = sm + kTile * K;   // [64][N] (mode 1)
-  const uint32_t u = blockIdx.x;
+    reduce_partials_kernel(const float4* __restrict__ Apart, uint32_t items,
+                           const uint32_t* __restrict__ u_items,
+                           const float* __restrict__ isd, uint32_t V, uint32_t K4,
+                           uint32_t U, float4* __restrict__ A) {
+  const uint64_t idx = blockIdx.x * 256ull + threadIdx.x;
+  const uint64_t per_u = uint64_t(kTile) * K4;
+  if (idx >= U * per_u) return;
   const uint64_t t = blockIdx.y;
-  const float* isd_t = isd + t * uint64_t(V) * kTile;
-  const uint32_t ib = u_items[u], ie = u_items[u + 1];
-  for (uint32_t idx = threadIdx.x; idx < kTile * K; idx += blockDim.x) {
-    float s = 0.f;
-    for (uint32_t it = ib; it < ie; ++it) s += Apart[(t * items + it) * uint64_t(kTile) * K + idx];
-    a[idx] = isd_t[uint64_t(u) * kTile + idx / K] * s;
+  const uint32_t u = uint32_t(idx / per_u);
+  const uint64_t rem = idx % per_u;
+  const uint32_t i = uint32_t(rem / K4);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t it = u_items[u]; it < u_items[u + 1]; ++it) {
+    const float4 p = Apart[(t * items + it) * per_u + rem];
+    s.x += p.x;
+    s.y += p.y;
+    s.z += p.z;
+    s.w += p.w;
   }
-  __syncthreads();
-  for (uint32_t idx = threadIdx.x; idx < kTile * N; idx += blockDim.x) {
-    const uint32_t i = idx / N, j = idx % N;
-    float v = bias[j];
-    const float* ai = a + i * K;
-    for (uint32_t k = 0; k < K; ++k) v = fmaf(ai[k], Wt[uint64_t(k) * N + j], v);
-    if (mode == 0)
-      H[((t * U + u) * kTile + i) * N + j] = fmaxf(v, 0.f);
-    else
-      z[idx] = v;
+  const float sc = isd[(t * V + u) * kTile + i];
+  A[(t * U + u) * per_u + rem] = make_float4(sc * s.x, sc * s.y, sc * s.z, sc * s.w);
+}
+
+// Softmax of each logit row (warp per row), p[cls] and optionally all probs.
+__global__ void softmax_rows_kernel(float* __restrict__ Z, uint32_t N, uint64_t row0,
+                                    uint64_t nbatch, uint64_t rows, uint32_t cls,
+                                    float* __restrict__ out, float* __restrict__ allprobs) {
+  const uint64_t r = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= nbatch || row0 + r >= rows) return;
+  float* z = Z + r * N;
+  if (lane == 0) {
+    softmax_row(z, N);
+    out[row0 + r] = z[cls];
   }
-  if (mode == 0) return;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = warp; i < kTile; i += int(blockDim.x >> 5)) {
-    const uint64_t row = row0 + t * kTile + i;
-    if (row >= rows) continue;
-    if (lane == 0) {
-      softmax_row(z + i * N, N);
-      out[row] = z[i * N + cls];
-    }
-    __syncwarp();
-    if (allprobs)
-      for (uint32_t c = lane; c < N; c += 32) allprobs[row * N + c] = z[i * N + c];
-  }
+  __syncwarp();
+  if (allprobs)
+    for (uint32_t c = lane; c < N; c += 32) allprobs[(row0 + r) * N + c] = z[c];
 }
 
 // ---------------------------------------------------------------- generic
@@ -422,7 +432,8 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- last layer
-// Target row only (gcn.cpp:134-140) + softmax (143-152), one CTA per tile.
+// Target row only (gcn.cpp:134-140) + softmax (143-152); one CTA per
+// (tile, block of cpb coalitions).
 // a_i = isd_i(0) sum_{v in {0} u kept N(0)} isd_i(v) X(v, i, :)
 // z_i = bias + a_i W   (skipped when X is already transformed: L == 1)
 // p_i = softmax(z_i) in float with max subtraction; out = p_i[cls].
@@ -435,18 +446,19 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
                             uint32_t Rin, uint32_t Din,
                             const float* __restrict__ Wt,
                             const float* __restrict__ bias, uint32_t C,
-                            uint32_t cls, uint64_t row0, uint64_t rows,
+                            uint32_t cls, uint64_t row0, uint64_t rows, uint32_t cpb,
                             float* __restrict__ out,
                             float* __restrict__ allprobs) {
   extern __shared__ float sm[];
-  float* a = sm;                  // [64][Din]
-  float* z = sm + kTile * Din;    // [64][C]
+  float* a = sm;                // [cpb][Din]
+  float* z = sm + cpb * Din;    // [cpb][C]
   const uint64_t t = blockIdx.x;
+  const uint32_t i0 = blockIdx.y * cpb;
   const uint64_t* mt = maskt + t * Wp;
   const float* isd_t = isd + t * uint64_t(V) * kTile;
   const uint32_t beg = row_ptr[0], end = row_ptr[1];
-  for (uint32_t idx = threadIdx.x; idx < kTile * Din; idx += blockDim.x) {
-    const uint32_t i = idx / Din, f = idx % Din;
+  for (uint32_t idx = threadIdx.x; idx < cpb * Din; idx += blockDim.x) {
+    const uint32_t i = i0 + idx / Din, f = idx % Din;
     auto x_at = [&](uint32_t v) {
       return shared_x ? X[uint64_t(v) * Din + f]
                       : X[((t * Rin + v) * kTile + i) * Din + f];
@@ -460,31 +472,31 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
     a[idx] = isd_t[i] * acc;
   }
   __syncthreads();
-  for (uint32_t idx = threadIdx.x; idx < kTile * C; idx += blockDim.x) {
-    const uint32_t i = idx / C, c = idx % C;
+  for (uint32_t idx = threadIdx.x; idx < cpb * C; idx += blockDim.x) {
+    const uint32_t il = idx / C, c = idx % C;
     float v = bias[c];
     if (Wt) {
       // bias-first sequential accumulation as in affine_row (gcn.cpp:116-123)
       for (uint32_t k = 0; k < Din; ++k)
-        v = __fadd_rn(v, __fmul_rn(a[i * Din + k], Wt[uint64_t(k) * C + c]));
+        v = __fadd_rn(v, __fmul_rn(a[il * Din + k], Wt[uint64_t(k) * C + c]));
     } else {
-      v = __fadd_rn(a[i * Din + c], v);
+      v = __fadd_rn(a[il * Din + c], v);
     }
     z[idx] = v;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  for (int i = warp; i < kTile; i += nwarps) {
-    const uint64_t row = row0 + t * kTile + i;
+  for (uint32_t il = warp; il < cpb; il += nwarps) {
+    const uint64_t row = row0 + t * kTile + i0 + il;
     if (row >= rows) continue;
     if (lane == 0) {
-      softmax_row(z + i * C, C);
-      out[row] = z[i * C + cls];
+      softmax_row(z + il * C, C);
+      out[row] = z[il * C + cls];
     }
     __syncwarp();
     if (allprobs)
-      for (uint32_t c = lane; c < C; c += 32) allprobs[row * C + c] = z[i * C + c];
+      for (uint32_t c = lane; c < C; c += 32) allprobs[row * C + c] = z[il * C + c];
   }
 }
 
@@ -632,13 +644,15 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   // layer-1 outputs at U; generic: two activation buffers + aggregation.
   uint64_t hmax = 0, amax = 0, apart = 0;
   const int first_generic = e.fused ? 2 : 0;  // first layer the generic path runs
+  uint64_t afused = 0;  // reduced layer-1 aggregation at U (fused path)
   if (e.fused) {
     apart = uint64_t(e.items) * kTile * e.dims[1];
-    if (L >= 3) hmax = uint64_t(e.U) * kTile * e.dims[2];
+    afused = uint64_t(e.U) * kTile * e.dims[1];
+    hmax = uint64_t(e.U) * kTile * e.dims[2];  // H at U (L >= 3) or logits (L == 2)
   }
   for (int l = first_generic; l + 1 < L; ++l) hmax = std::max(hmax, R[l] * kTile * e.dims[l + 1]);
   for (int l = std::max(1, first_generic); l + 1 < L; ++l) amax = std::max(amax, R[l] * kTile * e.dims[l]);
-  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * 4 + (2 * hmax + amax + apart) * 4;
+  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * 4 + (2 * hmax + amax + apart + afused) * 4;
   const uint64_t budget = 96ull << 20;  // keep a batch's intermediates L2-sized
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
@@ -648,13 +662,15 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   const uint64_t off_h1 = off_h0 + T * hmax * 4;
   const uint64_t off_a = off_h1 + T * hmax * 4;
   const uint64_t off_p = off_a + T * amax * 4;
-  ctx.work.reserve(off_p + T * apart * 4 + 256);
+  const uint64_t off_af = off_p + T * apart * 4;
+  ctx.work.reserve(off_af + T * afused * 4 + 256);
   unsigned char* base = ctx.work.p;
   uint64_t* maskt = reinterpret_cast<uint64_t*>(base);
   float* isd = reinterpret_cast<float*>(base + off_isd);
   float* hbuf[2] = {reinterpret_cast<float*>(base + off_h0), reinterpret_cast<float*>(base + off_h1)};
   float* abuf = reinterpret_cast<float*>(base + off_a);
   float* pbuf = reinterpret_cast<float*>(base + off_p);
+  float* afbuf = reinterpret_cast<float*>(base + off_af);
 
   for (uint64_t t0 = 0; t0 < tiles; t0 += T) {
     const uint64_t nt = std::min(T, tiles - t0);
@@ -692,16 +708,22 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       if (!ok) throw std::logic_error("fused width not instantiated");
       if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
-      const int mode = (L == 2) ? 1 : 0;
-      const size_t smem = size_t(kTile) * (K + (mode ? N : 0)) * 4;
-      if (smem > 48 * 1024)
-        SF_CUDA(cudaFuncSetAttribute(reduce_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(std::min<size_t>(smem, 227 * 1024))));
-      dim3 grid(e.U, unsigned(nt));
-      reduce_gemm_kernel<<<grid, 256, smem, ctx.stream>>>(
-          pbuf, e.items, e.u_items.p, isd, e.V, e.w[1]->p, e.b[1]->p, K, N, e.U, mode, hbuf[0], cls,
-          row0, rows, dev_out, dev_allprobs);
-      SF_LAUNCHED(ctx);
+      {
+        const uint64_t work = uint64_t(e.U) * kTile * (K / 4);
+        dim3 grid(unsigned((work + 255) / 256), unsigned(nt));
+        reduce_partials_kernel<<<grid, 256, 0, ctx.stream>>>(
+            reinterpret_cast<const float4*>(pbuf), e.items, e.u_items.p, isd, e.V, K / 4, e.U,
+            reinterpret_cast<float4*>(afbuf));
+        SF_LAUNCHED(ctx);
+      }
+      // layer 1: A W1 + b1 (ReLU for a hidden layer; logits when L == 2)
+      gemm(ctx, afbuf, e.w[1]->p, e.b[1]->p, hbuf[0], nt * e.U * kTile, N, K, L >= 3);
+      if (L == 2) {
+        const uint64_t nb = nt * kTile;
+        softmax_rows_kernel<<<unsigned((nb * 32 + 255) / 256), 256, 0, ctx.stream>>>(
+            hbuf[0], N, row0, nb, rows, cls, dev_out, dev_allprobs);
+        SF_LAUNCHED(ctx);
+      }
       if (L == 2) continue;
       X = hbuf[0];
       shared_x = false;
@@ -734,13 +756,15 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
     {
       const uint32_t Din = uint32_t(L == 1 ? C : e.dims[L - 1]);
       const float* Wt = (L == 1) ? nullptr : e.w[L - 1]->p;
-      const size_t smem = size_t(kTile) * (Din + C) * 4;
+      const uint32_t cpb = 8;  // coalitions per CTA
+      const size_t smem = size_t(cpb) * (Din + C) * 4;
       if (smem > 48 * 1024)
         SF_CUDA(cudaFuncSetAttribute(last_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(std::min<size_t>(smem, 227 * 1024))));
-      last_kernel<<<unsigned(nt), 256, smem, ctx.stream>>>(
+      dim3 grid(unsigned(nt), kTile / cpb);
+      last_kernel<<<grid, 256, smem, ctx.stream>>>(
           maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, shared_x ? 1 : 0,
-          uint32_t(Rin), Din, Wt, e.b[L - 1]->p, C, cls, row0, rows, dev_out, dev_allprobs);
+          uint32_t(Rin), Din, Wt, e.b[L - 1]->p, C, cls, row0, rows, cpb, dev_out, dev_allprobs);
       SF_LAUNCHED(ctx);
     }
   }
