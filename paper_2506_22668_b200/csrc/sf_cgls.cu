@@ -100,66 +100,74 @@ __global__ void init_r_kernel(const double* __restrict__ sw,
 }
 
 // ---------------------------------------------------------------- M u
-// part[c][row] = sum over set bits e of row within player chunk c of u[e]
-// for every row whose dot is needed (even rows; odd rows of non-complement
-// pairs). One warp per row, u chunk staged in shared memory.
-__global__ void __launch_bounds__(256)
-    forward_partial_kernel(const uint64_t* __restrict__ rows, uint32_t W,
-                           uint64_t nrows, const uint8_t* __restrict__ is_comp,
-                           const double* __restrict__ u, uint32_t n,
-                           double* __restrict__ part) {
-  extern __shared__ double su[];
-  const uint32_t c = blockIdx.y;
-  const uint32_t e0 = c * kChunk;
-  const uint32_t ce = min(n - e0, kChunk);
-  for (uint32_t i = threadIdx.x; i < ce; i += blockDim.x) su[i] = u[e0 + i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t w0 = e0 / 64, w1 = min(W, (e0 + ce + 63) / 64);
-  const uint64_t warps = uint64_t(gridDim.x) * 8;
-  for (uint64_t row = blockIdx.x * 8ull + warp; row < nrows; row += warps) {
-    if ((row & 1) && is_comp[row >> 1]) continue;
-    const uint64_t* rp = rows + row * W;
-    double acc = 0.0;
-    for (uint32_t w = w0 + lane; w < w1; w += 32) {
-      uint64_t x = rp[w];
-      const uint32_t base = w * 64 - e0;
-      while (x) {
-        const int b = __ffsll(static_cast<long long>(x)) - 1;
-        x &= x - 1;
-        acc += su[base + b];
-      }
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) part[uint64_t(c) * nrows + row] = acc;
-  }
-}
+// One CTA per block of kFwdRows rows (whole complement pairs). The player
+// axis is walked in chunks of kChunk; each chunk of u is staged in shared
+// memory once per CTA and every row of the block adds the u values of its
+// set bits in that chunk (warp per row, set-bit iteration), so each mask
+// word is read exactly once. Rows whose dot is not needed (odd rows of
+// complement pairs) are skipped. The epilogue applies the complement
+// shortcut (solver.cpp:261-263), writes v, and leaves the block's partial
+// sum of v^2 for a fixed-order reduction.
+constexpr uint32_t kFwdRows = 1024;
 
-// v_i = sw_i * dot_i; complement odd rows v = sw * (sum_u - dot_even);
-// dsq[j] = v_2j^2 + v_2j+1^2 (per pair, reduced later in fixed order)
-__global__ void forward_finish_kernel(const double* __restrict__ part,
-                                      uint32_t chunks, uint64_t nrows,
-                                      const uint8_t* __restrict__ is_comp,
-                                      const double* __restrict__ sw,
-                                      const double* __restrict__ sum_u,
-                                      double* __restrict__ v,
-                                      double* __restrict__ dsq) {
-  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (2 * j >= nrows) return;
-  const uint64_t e = 2 * j;
-  double de = 0.0, dot_o = 0.0;
-  for (uint32_t c = 0; c < chunks; ++c) de += part[uint64_t(c) * nrows + e];
-  const double ve = sw[e] * de;
-  double vo;
-  if (is_comp[j]) {
-    vo = sw[e + 1] * (*sum_u - de);
-  } else {
-    for (uint32_t c = 0; c < chunks; ++c) dot_o += part[uint64_t(c) * nrows + e + 1];
-    vo = sw[e + 1] * dot_o;
+__global__ void __launch_bounds__(256)
+    forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t nrows,
+                   const uint8_t* __restrict__ is_comp, const double* __restrict__ u,
+                   uint32_t n, const double* __restrict__ sw,
+                   const double* __restrict__ sum_u, double* __restrict__ v,
+                   double* __restrict__ dsq_part) {
+  extern __shared__ double su[];  // kChunk doubles
+  __shared__ double rowsum[kFwdRows];
+  __shared__ double red[8];
+  const uint64_t r0 = uint64_t(blockIdx.x) * kFwdRows;
+  const uint64_t left = nrows - r0;
+  const uint32_t nr = left < kFwdRows ? uint32_t(left) : kFwdRows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) rowsum[i] = 0.0;
+  for (uint32_t e0 = 0; e0 < n; e0 += kChunk) {
+    const uint32_t ce = min(n - e0, kChunk);
+    __syncthreads();  // the previous chunk's lookups are done
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < ce; i += blockDim.x) su[i] = u[e0 + i];
+    __syncthreads();
+    const uint32_t w0 = e0 / 64, w1 = min(W, (e0 + ce + 63) / 64);
+    for (uint32_t rl = warp; rl < nr; rl += 8) {
+      const uint64_t row = r0 + rl;
+      if ((row & 1) && is_comp[row >> 1]) continue;
+      const uint64_t* rp = rows + row * W;
+      double acc = 0.0;
+      for (uint32_t w = w0 + lane; w < w1; w += 32) {
+        uint64_t x = rp[w];
+        const uint32_t base = w * 64 - e0;
+        while (x) {
+          const int b = __ffsll(static_cast<long long>(x)) - 1;
+          x &= x - 1;
+          acc += su[base + b];
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) rowsum[rl] += acc;
+    }
   }
-  v[e] = ve;
-  v[e + 1] = vo;
-  dsq[j] = ve * ve + vo * vo;
+  __syncthreads();
+  double dsq = 0.0;
+  for (uint32_t jl = threadIdx.x; 2 * jl < nr; jl += blockDim.x) {
+    const uint64_t e = r0 + 2 * jl;
+    const double de = rowsum[2 * jl];
+    const double ve = sw[e] * de;
+    const double vo = is_comp[e >> 1] ? sw[e + 1] * (*sum_u - de) : sw[e + 1] * rowsum[2 * jl + 1];
+    v[e] = ve;
+    v[e + 1] = vo;
+    dsq += ve * ve + vo * vo;
+  }
+  dsq = warp_sum(dsq);
+  if (lane == 0) red[warp] = dsq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    dsq_part[blockIdx.x] = t;
+  }
 }
 
 // ---------------------------------------------------------------- updates
@@ -216,33 +224,55 @@ __global__ void coef_kernel(const double* __restrict__ sw, const double* __restr
     nz32[tile * 2 + ((row >> 5) & 1)] = b;
 }
 
-// s_part[split][e] = sum over tiles of the split, over set bits i of
-// (maskt[t][e] & nz[t]), of coef[t*64+i]
+// s_part[split][e] = sum over the split's tiles, over set bits i of
+// (maskt[t][e] & nz[t]), of coef[t*64+i]. Each thread owns two players;
+// kTT tiles are processed per step: their coefficients are staged in shared
+// memory while all 2*kTT mask words are already in flight.
+constexpr int kTT = 8;
+
 __global__ void __launch_bounds__(256)
     transpose_partial_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
                              uint32_t n, uint64_t tiles, uint64_t tiles_per_split,
                              const double* __restrict__ coef,
                              const uint64_t* __restrict__ nzmask,
                              double* __restrict__ s_part) {
-  __shared__ double sc[64];
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double sc[kTT][64];
+  __shared__ uint64_t snz[kTT];
+  const uint32_t ea = blockIdx.x * 512 + threadIdx.x, eb = ea + 256;
   const uint64_t t0 = blockIdx.y * tiles_per_split;
   const uint64_t t1 = min(tiles, t0 + tiles_per_split);
-  double acc = 0.0;
-  for (uint64_t t = t0; t < t1; ++t) {
+  double acc_a = 0.0, acc_b = 0.0;
+  for (uint64_t tb = t0; tb < t1; tb += kTT) {
+    const int nt = (t1 - tb) < uint64_t(kTT) ? int(t1 - tb) : kTT;
+    uint64_t wa[kTT], wb[kTT];
+#pragma unroll
+    for (int q = 0; q < kTT; ++q) {
+      wa[q] = (q < nt && ea < n) ? maskt[(tb + q) * Wp + ea] : 0ull;
+      wb[q] = (q < nt && eb < n) ? maskt[(tb + q) * Wp + eb] : 0ull;
+    }
+    __syncthreads();  // the previous step's coefficients are consumed
+    for (int idx = threadIdx.x; idx < nt * 64; idx += blockDim.x) sc[idx >> 6][idx & 63] = coef[tb * 64 + idx];
+    if (threadIdx.x < nt) snz[threadIdx.x] = nzmask[tb + threadIdx.x];
     __syncthreads();
-    if (threadIdx.x < 64) sc[threadIdx.x] = coef[t * 64 + threadIdx.x];
-    __syncthreads();
-    if (e < n) {
-      uint64_t x = maskt[t * Wp + e] & nzmask[t];
+#pragma unroll
+    for (int q = 0; q < kTT; ++q) {
+      const uint64_t nz = q < nt ? snz[q] : 0ull;
+      uint64_t x = wa[q] & nz;
       while (x) {
         const int b = __ffsll(static_cast<long long>(x)) - 1;
         x &= x - 1;
-        acc += sc[b];
+        acc_a += sc[q][b];
+      }
+      x = wb[q] & nz;
+      while (x) {
+        const int b = __ffsll(static_cast<long long>(x)) - 1;
+        x &= x - 1;
+        acc_b += sc[q][b];
       }
     }
   }
-  if (e < n) s_part[uint64_t(blockIdx.y) * n + e] = acc;
+  if (ea < n) s_part[uint64_t(blockIdx.y) * n + ea] = acc_a;
+  if (eb < n) s_part[uint64_t(blockIdx.y) * n + eb] = acc_b;
 }
 
 // s_e = K + sum_split s_part[split][e]
@@ -375,18 +405,18 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint32_t W = in.W;
   const uint64_t tiles = (rows + 63) / 64;
   const uint64_t Wp = uint64_t(W) * 64;
-  const uint32_t chunks = (n + kChunk - 1) / kChunk;
   int sms = 148;
   SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
   // transpose grid: player blocks x tile splits ~ 8 CTAs per SM
-  const uint64_t pblocks = (n + 255) / 256;
+  const uint64_t pblocks = (n + 511) / 512;
   const uint64_t want_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
   const uint64_t tiles_per_split =
       std::max<uint64_t>(1, (tiles + want_splits - 1) / want_splits);
   const uint32_t splits = uint32_t((tiles + tiles_per_split - 1) / tiles_per_split);
 
   // scratch layout
-  const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + uint64_t(chunks) * rows * 8 +
+  const uint64_t fblocks = (rows + kFwdRows - 1) / kFwdRows;
+  const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + fblocks * 8 +
                          tiles * 64 * 8 + tiles * 8 + pairs * 8 * 2 + uint64_t(splits) * n * 8 +
                          uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
   ctx.solver_work.reserve(bytes);
@@ -397,8 +427,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* v = sc.take<double>(rows);
   double* coef = sc.take<double>(tiles * 64);
   uint64_t* nz = sc.take<uint64_t>(tiles);
-  double* part = sc.take<double>(uint64_t(chunks) * rows);
-  double* dsq = sc.take<double>(pairs);
+  double* dsq = sc.take<double>(fblocks);
   double* kc = sc.take<double>(pairs);
   double* s_part = sc.take<double>(uint64_t(splits) * n);
   double* s = sc.take<double>(n);
@@ -448,7 +477,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       SF_LAUNCHED(ctx);
     }
     reduce(kc, pairs, 0, 0.0, scal + 4);
-    dim3 grid(blocks_for(n), splits);
+    dim3 grid(unsigned(pblocks), splits);
     transpose_partial_kernel<<<grid, 256, 0, st>>>(maskt, Wp, n, tiles, tiles_per_split, coef,
                                                    nz, s_part);
     SF_LAUNCHED(ctx);
@@ -463,17 +492,13 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     reduce(u, n, 0, 0.0, scal + 0);  // sum_u
     if (rows) {
       const size_t smem = size_t(std::min<uint32_t>(n, kChunk)) * 8;
-      SF_CUDA(cudaFuncSetAttribute(forward_partial_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChunk * 8)));
-      const uint64_t want = (rows + 7) / 8;
-      dim3 grid(unsigned(std::min<uint64_t>(want, uint64_t(sms) * 4)), chunks);
-      forward_partial_kernel<<<grid, 256, smem, st>>>(in.dev_rows, W, rows, is_comp, u, n, part);
-      SF_LAUNCHED(ctx);
-      forward_finish_kernel<<<blocks_for(pairs), 256, 0, st>>>(part, chunks, rows, is_comp,
-                                                                in.dev_sw, scal + 0, v, dsq);
+      SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kChunk * 8)));
+      forward_kernel<<<unsigned(fblocks), 256, smem, st>>>(in.dev_rows, W, rows, is_comp, u, n,
+                                                           in.dev_sw, scal + 0, v, dsq);
       SF_LAUNCHED(ctx);
     }
-    reduce(dsq, pairs, 0, 0.0, scal + 1);
+    reduce(dsq, fblocks, 0, 0.0, scal + 1);
     comm_allreduce_sum(ctx, scal + 1, 1);
     fetch(0, 2);
     delta = host[1];

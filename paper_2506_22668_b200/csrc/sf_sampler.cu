@@ -45,15 +45,25 @@ __device__ __forceinline__ uint32_t find_class(const ClassTable& ct,
 struct SmemSet {
   uint64_t* w;
   __device__ bool test(uint32_t t) const { return (w[t >> 6] >> (t & 63)) & 1ull; }
-  __device__ void set(uint32_t t) const {
-    atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), 1ull << (t & 63));
+  __device__ bool test_and_set(uint32_t t) const {
+    const unsigned long long b = 1ull << (t & 63);
+    return atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), b) & b;
+  }
+  __device__ void set(uint32_t t) const { test_and_set(t); }
+  __device__ void clear(uint32_t t) const {
+    atomicAnd(reinterpret_cast<unsigned long long*>(&w[t >> 6]), ~(1ull << (t & 63)));
   }
 };
 struct GmemSet {
   uint64_t* w;
   __device__ bool test(uint32_t t) const { return (__ldcg(&w[t >> 6]) >> (t & 63)) & 1ull; }
-  __device__ void set(uint32_t t) const {
-    atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), 1ull << (t & 63));
+  __device__ bool test_and_set(uint32_t t) const {
+    const unsigned long long b = 1ull << (t & 63);
+    return atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), b) & b;
+  }
+  __device__ void set(uint32_t t) const { test_and_set(t); }
+  __device__ void clear(uint32_t t) const {
+    atomicAnd(reinterpret_cast<unsigned long long*>(&w[t >> 6]), ~(1ull << (t & 63)));
   }
 };
 
@@ -61,9 +71,13 @@ struct GmemSet {
 // insert t, or m when t is already present. The warp draws 64 consecutive
 // values at once (lane i owns Philox block base/2 + i, i.e. draws base+2i
 // and base+2i+1), tests them against the set as it stood before the chunk,
-// then replays the chunk in order with shuffles so that a draw colliding
-// with an earlier pick of the same chunk resolves exactly as the
-// sequential loop would.
+// inserts the provisional picks (t, or m when t was already present). The
+// sequential loop picks something else only when a draw hits an earlier
+// pick of the same chunk, and then two provisional picks coincide (a
+// provisional pick is never in the pre-chunk set: t only when absent, m
+// above every earlier pick). So a clash seen by the atomic inserts is
+// exactly the case that needs the in-order replay: the chunk's inserts are
+// undone and the chunk is replayed with shuffles.
 template <typename Set>
 __device__ void floyd_warp(const Set& set, uint32_t n, uint32_t s,
                            uint64_t seed, uint64_t g, int lane) {
@@ -79,17 +93,27 @@ __device__ void floyd_warp(const Set& set, uint32_t n, uint32_t s,
     __syncwarp();
     bool hit0 = v0 && set.test(t0);
     bool hit1 = v1 && set.test(t1);
-    const uint32_t chunk = min(64u, s - base);
-    for (uint32_t k = 0; k < chunk; ++k) {
-      const int owner = k >> 1;
-      uint32_t pk = (k & 1) ? (hit1 ? mm1 : t1) : (hit0 ? mm0 : t0);
-      pk = __shfl_sync(kFull, pk, owner);
-      // later draws of this chunk that drew the value just picked
-      if (i0 > base + k && t0 == pk) hit0 = true;
-      if (i1 > base + k && t1 == pk) hit1 = true;
+    __syncwarp();
+    bool clash = false;
+    if (v0) clash |= set.test_and_set(hit0 ? mm0 : t0);
+    if (v1) clash |= set.test_and_set(hit1 ? mm1 : t1);
+    if (__any_sync(kFull, clash)) {
+      __syncwarp();
+      if (v0) set.clear(hit0 ? mm0 : t0);
+      if (v1) set.clear(hit1 ? mm1 : t1);
+      __syncwarp();
+      const uint32_t chunk = min(64u, s - base);
+      for (uint32_t k = 0; k < chunk; ++k) {
+        const int owner = k >> 1;
+        uint32_t pk = (k & 1) ? (hit1 ? mm1 : t1) : (hit0 ? mm0 : t0);
+        pk = __shfl_sync(kFull, pk, owner);
+        // later draws of this chunk that drew the value just picked
+        if (i0 > base + k && t0 == pk) hit0 = true;
+        if (i1 > base + k && t1 == pk) hit1 = true;
+      }
+      if (v0) set.set(hit0 ? mm0 : t0);
+      if (v1) set.set(hit1 ? mm1 : t1);
     }
-    if (v0) set.set(hit0 ? mm0 : t0);
-    if (v1) set.set(hit1 ? mm1 : t1);
     __syncwarp();
   }
 }

@@ -87,6 +87,6 @@ def test_c2_shard_properties_and_slices(ctx, port):
     total = int(pp["first"][-1] + pp["pairs"][-1])
     for g0 in [0, 200_000, 248_000, 249_900]:
         want = port.generate_masks(n, pp, seed, 0, world, g0, min(total, g0 + 8 * 24))
-        j0 = g0 // world
+        j0 = (g0 + world - 1) // world  # first local pair (rank 0) at or after g0
         assert (bits[2 * j0: 2 * j0 + want.shape[0]] == want).all()
     assert bits.shape[1] == W
