@@ -111,7 +111,7 @@ __global__ void init_r_kernel(const double* __restrict__ sw,
 constexpr uint32_t kFwdRows = 1024;
 
 __global__ void __launch_bounds__(256)
-    forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t nrows,
+    forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t nrows, uint32_t rpc,
                    const uint8_t* __restrict__ is_comp, const double* __restrict__ u,
                    uint32_t n, const double* __restrict__ sw,
                    const double* __restrict__ sum_u, double* __restrict__ v,
@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(256)
   extern __shared__ double su[];  // kChunk doubles
   __shared__ double rowsum[kFwdRows];
   __shared__ double red[8];
-  const uint64_t r0 = uint64_t(blockIdx.x) * kFwdRows;
+  const uint64_t r0 = uint64_t(blockIdx.x) * rpc;
   const uint64_t left = nrows - r0;
-  const uint32_t nr = left < kFwdRows ? uint32_t(left) : kFwdRows;
+  const uint32_t nr = left < rpc ? uint32_t(left) : rpc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) rowsum[i] = 0.0;
   for (uint32_t e0 = 0; e0 < n; e0 += kChunk) {
@@ -415,7 +415,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint32_t splits = uint32_t((tiles + tiles_per_split - 1) / tiles_per_split);
 
   // scratch layout
-  const uint64_t fblocks = (rows + kFwdRows - 1) / kFwdRows;
+  // rows per forward CTA: even, <= kFwdRows, enough CTAs for ~4 per SM
+  uint32_t rpc = uint32_t(std::min<uint64_t>(kFwdRows, std::max<uint64_t>(64, (rows + 4ull * sms - 1) / (4ull * sms))));
+  rpc = (rpc + 1) & ~1u;
+  const uint64_t fblocks = (rows + rpc - 1) / rpc;
   const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + fblocks * 8 +
                          tiles * 64 * 8 + tiles * 8 + pairs * 8 * 2 + uint64_t(splits) * n * 8 +
                          uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
@@ -494,7 +497,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       const size_t smem = size_t(std::min<uint32_t>(n, kChunk)) * 8;
       SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kChunk * 8)));
-      forward_kernel<<<unsigned(fblocks), 256, smem, st>>>(in.dev_rows, W, rows, is_comp, u, n,
+      forward_kernel<<<unsigned(fblocks), 256, smem, st>>>(in.dev_rows, W, rows, rpc, is_comp, u, n,
                                                            in.dev_sw, scal + 0, v, dsq);
       SF_LAUNCHED(ctx);
     }

@@ -134,7 +134,7 @@ __device__ __forceinline__ void consumer_sync() {
 // euv (mask player of the (u, v) edge, self entries only), flags bit0 =
 // first entry of a segment (x = v), bit1 = last entry of a segment
 template <int D>
-__global__ void __launch_bounds__(kConsumers + 32) __maxnreg__(D >= 256 ? 224 : 112)
+__global__ void __launch_bounds__(kConsumers + 32) __maxnreg__(D >= 256 ? 224 : 96)
     fused_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
                  const float* __restrict__ isd, uint32_t V,
                  const float* __restrict__ P, const float* __restrict__ bias,
@@ -524,6 +524,9 @@ bool try_fused(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
   static bool configured = false;
   if (!configured) {
     SF_CUDA(cudaFuncSetAttribute(fused_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    // two CTAs per SM need the maximum shared-memory carveout
+    SF_CUDA(cudaFuncSetAttribute(fused_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 int(cudaSharedmemCarveoutMaxShared)));
     configured = true;
   }
   dim3 grid(e.items, unsigned(nt));
