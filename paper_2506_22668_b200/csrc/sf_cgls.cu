@@ -92,6 +92,19 @@ __global__ void comp_flags_kernel(const uint64_t* __restrict__ rows, uint32_t W,
   if (lane == 0) is_comp[j] = ok ? 1 : 0;
 }
 
+// set bits per row (load-balancing weights for the matvec partitions)
+__global__ void rowpop_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t nrows,
+                              uint32_t* __restrict__ pop) {
+  const uint64_t row = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  uint32_t c = 0;
+  for (uint32_t w = lane; w < W; w += 32) c += __popcll(rows[row * W + w]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if (lane == 0) pop[row] = c;
+}
+
 __global__ void init_r_kernel(const double* __restrict__ sw,
                               const double* __restrict__ tgt, uint64_t rows,
                               double* __restrict__ r) {
@@ -100,7 +113,8 @@ __global__ void init_r_kernel(const double* __restrict__ sw,
 }
 
 // ---------------------------------------------------------------- M u
-// One CTA per block of kFwdRows rows (whole complement pairs). The player
+// One CTA per block of rows (whole complement pairs; block boundaries
+// balance the set-bit count, rows are ordered by coalition size). The player
 // axis is walked in chunks of kChunk; each chunk of u is staged in shared
 // memory once per CTA and every row of the block adds the u values of its
 // set bits in that chunk (warp per row, set-bit iteration), so each mask
@@ -111,7 +125,7 @@ __global__ void init_r_kernel(const double* __restrict__ sw,
 constexpr uint32_t kFwdRows = 1024;
 
 __global__ void __launch_bounds__(256)
-    forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t nrows, uint32_t rpc,
+    forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, const uint32_t* __restrict__ row_start,
                    const uint8_t* __restrict__ is_comp, const double* __restrict__ u,
                    uint32_t n, const double* __restrict__ sw,
                    const double* __restrict__ sum_u, double* __restrict__ v,
@@ -119,19 +133,26 @@ __global__ void __launch_bounds__(256)
   extern __shared__ double su[];  // kChunk doubles
   __shared__ double rowsum[kFwdRows];
   __shared__ double red[8];
-  const uint64_t r0 = uint64_t(blockIdx.x) * rpc;
-  const uint64_t left = nrows - r0;
-  const uint32_t nr = left < rpc ? uint32_t(left) : rpc;
+  __shared__ unsigned next_row;
+  const uint64_t r0 = row_start[blockIdx.x];
+  const uint32_t nr = row_start[blockIdx.x + 1] - uint32_t(r0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) rowsum[i] = 0.0;
   for (uint32_t e0 = 0; e0 < n; e0 += kChunk) {
     const uint32_t ce = min(n - e0, kChunk);
     __syncthreads();  // the previous chunk's lookups are done
+    if (threadIdx.x == 0) next_row = 0;
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < ce; i += blockDim.x) su[i] = u[e0 + i];
     __syncthreads();
     const uint32_t w0 = e0 / 64, w1 = min(W, (e0 + ce + 63) / 64);
-    for (uint32_t rl = warp; rl < nr; rl += 8) {
+    for (;;) {
+      // dynamic row fetch, largest coalitions (end of the block) first
+      unsigned f = 0;
+      if (lane == 0) f = atomicAdd(&next_row, 1u);
+      f = __shfl_sync(kFull, f, 0);
+      if (f >= nr) break;
+      const uint32_t rl = nr - 1 - f;
       const uint64_t row = r0 + rl;
       if ((row & 1) && is_comp[row >> 1]) continue;
       const uint64_t* rp = rows + row * W;
@@ -232,15 +253,14 @@ constexpr int kTT = 8;
 
 __global__ void __launch_bounds__(256)
     transpose_partial_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
-                             uint32_t n, uint64_t tiles, uint64_t tiles_per_split,
+                             uint32_t n, const uint32_t* __restrict__ split_start,
                              const double* __restrict__ coef,
                              const uint64_t* __restrict__ nzmask,
                              double* __restrict__ s_part) {
   __shared__ double sc[kTT][64];
   __shared__ uint64_t snz[kTT];
   const uint32_t ea = blockIdx.x * 512 + threadIdx.x, eb = ea + 256;
-  const uint64_t t0 = blockIdx.y * tiles_per_split;
-  const uint64_t t1 = min(tiles, t0 + tiles_per_split);
+  const uint64_t t0 = split_start[blockIdx.y], t1 = split_start[blockIdx.y + 1];
   double acc_a = 0.0, acc_b = 0.0;
   for (uint64_t tb = t0; tb < t1; tb += kTT) {
     const int nt = (t1 - tb) < uint64_t(kTT) ? int(t1 - tb) : kTT;
@@ -407,20 +427,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t Wp = uint64_t(W) * 64;
   int sms = 148;
   SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
-  // transpose grid: player blocks x tile splits ~ 8 CTAs per SM
-  const uint64_t pblocks = (n + 511) / 512;
-  const uint64_t want_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
-  const uint64_t tiles_per_split =
-      std::max<uint64_t>(1, (tiles + want_splits - 1) / want_splits);
-  const uint32_t splits = uint32_t((tiles + tiles_per_split - 1) / tiles_per_split);
-
-  // scratch layout
-  // rows per forward CTA: even, <= kFwdRows, enough CTAs for ~4 per SM
-  uint32_t rpc = uint32_t(std::min<uint64_t>(kFwdRows, std::max<uint64_t>(64, (rows + 4ull * sms - 1) / (4ull * sms))));
-  rpc = (rpc + 1) & ~1u;
-  const uint64_t fblocks = (rows + rpc - 1) / rpc;
-  const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + fblocks * 8 +
-                         tiles * 64 * 8 + tiles * 8 + pairs * 8 * 2 + uint64_t(splits) * n * 8 +
+  const uint64_t pblocks = (n + 511) / 512;  // transpose: 512 players per CTA
+  const uint64_t max_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
+  const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2;
+  const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + fblocks_max * 8 + rows * 4 +
+                         (fblocks_max + max_splits + 2) * 4 + tiles * 64 * 8 + tiles * 8 + pairs * 8 * 2 +
+                         max_splits * n * 8 +
                          uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
   ctx.solver_work.reserve(bytes);
   Scratch sc{ctx.solver_work.p, 0};
@@ -430,9 +442,11 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* v = sc.take<double>(rows);
   double* coef = sc.take<double>(tiles * 64);
   uint64_t* nz = sc.take<uint64_t>(tiles);
-  double* dsq = sc.take<double>(fblocks);
+  double* dsq = sc.take<double>(fblocks_max);
+  uint32_t* pop = sc.take<uint32_t>(rows);
+  uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + 2);
   double* kc = sc.take<double>(pairs);
-  double* s_part = sc.take<double>(uint64_t(splits) * n);
+  double* s_part = sc.take<double>(max_splits * n);
   double* s = sc.take<double>(n);
   double* u = sc.take<double>(n);
   double* phi = sc.take<double>(n);
@@ -467,7 +481,65 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     SF_LAUNCHED(ctx);
     init_r_kernel<<<blocks_for(rows), 256, 0, st>>>(in.dev_sw, in.dev_targets, rows, r);
     SF_LAUNCHED(ctx);
+    rowpop_kernel<<<blocks_for(rows * 32), 256, 0, st>>>(in.dev_rows, W, rows, pop);
+    SF_LAUNCHED(ctx);
   }
+  // Load balance (rows are ordered by coalition size, so uniform splits put
+  // every dense row in the last blocks): forward row blocks and transpose
+  // tile splits are cut at equal cumulative set-bit cost, once per solve.
+  std::vector<uint32_t> h_pop(rows);
+  std::vector<uint8_t> h_comp(pairs);
+  if (rows) {
+    SF_CUDA(cudaMemcpyAsync(h_pop.data(), pop, rows * 4, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaMemcpyAsync(h_comp.data(), is_comp, pairs, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+    ctx.d2h_bytes += rows * 4 + pairs;
+  }
+  auto needed = [&](uint64_t row) { return !((row & 1) && h_comp[row >> 1]); };
+  std::vector<uint32_t> bounds{0};
+  {
+    const uint64_t wcost = (W + 31) / 32 * 4 + 16;  // word loads + row overhead per needed row
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < rows; ++i) total += needed(i) ? h_pop[i] + wcost : 1;
+    const uint64_t target = std::max<uint64_t>(1, total / (4ull * sms));
+    uint64_t acc = 0;
+    for (uint64_t i = 0; i < rows; i += 2) {
+      acc += (needed(i) ? h_pop[i] + wcost : 1) + (needed(i + 1) ? h_pop[i + 1] + wcost : 1);
+      const uint64_t cur = i + 2 - bounds.back();
+      if (acc >= target || cur >= kFwdRows) {
+        bounds.push_back(uint32_t(i + 2));
+        acc = 0;
+      }
+    }
+    if (bounds.back() != rows) bounds.push_back(uint32_t(rows));
+  }
+  const uint64_t fblocks = bounds.size() - 1;
+  std::vector<uint32_t> sbounds{0};
+  {
+    std::vector<uint64_t> tcost(tiles, n / 8 + 64);
+    for (uint64_t i = 0; i < rows; ++i)
+      if (needed(i)) tcost[i / 64] += h_pop[i];
+    uint64_t total = 0;
+    for (uint64_t c : tcost) total += c;
+    const uint64_t target = std::max<uint64_t>(1, (total + max_splits - 1) / max_splits);
+    uint64_t acc = 0;
+    for (uint64_t t = 0; t < tiles; ++t) {
+      acc += tcost[t];
+      if (acc >= target && sbounds.size() < max_splits) {
+        sbounds.push_back(uint32_t(t + 1));
+        acc = 0;
+      }
+    }
+    if (sbounds.back() != tiles) sbounds.push_back(uint32_t(tiles));
+  }
+  const uint32_t splits = uint32_t(sbounds.size() - 1);
+  const uint32_t* row_start = d_bounds;
+  const uint32_t* split_start = d_bounds + bounds.size();
+  SF_CUDA(cudaMemcpyAsync(d_bounds, bounds.data(), bounds.size() * 4, cudaMemcpyHostToDevice, st));
+  SF_CUDA(cudaMemcpyAsync(d_bounds + bounds.size(), sbounds.data(), sbounds.size() * 4,
+                          cudaMemcpyHostToDevice, st));
+  ctx.h2d_bytes += (bounds.size() + sbounds.size()) * 4;
+  SF_CUDA(cudaStreamSynchronize(st));
   const double scw = std::sqrt(in.constraint_weight);
   double r_c = scw * in.constraint_target;
 
@@ -481,7 +553,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     }
     reduce(kc, pairs, 0, 0.0, scal + 4);
     dim3 grid(unsigned(pblocks), splits);
-    transpose_partial_kernel<<<grid, 256, 0, st>>>(maskt, Wp, n, tiles, tiles_per_split, coef,
+    transpose_partial_kernel<<<grid, 256, 0, st>>>(maskt, Wp, n, split_start, coef,
                                                    nz, s_part);
     SF_LAUNCHED(ctx);
     transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits, n, scal + 4, s);
@@ -497,7 +569,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       const size_t smem = size_t(std::min<uint32_t>(n, kChunk)) * 8;
       SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kChunk * 8)));
-      forward_kernel<<<unsigned(fblocks), 256, smem, st>>>(in.dev_rows, W, rows, rpc, is_comp, u, n,
+      forward_kernel<<<unsigned(fblocks), 256, smem, st>>>(in.dev_rows, W, row_start, is_comp, u, n,
                                                            in.dev_sw, scal + 0, v, dsq);
       SF_LAUNCHED(ctx);
     }
