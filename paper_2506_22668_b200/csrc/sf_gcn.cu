@@ -284,6 +284,207 @@ __global__ void __launch_bounds__(kConsumers + 32) __maxnreg__(D >= 256 ? 224 : 
     reinterpret_cast<float4*>(out + uint64_t(cg * Cfg::CB + j) * D)[fg] = acc[j];
 }
 
+// Wide variant for D in {32, 64, 128}: two tiles (128 coalitions) per CTA,
+// each consumer thread owns 8 features of CB coalitions (64 FFMA per entry
+// for D = 128), so every staged P row serves 128 coalitions and the FMA
+// density per issued instruction doubles. The per-u accumulators live in
+// shared memory (thread-strided, conflict-free) and are touched only at
+// segment ends; the open segment's partial sums stay in registers.
+template <int D>
+struct WideCfg {
+  static constexpr int TPC = 2;                  // tiles per CTA
+  static constexpr int CO = kTile * TPC;          // coalitions per CTA
+  static constexpr int FG = D / 8;                // threads per feature row
+  static constexpr int CGS = kConsumers / FG;     // coalition groups
+  static constexpr int CB = CO / CGS;             // coalitions per thread
+  static constexpr int STAGES = 3;
+  static constexpr int OFF_P = kChunkEntries * 16;
+  static constexpr int OFF_ISD = OFF_P + kChunkEntries * D * 4;
+  static constexpr int OFF_W = OFF_ISD + kChunkEntries * CO * 4;
+  static constexpr int OFF_COEF = OFF_W + kChunkEntries * TPC * 32;
+  static constexpr int OFF_FLAGS = OFF_COEF + kChunkEntries * CO * 4;
+  static constexpr int STAGE_BYTES = OFF_FLAGS + 16;
+  static constexpr int ACC_BYTES = kConsumers * CB * 8 * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + ACC_BYTES + 2 * STAGES * 8;
+  static_assert(D % 8 == 0 && FG <= 32 && CO % CGS == 0 && CB >= 1, "shape");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+template <int D>
+__global__ void __launch_bounds__(kConsumers + 32, 1)
+    fused_wide_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
+                      const float* __restrict__ isd, uint32_t V,
+                      const float* __restrict__ P, const float* __restrict__ bias,
+                      const uint4* __restrict__ ent, const uint32_t* __restrict__ item_ent,
+                      const uint32_t* __restrict__ item_order, uint32_t items,
+                      float* __restrict__ Apart) {
+  using Cfg = WideCfg<D>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* accs = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::ACC_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  const uint32_t item = item_order[blockIdx.x];
+  const uint64_t t = uint64_t(blockIdx.y) * Cfg::TPC;  // first tile of the pair
+  const int tid = threadIdx.x;
+  const uint32_t e0 = item_ent[item], e1 = item_ent[item + 1];
+  const uint32_t nchunks = (e1 - e0 + kChunkEntries - 1) / kChunkEntries;
+  if (tid == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < kConsumers * Cfg::CB * 8; i += blockDim.x) accs[i] = 0.f;
+  __syncthreads();
+
+  if (tid >= kConsumers) {
+    // ------------------------------------------------------------ producer
+    const int lane = tid - kConsumers;
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      const int s = c % Cfg::STAGES;
+      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
+      unsigned char* st = smem + s * Cfg::STAGE_BYTES;
+      const uint32_t base = e0 + c * kChunkEntries;
+      const bool on = base + lane < e1;
+      uint4 rec = make_uint4(0, kSelf, kSelf, 0);
+      uint32_t bytes = 0;
+      if (on) {
+        rec = ent[base + lane];
+        bytes = D * 4 + Cfg::TPC * (kTile * 4 + (rec.y != kSelf ? 16 : 0) + (rec.z != kSelf ? 16 : 0));
+        reinterpret_cast<uint4*>(st)[lane] = rec;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
+      const uint32_t startm = __ballot_sync(kFull, on && (rec.w & 1u));
+      const uint32_t endm = __ballot_sync(kFull, on && (rec.w & 2u));
+      if (lane == 0) {
+        reinterpret_cast<uint32_t*>(st + Cfg::OFF_FLAGS)[0] = startm;
+        reinterpret_cast<uint32_t*>(st + Cfg::OFF_FLAGS)[1] = endm;
+        mbar_arrive_expect_tx(&full[s], bytes);
+      }
+      __syncwarp();
+      if (on) {
+        bulk_g2s(st + Cfg::OFF_P + lane * D * 4, P + uint64_t(rec.x) * D, D * 4, &full[s]);
+#pragma unroll
+        for (int q = 0; q < Cfg::TPC; ++q) {
+          const uint64_t* mt = maskt + (t + q) * Wp;
+          const float* isd_t = isd + (t + q) * uint64_t(V) * kTile;
+          bulk_g2s(st + Cfg::OFF_ISD + (lane * Cfg::CO + q * kTile) * 4, isd_t + uint64_t(rec.x) * kTile,
+                   kTile * 4, &full[s]);
+          if (rec.y != kSelf)
+            bulk_g2s(st + Cfg::OFF_W + (lane * Cfg::TPC + q) * 32, mt + (rec.y & ~1u), 16, &full[s]);
+          if (rec.z != kSelf)
+            bulk_g2s(st + Cfg::OFF_W + (lane * Cfg::TPC + q) * 32 + 16, mt + (rec.z & ~1u), 16, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int fg = tid % Cfg::FG, cg = tid / Cfg::FG;
+  const int c0i = cg * Cfg::CB;  // first coalition of this thread (0..127)
+  const float4 bv0 = reinterpret_cast<const float4*>(bias)[2 * fg];
+  const float4 bv1 = reinterpret_cast<const float4*>(bias)[2 * fg + 1];
+  float4 h0[Cfg::CB], h1[Cfg::CB];
+  float sv[Cfg::CB];
+  uint32_t dmask = 0;
+#pragma unroll
+  for (int j = 0; j < Cfg::CB; ++j) {
+    h0[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    h1[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sv[j] = 0.f;
+  }
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    const int s = c % Cfg::STAGES;
+    mbar_wait(&full[s], (c / Cfg::STAGES) & 1);
+    unsigned char* st = smem + s * Cfg::STAGE_BYTES;
+    const uint4* recs = reinterpret_cast<const uint4*>(st);
+    const float* Ps = reinterpret_cast<const float*>(st + Cfg::OFF_P);
+    const float* isds = reinterpret_cast<const float*>(st + Cfg::OFF_ISD);
+    const uint64_t* ws = reinterpret_cast<const uint64_t*>(st + Cfg::OFF_W);
+    float* coef = reinterpret_cast<float*>(st + Cfg::OFF_COEF);
+    const int cnt = int(min(uint32_t(kChunkEntries), e1 - (e0 + c * kChunkEntries)));
+    // coefficients m_i(e) isd_i(x) for the 128 coalitions of the chunk's entries
+    for (int idx = tid; idx < cnt * Cfg::CO; idx += kConsumers) {
+      const int k = idx / Cfg::CO, i = idx % Cfg::CO, q = i / kTile;
+      const uint32_t y = recs[k].y;
+      const bool kept = y == kSelf || ((ws[(k * Cfg::TPC + q) * 4 + (y & 1u)] >> (i % kTile)) & 1ull);
+      coef[idx] = kept ? isds[idx] : 0.f;
+    }
+    consumer_sync();
+    const uint32_t startm = reinterpret_cast<const uint32_t*>(st + Cfg::OFF_FLAGS)[0];
+    const uint32_t endm = reinterpret_cast<const uint32_t*>(st + Cfg::OFF_FLAGS)[1];
+    int k = 0;
+    while (k < cnt) {
+      if ((startm >> k) & 1u) {  // segment start: keep isd_i(v), m_i(e_uv) for my coalitions
+        const uint32_t z = recs[k].z;
+        dmask = 0;
+#pragma unroll
+        for (int j = 0; j < Cfg::CB; ++j) {
+          const int i = c0i + j;
+          sv[j] = isds[k * Cfg::CO + i];
+          const bool m = z == kSelf || ((ws[(k * Cfg::TPC + i / kTile) * 4 + 2 + (z & 1u)] >> (i % kTile)) & 1ull);
+          dmask |= uint32_t(m) << j;
+        }
+      }
+      const uint32_t rest = endm >> k;
+      const int stop = rest ? k + __ffs(int(rest)) - 1 : cnt - 1;
+#pragma unroll 2
+      for (; k <= stop; ++k) {
+        const float4 xa = reinterpret_cast<const float4*>(Ps + k * D)[2 * fg];
+        const float4 xb = reinterpret_cast<const float4*>(Ps + k * D)[2 * fg + 1];
+        const float* ckp = coef + k * Cfg::CO + c0i;
+#pragma unroll
+        for (int j = 0; j < Cfg::CB; ++j) {
+          const float cc = ckp[j];
+          h0[j].x = fmaf(cc, xa.x, h0[j].x);
+          h0[j].y = fmaf(cc, xa.y, h0[j].y);
+          h0[j].z = fmaf(cc, xa.z, h0[j].z);
+          h0[j].w = fmaf(cc, xa.w, h0[j].w);
+          h1[j].x = fmaf(cc, xb.x, h1[j].x);
+          h1[j].y = fmaf(cc, xb.y, h1[j].y);
+          h1[j].z = fmaf(cc, xb.z, h1[j].z);
+          h1[j].w = fmaf(cc, xb.w, h1[j].w);
+        }
+      }
+      if (rest) {  // segment end: A += m isd_i(v) relu(isd_i(v) h + b0)
+#pragma unroll
+        for (int j = 0; j < Cfg::CB; ++j) {
+          const float sj = sv[j];
+          const float dv = ((dmask >> j) & 1u) ? sj : 0.f;
+          float* a = accs + (j * 8) * kConsumers + tid;
+          a[0 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].x, bv0.x), 0.f), a[0 * kConsumers]);
+          a[1 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].y, bv0.y), 0.f), a[1 * kConsumers]);
+          a[2 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].z, bv0.z), 0.f), a[2 * kConsumers]);
+          a[3 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].w, bv0.w), 0.f), a[3 * kConsumers]);
+          a[4 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].x, bv1.x), 0.f), a[4 * kConsumers]);
+          a[5 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].y, bv1.y), 0.f), a[5 * kConsumers]);
+          a[6 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].z, bv1.z), 0.f), a[6 * kConsumers]);
+          a[7 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].w, bv1.w), 0.f), a[7 * kConsumers]);
+          h0[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          h1[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  // Apart[t'][item][i][f] for both tiles of the pair
+#pragma unroll
+  for (int j = 0; j < Cfg::CB; ++j) {
+    const int i = c0i + j;
+    const uint64_t tt = t + i / kTile;
+    float* out = Apart + ((tt * items + item) * kTile + (i % kTile)) * uint64_t(D);
+    const float* a = accs + (j * 8) * kConsumers + tid;
+    reinterpret_cast<float4*>(out)[2 * fg] =
+        make_float4(a[0 * kConsumers], a[1 * kConsumers], a[2 * kConsumers], a[3 * kConsumers]);
+    reinterpret_cast<float4*>(out)[2 * fg + 1] =
+        make_float4(a[4 * kConsumers], a[5 * kConsumers], a[6 * kConsumers], a[7 * kConsumers]);
+  }
+}
+
 // Softmax of z (float, max subtraction, sequential sum) as gcn.cpp:143-152.
 __device__ __forceinline__ void softmax_row(float* zi, uint32_t C) {
   float mx = zi[0];
@@ -537,6 +738,27 @@ bool try_fused(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
   return true;
 }
 
+template <int D>
+bool try_fused_wide(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
+                    uint64_t ntp, float* apart) {
+  if (e.dims[1] != uint64_t(D)) return false;
+  using Cfg = WideCfg<D>;
+  static bool configured = false;
+  if (!configured) {
+    SF_CUDA(cudaFuncSetAttribute(fused_wide_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM));
+    configured = true;
+  }
+  dim3 grid(e.items, unsigned(ntp / Cfg::TPC));
+  fused_wide_kernel<D><<<grid, kConsumers + 32, Cfg::SMEM, ctx.stream>>>(
+      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint4*>(e.ent.p), e.item_ent.p,
+      e.item_order.p, e.items, apart);
+  SF_LAUNCHED(ctx);
+  return true;
+}
+
+bool wide_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
+
 // Entry records and work items of the fused plan (see Engine / fused_kernel).
 void build_fused_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   const uint32_t U = uint32_t(e.ball[e.L - 2]);
@@ -659,7 +881,9 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   const uint64_t budget = 96ull << 20;  // keep a batch's intermediates L2-sized
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
-  T = std::min<uint64_t>(T, 65535);
+  T = std::min<uint64_t>(T, 65534);
+  const bool wide = e.fused && wide_width(e.dims[1]);
+  if (wide) T = (T + 1) & ~uint64_t(1);  // tile pairs: odd batches get an all-zero tile
   const uint64_t off_isd = T * Wp * 8;
   const uint64_t off_h0 = off_isd + T * uint64_t(e.V) * kTile * 4;
   const uint64_t off_h1 = off_h0 + T * hmax * 4;
@@ -679,9 +903,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
     const uint64_t nt = std::min(T, tiles - t0);
     const uint64_t row0 = t0 * kTile;
     const uint64_t nrows = std::min<uint64_t>(rows - row0, nt * kTile);
-    launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, nt, maskt);
+    const uint64_t ntp = wide ? (nt + 1) & ~uint64_t(1) : nt;  // tiles the fused kernel covers
+    launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, ntp, maskt);
     {
-      dim3 grid((e.V + 7) / 8, unsigned(nt));
+      dim3 grid((e.V + 7) / 8, unsigned(ntp));
       isd_kernel<<<grid, 256, 0, ctx.stream>>>(maskt, Wp, e.row_ptr.p, e.edge_player.p, e.V, isd);
       SF_LAUNCHED(ctx);
     }
@@ -703,7 +928,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         ctx.dom_pairs += nrows / 2;
         SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
       }
-      const bool ok = try_fused<128>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
+      const bool ok = (wide && (try_fused_wide<128>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
+                                try_fused_wide<64>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
+                                try_fused_wide<32>(ctx, e, maskt, Wp, isd, ntp, pbuf))) ||
+                      try_fused<128>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<64>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<32>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<16>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
