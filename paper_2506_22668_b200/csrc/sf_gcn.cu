@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sf_device.cuh"
 #include "sf_internal.hpp"
@@ -162,18 +163,21 @@ __global__ void __launch_bounds__(kConsumers + 32) __maxnreg__(D >= 256 ? 224 : 
   if (tid >= kConsumers) {
     // ------------------------------------------------------------ producer
     const int lane = tid - kConsumers;
+    uint4 rec_next = make_uint4(0, kSelf, kSelf, 0);
+    if (e0 + lane < e1) rec_next = ent[e0 + lane];
     const uint64_t* mt = maskt + t * Wp;
     const float* isd_t = isd + t * uint64_t(V) * kTile;
     for (uint32_t c = 0; c < nchunks; ++c) {
       const int s = c % Cfg::STAGES;
-      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
       unsigned char* st = smem + s * Cfg::STAGE_BYTES;
       const uint32_t base = e0 + c * kChunkEntries;
       const bool on = base + lane < e1;
-      uint4 rec = make_uint4(0, kSelf, kSelf, 0);
+      const uint4 rec = on ? rec_next : make_uint4(0, kSelf, kSelf, 0);
+      // prefetch the next chunk's records before waiting for a free stage
+      if (base + kChunkEntries + lane < e1) rec_next = ent[base + kChunkEntries + lane];
+      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
       uint32_t bytes = 0;
       if (on) {
-        rec = ent[base + lane];
         bytes = D * 4 + kTile * 4 + (rec.y != kSelf ? 16 : 0) + (rec.z != kSelf ? 16 : 0);
         reinterpret_cast<uint4*>(st)[lane] = rec;
       }
@@ -341,16 +345,19 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
   if (tid >= kConsumers) {
     // ------------------------------------------------------------ producer
     const int lane = tid - kConsumers;
+    uint4 rec_next = make_uint4(0, kSelf, kSelf, 0);
+    if (e0 + lane < e1) rec_next = ent[e0 + lane];
     for (uint32_t c = 0; c < nchunks; ++c) {
       const int s = c % Cfg::STAGES;
-      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
       unsigned char* st = smem + s * Cfg::STAGE_BYTES;
       const uint32_t base = e0 + c * kChunkEntries;
       const bool on = base + lane < e1;
-      uint4 rec = make_uint4(0, kSelf, kSelf, 0);
+      const uint4 rec = on ? rec_next : make_uint4(0, kSelf, kSelf, 0);
+      // prefetch the next chunk's records before waiting for a free stage
+      if (base + kChunkEntries + lane < e1) rec_next = ent[base + kChunkEntries + lane];
+      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
       uint32_t bytes = 0;
       if (on) {
-        rec = ent[base + lane];
         bytes = D * 4 + Cfg::TPC * (kTile * 4 + (rec.y != kSelf ? 16 : 0) + (rec.z != kSelf ? 16 : 0));
         reinterpret_cast<uint4*>(st)[lane] = rec;
       }
@@ -882,7 +889,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
   T = std::min<uint64_t>(T, 65534);
-  const bool wide = e.fused && wide_width(e.dims[1]);
+  // the wide variant (two tiles per CTA) measured slower than the narrow one
+  // on B200 (smem-bandwidth co-limited at 1 CTA/SM); opt in for A/B runs
+  static const bool narrow_only = std::getenv("SF_FUSED_WIDE") == nullptr;
+  const bool wide = e.fused && wide_width(e.dims[1]) && !narrow_only;
   if (wide) T = (T + 1) & ~uint64_t(1);  // tile pairs: odd batches get an all-zero tile
   const uint64_t off_isd = T * Wp * 8;
   const uint64_t off_h0 = off_isd + T * uint64_t(e.V) * kTile * 4;
