@@ -1,0 +1,448 @@
+// Tensor-core (tcgen05) variant of the fused layer-0 -> layer-1 kernel
+// (sf_gcn.cu "fused" documents the math). For a work item (u, segments
+// v of {u} u N(u)) and two tiles (M = 128 coalitions):
+//   H_v[m][:] = sum_{entries k of v} coef[k][m] * P[x_k][:]     (GEMM, K = entries)
+//   A_u[m][:] += m_m(e_uv) isd_m(v) relu(isd_m(v) H_v[m][:] + b0)  (per segment)
+// The GEMM runs as tcgen05.mma kind::tf32 in 3xTF32 form
+// (A_hi B_hi + A_hi B_lo + A_lo B_hi, FP32-level accuracy; a single TF32
+// product would miss the 1e-5 prediction bar), with the segment sums H_v
+// accumulated in TMEM. Segments are padded to multiples of 8 entries in the
+// plan (zero coefficients), so every segment is a whole number of MMA
+// k-steps.
+//
+// Warp roles (416 threads):
+//   warps 0-3   epilogue: per finished segment, tcgen05.ld H_v, fold it into
+//               the TMEM accumulator A_u, release the H buffer
+//   warps 4-11  staging: per 32-entry chunk build the A (coefficients,
+//               K-major) and B (gathered P rows, MN-major) operand tiles,
+//               hi/lo split, in the canonical no-swizzle layouts
+//   warp 12     one elected thread issues the MMAs and the commits
+// Pipelines: kStages smem stages (full/empty mbarriers), two TMEM H buffers
+// (hfull/hfree mbarriers).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "sf_device.cuh"
+#include "sf_internal.hpp"
+
+namespace sfb {
+
+namespace {
+
+constexpr int kTile = 64;
+constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
+constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
+constexpr int kM = 128;                  // coalitions per CTA (two tiles)
+constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
+constexpr int kStages = 3;
+constexpr int kEpiWarps = 4, kStgWarps = 8;
+constexpr int kThreads = (kEpiWarps + kStgWarps + 1) * 32;
+
+template <int D>
+struct TcCfg {
+  static constexpr int A_BYTES = kM * kKC * 4;        // one of hi / lo
+  static constexpr int B_SBO = (kKC / 8) * 128 + 16;   // n-group stride (+16 B: bank spread)
+  static constexpr int B_BYTES = (D / 4) * B_SBO;
+  static constexpr int OFF_ALO = A_BYTES;
+  static constexpr int OFF_BHI = 2 * A_BYTES;
+  static constexpr int OFF_BLO = 2 * A_BYTES + B_BYTES;
+  static constexpr int STAGE = ((2 * A_BYTES + 2 * B_BYTES + 127) / 128) * 128;
+  static constexpr int SMEM = kStages * STAGE + 8 * (2 * kStages + 4) + 16 + 128;
+  static constexpr uint32_t TMEM_COLS = 3 * D <= 256 ? 256 : 512;  // 2 H buffers + accumulator
+  static_assert(D % 32 == 0 && D <= 256, "width");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem], kind::tf32, cta_group::1
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Shared-memory matrix descriptor, no swizzle (SmemDescriptor, version 1)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // version (Blackwell)
+  return d;                // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+}
+
+#define TC_LD32(taddr, r)                                                                          \
+  asm volatile(                                                                                    \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                         \
+      : "r"(taddr))
+#define TC_ST32(taddr, r)                                                                          \
+  asm volatile(                                                                                    \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr), \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),      \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), \
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),           \
+      "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),           \
+      "r"(r[30]), "r"(r[31])                                                                       \
+      : "memory")
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// entry: (x, e) — P / isd row x, mask player e (kSelf: always kept, kPad:
+// coefficient 0). kflags[k-step]: bit0 segment start, bit1 segment end.
+// seg: (v, e_uv) per segment in item order.
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
+                    uint32_t V, const float* __restrict__ Phi, const float* __restrict__ Plo,
+                    const float* __restrict__ bias, const uint2* __restrict__ ent,
+                    const uint8_t* __restrict__ kflags, const uint2* __restrict__ seg,
+                    const uint32_t* __restrict__ item_ent, const uint32_t* __restrict__ item_seg,
+                    const uint32_t* __restrict__ item_order, uint32_t items,
+                    float* __restrict__ Apart) {
+  using Cfg = TcCfg<D>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::STAGE);
+  uint64_t* empty = full + kStages;
+  uint64_t* hfull = empty + kStages;
+  uint64_t* hfree = hfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t item = item_order[blockIdx.x];
+  const uint64_t t0 = uint64_t(blockIdx.y) * 2;  // tiles t0, t0+1
+  const uint32_t e0 = item_ent[item], e1 = item_ent[item + 1];
+  const uint32_t nchunks = (e1 - e0 + kKC - 1) / kKC;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kStgWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&hfull[b], 1);
+      mbar_init(&hfree[b], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= kEpiWarps && warp < kEpiWarps + kStgWarps) {
+    // ------------------------------------------------------------ staging
+    const int st_tid = tid - kEpiWarps * 32;  // 0..255
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      const int s = c % kStages;
+      if (c >= uint32_t(kStages)) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
+      unsigned char* st = smem + s * Cfg::STAGE;
+      const uint32_t base = e0 + c * kKC;
+      const int cnt = int(min(uint32_t(kKC), e1 - base));  // multiple of 8
+      // A: coefficients m_m(e) isd_m(x), K-major, unit (m, 4 entries)
+      for (int J = st_tid; J < kM * (cnt / 4); J += kStgWarps * 32) {
+        const int m = J & (kM - 1), u = J >> 7;
+        const uint64_t tile = t0 + (m >> 6);
+        const int i = m & 63;
+        const uint64_t* mt = maskt + tile * Wp;
+        const float* isd_t = isd + tile * uint64_t(V) * kTile;
+        float c4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint2 en = ent[base + 4 * u + q];
+          bool kept;
+          if (en.y == kSelf)
+            kept = true;
+          else if (en.y == kPad)
+            kept = false;
+          else
+            kept = (__ldg(&mt[en.y]) >> i) & 1ull;
+          c4[q] = kept ? __ldg(&isd_t[uint64_t(en.x) * kTile + i]) : 0.f;
+        }
+        float4 hi, lo;
+        hi.x = tf32_hi(c4[0]);
+        hi.y = tf32_hi(c4[1]);
+        hi.z = tf32_hi(c4[2]);
+        hi.w = tf32_hi(c4[3]);
+        lo.x = c4[0] - hi.x;
+        lo.y = c4[1] - hi.y;
+        lo.z = c4[2] - hi.z;
+        lo.w = c4[3] - hi.w;
+        const uint32_t off = u * 2048 + (m >> 3) * 128 + (m & 7) * 16;
+        *reinterpret_cast<float4*>(st + off) = hi;
+        *reinterpret_cast<float4*>(st + Cfg::OFF_ALO + off) = lo;
+      }
+      // B: gathered P rows, MN-major, unit (4 features, entry)
+      for (int J = st_tid; J < cnt * (D / 4); J += kStgWarps * 32) {
+        const int k = J / (D / 4), ng = J % (D / 4);
+        const uint32_t x = ent[base + k].x;
+        const float4 ph = __ldg(reinterpret_cast<const float4*>(Phi + uint64_t(x) * D) + ng);
+        const float4 pl = __ldg(reinterpret_cast<const float4*>(Plo + uint64_t(x) * D) + ng);
+        const uint32_t off = ng * Cfg::B_SBO + (k >> 3) * 128 + (k & 7) * 16;
+        *reinterpret_cast<float4*>(st + Cfg::OFF_BHI + off) = ph;
+        *reinterpret_cast<float4*>(st + Cfg::OFF_BLO + off) = pl;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else if (warp == kEpiWarps + kStgWarps) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // kind::tf32, D f32, A K-major, B MN-major, N = D, M = 128
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) |
+                             (uint32_t(kM >> 4) << 24);
+      uint32_t sg = 0, b = 0, acc = 0;
+      for (uint32_t c = 0; c < nchunks; ++c) {
+        const int s = c % kStages;
+        mbar_wait(&full[s], (c / kStages) & 1);
+        tc_fence_after();
+        const uint32_t base = e0 + c * kKC;
+        const int nk = int(min(uint32_t(kKC), e1 - base)) / 8;
+        const uint32_t sa = su32(smem + s * Cfg::STAGE);
+        for (int j = 0; j < nk; ++j) {
+          const uint8_t f = kflags[base / 8 + j];
+          if (f & 1u) {
+            b = sg & 1u;
+            if (sg >= 2) {
+              mbar_wait(&hfree[b], ((sg >> 1) - 1) & 1);
+              tc_fence_after();
+            }
+            acc = 0;
+          }
+          const uint32_t d = tmem + b * D;
+          const uint64_t ahi = smem_desc(sa + j * 4096, 2048, 128);
+          const uint64_t alo = smem_desc(sa + Cfg::OFF_ALO + j * 4096, 2048, 128);
+          const uint64_t bhi = smem_desc(sa + Cfg::OFF_BHI + j * 128, 128, Cfg::B_SBO);
+          const uint64_t blo = smem_desc(sa + Cfg::OFF_BLO + j * 128, 128, Cfg::B_SBO);
+          tc_mma(d, ahi, bhi, idesc, acc);
+          tc_mma(d, ahi, blo, idesc, 1);
+          tc_mma(d, alo, bhi, idesc, 1);
+          acc = 1;
+          if (f & 2u) {
+            tc_commit(&hfull[b]);
+            ++sg;
+          }
+        }
+        tc_commit(&empty[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp;  // TMEM lane quarter
+    const int m = q * 32 + lane;
+    const uint64_t tile = t0 + (m >> 6);
+    const int i = m & 63;
+    const uint64_t* mt = maskt + tile * Wp;
+    const float* isd_t = isd + tile * uint64_t(V) * kTile;
+    const uint32_t lane_base = uint32_t(q * 32) << 16;
+    const uint32_t acc_col = 2 * D;
+    uint32_t r[32], a[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a[j] = 0u;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) TC_ST32(tmem + lane_base + acc_col + cc * 32, a);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    const uint32_t s0 = item_seg[item], s1 = item_seg[item + 1];
+    for (uint32_t sg = 0; sg < s1 - s0; ++sg) {
+      const uint2 sv_e = seg[s0 + sg];
+      const float sv = __ldg(&isd_t[uint64_t(sv_e.x) * kTile + i]);
+      const bool muv = sv_e.y == kSelf || ((__ldg(&mt[sv_e.y]) >> i) & 1ull);
+      const float dv = muv ? sv : 0.f;
+      const uint32_t b = sg & 1u;
+      mbar_wait(&hfull[b], (sg >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cc = 0; cc < D / 32; ++cc) {
+        TC_LD32(tmem + lane_base + b * D + cc * 32, r);
+        TC_LD32(tmem + lane_base + acc_col + cc * 32, a);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const float4* b4 = reinterpret_cast<const float4*>(bias + cc * 32);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 bb = __ldg(b4 + j4);
+          const float bj[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int j = 4 * j4 + w;
+            const float hv = fmaxf(fmaf(sv, __uint_as_float(r[j]), bj[w]), 0.f);
+            a[j] = __float_as_uint(fmaf(dv, hv, __uint_as_float(a[j])));
+          }
+        }
+        TC_ST32(tmem + lane_base + acc_col + cc * 32, a);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hfree[b]);
+    }
+    // write the accumulator: Apart[tile][item][i][:]
+    float* out = Apart + ((tile * items + item) * kTile + i) * uint64_t(D);
+#pragma unroll 1
+    for (int cc = 0; cc < D / 32; ++cc) {
+      TC_LD32(tmem + lane_base + acc_col + cc * 32, a);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4)
+        reinterpret_cast<float4*>(out + cc * 32)[j4] =
+            make_float4(__uint_as_float(a[4 * j4]), __uint_as_float(a[4 * j4 + 1]),
+                        __uint_as_float(a[4 * j4 + 2]), __uint_as_float(a[4 * j4 + 3]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::TMEM_COLS));
+  }
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ x, uint64_t n, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const float h = tf32_hi(x[i]);
+  hi[i] = h;
+  lo[i] = x[i] - h;
+}
+
+template <int D>
+void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
+               uint64_t ntp, float* apart) {
+  using Cfg = TcCfg<D>;
+  static bool configured = false;
+  if (!configured) {
+    SF_CUDA(cudaFuncSetAttribute(fused_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    configured = true;
+  }
+  dim3 grid(e.tc_items, unsigned(ntp / 2));
+  fused_tc_kernel<D><<<grid, kThreads, Cfg::SMEM, ctx.stream>>>(
+      maskt, Wp, isd, e.V, e.p0_hi.p, e.p0_lo.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
+      e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
+      e.tc_item_order.p, e.tc_items, apart);
+  SF_LAUNCHED(ctx);
+}
+
+}  // namespace
+
+bool tc_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
+
+// Padded entries / k-step flags / segments / items for the tensor-core path.
+void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
+  const uint32_t U = uint32_t(e.ball[e.L - 2]);
+  constexpr uint64_t kItem = 512;
+  std::vector<uint32_t> ent;        // 2 words per entry
+  std::vector<uint8_t> kfl;         // per 8 entries
+  std::vector<uint32_t> segs;       // 2 words per segment
+  std::vector<uint32_t> item_ent{0}, item_seg{0}, u_items{0};
+  std::vector<uint64_t> work;
+  for (uint32_t u = 0; u < U; ++u) {
+    uint64_t open = 0;
+    auto close = [&]() {
+      if (ent.size() / 2 > item_ent.back()) {
+        item_ent.push_back(uint32_t(ent.size() / 2));
+        item_seg.push_back(uint32_t(segs.size() / 2));
+        work.push_back(open);
+        open = 0;
+      }
+    };
+    auto segment = [&](uint32_t v, uint32_t euv) {
+      const uint64_t w = sg.row_ptr[v + 1] - sg.row_ptr[v] + 1;
+      const uint64_t padded = (w + 7) / 8 * 8;
+      if (open && open + padded > kItem) close();
+      const size_t k0 = ent.size() / 2;
+      ent.insert(ent.end(), {v, kSelf});
+      for (uint64_t k = sg.row_ptr[v]; k < sg.row_ptr[v + 1]; ++k)
+        ent.insert(ent.end(), {sg.col[k], sg.edge_player[k]});
+      for (uint64_t k = w; k < padded; ++k) ent.insert(ent.end(), {v, kPad});
+      const size_t nk = padded / 8;
+      for (size_t j = 0; j < nk; ++j) kfl.push_back(uint8_t((j == 0 ? 1 : 0) | (j + 1 == nk ? 2 : 0)));
+      (void)k0;
+      segs.insert(segs.end(), {v, euv});
+      open += padded;
+    };
+    segment(u, kSelf);
+    for (uint64_t k = sg.row_ptr[u]; k < sg.row_ptr[u + 1]; ++k) segment(sg.col[k], sg.edge_player[k]);
+    close();
+    u_items.push_back(uint32_t(item_ent.size() - 1));
+  }
+  std::vector<uint32_t> order(work.size());
+  for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return work[a] > work[b]; });
+  e.tc_items = uint32_t(work.size());
+  e.tc_ent.upload(ent.data(), ent.size(), ctx.stream);
+  e.tc_kflags.upload(kfl.data(), kfl.size(), ctx.stream);
+  e.tc_seg.upload(segs.data(), segs.size(), ctx.stream);
+  e.tc_item_ent.upload(item_ent.data(), item_ent.size(), ctx.stream);
+  e.tc_item_seg.upload(item_seg.data(), item_seg.size(), ctx.stream);
+  e.tc_item_order.upload(order.data(), order.size(), ctx.stream);
+  e.tc_u_items.upload(u_items.data(), u_items.size(), ctx.stream);
+  // P0 split into TF32 hi + residual lo (3xTF32)
+  const uint64_t np = uint64_t(e.V) * e.dims[1];
+  e.p0_hi.reserve(np);
+  e.p0_lo.reserve(np);
+  split_tf32_kernel<<<unsigned((np + 255) / 256), 256, 0, ctx.stream>>>(e.p0.p, np, e.p0_hi.p, e.p0_lo.p);
+  SF_LAUNCHED(ctx);
+  ctx.h2d_bytes += ent.size() * 4 + kfl.size() + segs.size() * 4 +
+                   (item_ent.size() + item_seg.size() + order.size() + u_items.size()) * 4;
+  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+bool launch_fused_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
+                     uint64_t ntp, float* apart) {
+  switch (e.dims[1]) {
+    case 128: launch_tc<128>(ctx, e, maskt, Wp, isd, ntp, apart); return true;
+    case 64: launch_tc<64>(ctx, e, maskt, Wp, isd, ntp, apart); return true;
+    case 32: launch_tc<32>(ctx, e, maskt, Wp, isd, ntp, apart); return true;
+    default: return false;
+  }
+}
+
+}  // namespace sfb

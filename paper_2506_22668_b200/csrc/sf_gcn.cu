@@ -855,6 +855,10 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   SF_CUDA(cudaStreamSynchronize(ctx.stream));  // temporaries x, w0 die here
   e.fused = e.L >= 2 && fused_width(e.dims[1]) && e.n > 0;
   if (e.fused) build_fused_plan(ctx, e, sg);
+  // tensor-core fused kernel (A/B switch while it is validated)
+  static const bool use_tc = std::getenv("SF_FUSED_TC") != nullptr;
+  e.tc = e.fused && use_tc && tc_width(e.dims[1]);
+  if (e.tc) build_tc_plan(ctx, e, sg);
   e.sg_id = sg.id;
   e.model_id = m.id;
 }
@@ -878,7 +882,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   const int first_generic = e.fused ? 2 : 0;  // first layer the generic path runs
   uint64_t afused = 0;  // reduced layer-1 aggregation at U (fused path)
   if (e.fused) {
-    apart = uint64_t(e.items) * kTile * e.dims[1];
+    apart = uint64_t(std::max(e.items, e.tc_items)) * kTile * e.dims[1];
     afused = uint64_t(e.U) * kTile * e.dims[1];
     hmax = uint64_t(e.U) * kTile * e.dims[2];  // H at U (L >= 3) or logits (L == 2)
   }
@@ -892,7 +896,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   // the wide variant (two tiles per CTA) measured slower than the narrow one
   // on B200 (smem-bandwidth co-limited at 1 CTA/SM); opt in for A/B runs
   static const bool narrow_only = std::getenv("SF_FUSED_WIDE") == nullptr;
-  const bool wide = e.fused && wide_width(e.dims[1]) && !narrow_only;
+  const bool wide = (e.fused && wide_width(e.dims[1]) && !narrow_only) || e.tc;
   if (wide) T = (T + 1) & ~uint64_t(1);  // tile pairs: odd batches get an all-zero tile
   const uint64_t off_isd = T * Wp * 8;
   const uint64_t off_h0 = off_isd + T * uint64_t(e.V) * kTile * 4;
@@ -938,7 +942,8 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         ctx.dom_pairs += nrows / 2;
         SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
       }
-      const bool ok = (wide && (try_fused_wide<128>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
+      const bool ok = (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, ntp, pbuf)) ||
+                      (wide && (try_fused_wide<128>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
                                 try_fused_wide<64>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
                                 try_fused_wide<32>(ctx, e, maskt, Wp, isd, ntp, pbuf))) ||
                       try_fused<128>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
@@ -953,7 +958,8 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         const uint64_t work = uint64_t(e.U) * kTile * (K / 4);
         dim3 grid(unsigned((work + 255) / 256), unsigned(nt));
         reduce_partials_kernel<<<grid, 256, 0, ctx.stream>>>(
-            reinterpret_cast<const float4*>(pbuf), e.items, e.u_items.p, isd, e.V, K / 4, e.U,
+            reinterpret_cast<const float4*>(pbuf), e.tc ? e.tc_items : e.items,
+            e.tc ? e.tc_u_items.p : e.u_items.p, isd, e.V, K / 4, e.U,
             reinterpret_cast<float4*>(afbuf));
         SF_LAUNCHED(ctx);
       }

@@ -142,6 +142,12 @@ struct Engine {
   uint64_t entries = 0;
   DevBuf<uint32_t> ent;  // 4 words per entry: x, e, e_uv, flags
   DevBuf<uint32_t> item_ent, item_order, u_items;
+  // tensor-core (tcgen05) plan: segments padded to 8 entries (sf_fused_tc.cu)
+  bool tc = false;
+  uint32_t tc_items = 0;
+  DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items;
+  DevBuf<uint8_t> tc_kflags;
+  DevBuf<float> p0_hi, p0_lo;  // X W0 split for 3xTF32
 };
 
 struct CommStats {  // comm.hpp:13-19
@@ -230,6 +236,12 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m);
 void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                     uint32_t cls, float* dev_out, float* dev_allprobs,
                     float* dominant_ms);
+
+// sf_fused_tc.cu
+bool tc_width(uint64_t d);
+void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg);
+bool launch_fused_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp,
+                     const float* isd, uint64_t ntp, float* apart);
 
 // sf_cgls.cu
 struct CglsResult {
