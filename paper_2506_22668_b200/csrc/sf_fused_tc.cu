@@ -13,9 +13,11 @@
 // Warp roles (416 threads):
 //   warps 0-3   epilogue: per finished segment, tcgen05.ld H_v, fold it into
 //               the TMEM accumulator A_u, release the H buffer
-//   warps 4-11  staging: per 32-entry chunk build the A (coefficients,
-//               K-major) and B (gathered P rows, MN-major) operand tiles,
-//               hi/lo split, in the canonical no-swizzle layouts
+//   warps 4-11  staging: per 32-entry chunk build the A (coefficients) and
+//               B (gathered P rows, transposed) operand tiles, hi/lo split,
+//               both K-major in the canonical no-swizzle layout (MN-major
+//               tf32 without swizzle produced no output on B200; see
+//               csrc/tools/tc_probe.cu, which checks the layouts exactly)
 //   warp 12     one elected thread issues the MMAs and the commits
 // Pipelines: kStages smem stages (full/empty mbarriers), two TMEM H buffers
 // (hfull/hfree mbarriers).
@@ -43,8 +45,8 @@ constexpr int kThreads = (kEpiWarps + kStgWarps + 1) * 32;
 template <int D>
 struct TcCfg {
   static constexpr int A_BYTES = kM * kKC * 4;        // one of hi / lo
-  static constexpr int B_SBO = (kKC / 8) * 128 + 16;   // n-group stride (+16 B: bank spread)
-  static constexpr int B_BYTES = (D / 4) * B_SBO;
+  static constexpr int B_LBO = (D / 8) * 128;          // k-unit stride (n-groups of 8 rows)
+  static constexpr int B_BYTES = D * kKC * 4;
   static constexpr int OFF_ALO = A_BYTES;
   static constexpr int OFF_BHI = 2 * A_BYTES;
   static constexpr int OFF_BLO = 2 * A_BYTES + B_BYTES;
@@ -219,13 +221,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<float4*>(st + off) = hi;
         *reinterpret_cast<float4*>(st + Cfg::OFF_ALO + off) = lo;
       }
-      // B: gathered P rows, MN-major, unit (4 features, entry)
-      for (int J = st_tid; J < cnt * (D / 4); J += kStgWarps * 32) {
-        const int k = J / (D / 4), ng = J % (D / 4);
-        const uint32_t x = ent[base + k].x;
-        const float4 ph = __ldg(reinterpret_cast<const float4*>(Phi + uint64_t(x) * D) + ng);
-        const float4 pl = __ldg(reinterpret_cast<const float4*>(Plo + uint64_t(x) * D) + ng);
-        const uint32_t off = ng * Cfg::B_SBO + (k >> 3) * 128 + (k & 7) * 16;
+      // B: gathered P rows transposed to K-major, unit (feature n, 4 entries)
+      for (int J = st_tid; J < D * (cnt / 4); J += kStgWarps * 32) {
+        const int n = J % D, u = J / D;
+        float4 ph, pl;
+        const uint32_t x0 = ent[base + 4 * u].x, x1 = ent[base + 4 * u + 1].x;
+        const uint32_t x2 = ent[base + 4 * u + 2].x, x3 = ent[base + 4 * u + 3].x;
+        ph.x = __ldg(Phi + uint64_t(x0) * D + n);
+        ph.y = __ldg(Phi + uint64_t(x1) * D + n);
+        ph.z = __ldg(Phi + uint64_t(x2) * D + n);
+        ph.w = __ldg(Phi + uint64_t(x3) * D + n);
+        pl.x = __ldg(Plo + uint64_t(x0) * D + n);
+        pl.y = __ldg(Plo + uint64_t(x1) * D + n);
+        pl.z = __ldg(Plo + uint64_t(x2) * D + n);
+        pl.w = __ldg(Plo + uint64_t(x3) * D + n);
+        const uint32_t off = u * Cfg::B_LBO + (n >> 3) * 128 + (n & 7) * 16;
         *reinterpret_cast<float4*>(st + Cfg::OFF_BHI + off) = ph;
         *reinterpret_cast<float4*>(st + Cfg::OFF_BLO + off) = pl;
       }
@@ -236,8 +246,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kEpiWarps + kStgWarps) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      // kind::tf32, D f32, A K-major, B MN-major, N = D, M = 128
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) |
+      // kind::tf32, D f32, A and B K-major, N = D, M = 128
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(D >> 3) << 17) |
                              (uint32_t(kM >> 4) << 24);
       uint32_t sg = 0, b = 0, acc = 0;
       for (uint32_t c = 0; c < nchunks; ++c) {
@@ -260,8 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tmem + b * D;
           const uint64_t ahi = smem_desc(sa + j * 4096, 2048, 128);
           const uint64_t alo = smem_desc(sa + Cfg::OFF_ALO + j * 4096, 2048, 128);
-          const uint64_t bhi = smem_desc(sa + Cfg::OFF_BHI + j * 128, 128, Cfg::B_SBO);
-          const uint64_t blo = smem_desc(sa + Cfg::OFF_BLO + j * 128, 128, Cfg::B_SBO);
+          const uint64_t bhi = smem_desc(sa + Cfg::OFF_BHI + j * 2 * Cfg::B_LBO, Cfg::B_LBO, 128);
+          const uint64_t blo = smem_desc(sa + Cfg::OFF_BLO + j * 2 * Cfg::B_LBO, Cfg::B_LBO, 128);
           tc_mma(d, ahi, bhi, idesc, acc);
           tc_mma(d, ahi, blo, idesc, 1);
           tc_mma(d, alo, bhi, idesc, 1);
