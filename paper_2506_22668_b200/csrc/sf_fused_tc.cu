@@ -34,13 +34,15 @@ namespace sfb {
 namespace {
 
 constexpr int kTile = 64;
+constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
 constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
-constexpr int kStages = 3;
+constexpr int kRawStages = 2, kCanStages = 2;
 constexpr int kEpiWarps = 4, kStgWarps = 8;
-constexpr int kThreads = (kEpiWarps + kStgWarps + 1) * 32;
+constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + 1;
+constexpr int kThreads = (kMmaWarp + 1) * 32;
 
 template <int D>
 struct TcCfg {
@@ -50,8 +52,15 @@ struct TcCfg {
   static constexpr int OFF_ALO = A_BYTES;
   static constexpr int OFF_BHI = 2 * A_BYTES;
   static constexpr int OFF_BLO = 2 * A_BYTES + B_BYTES;
-  static constexpr int STAGE = ((2 * A_BYTES + 2 * B_BYTES + 127) / 128) * 128;
-  static constexpr int SMEM = kStages * STAGE + 8 * (2 * kStages + 4) + 16 + 128;
+  static constexpr int STAGE = ((2 * A_BYTES + 2 * B_BYTES + 1023) / 1024) * 1024;  // canonical tiles
+  // raw stage (bulk copies): records | P rows | isd rows (2 tiles) | mask blocks (2 tiles)
+  static constexpr int RAW_P = kKC * 8;
+  static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
+  static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
+  static constexpr int RAW = ((RAW_W + kKC * 2 * 16 + 127) / 128) * 128;
+  static constexpr int OFF_RAW = kCanStages * STAGE;
+  static constexpr int OFF_BARS = OFF_RAW + kRawStages * RAW;
+  static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
   static constexpr uint32_t TMEM_COLS = 3 * D <= 256 ? 256 : 512;  // 2 H buffers + accumulator
   static_assert(D % 32 == 0 && D <= 256, "width");
   static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -74,6 +83,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!p bra W_%=;\n\t}" ::"r"(su32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -138,19 +156,20 @@ __device__ __forceinline__ float tf32_hi(float x) {
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
-                    uint32_t V, const float* __restrict__ Phi, const float* __restrict__ Plo,
-                    const float* __restrict__ bias, const uint2* __restrict__ ent,
-                    const uint8_t* __restrict__ kflags, const uint2* __restrict__ seg,
-                    const uint32_t* __restrict__ item_ent, const uint32_t* __restrict__ item_seg,
-                    const uint32_t* __restrict__ item_order, uint32_t items,
-                    float* __restrict__ Apart) {
+                    uint32_t V, const float* __restrict__ P, const float* __restrict__ bias,
+                    const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
+                    const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
+                    const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
+                    uint32_t items, float* __restrict__ Apart) {
   using Cfg = TcCfg<D>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::STAGE);
-  uint64_t* empty = full + kStages;
-  uint64_t* hfull = empty + kStages;
-  uint64_t* hfree = hfull + 2;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BARS);
+  uint64_t* raw_full = bars;                   // producer (expect_tx) -> staging
+  uint64_t* raw_empty = raw_full + kRawStages;  // staging -> producer
+  uint64_t* can_full = raw_empty + kRawStages;  // staging -> MMA
+  uint64_t* can_empty = can_full + kCanStages;  // MMA commit -> staging
+  uint64_t* hfull = can_empty + kCanStages;     // MMA commit -> epilogue
+  uint64_t* hfree = hfull + 2;                  // epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t item = item_order[blockIdx.x];
@@ -159,9 +178,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t nchunks = (e1 - e0 + kKC - 1) / kKC;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], kStgWarps);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kRawStages; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], kStgWarps);
+    }
+    for (int s = 0; s < kCanStages; ++s) {
+      mbar_init(&can_full[s], kStgWarps);
+      mbar_init(&can_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
@@ -179,71 +202,97 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= kEpiWarps && warp < kEpiWarps + kStgWarps) {
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ producer
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      const int r = c % kRawStages;
+      if (c >= uint32_t(kRawStages)) mbar_wait(&raw_empty[r], ((c / kRawStages) - 1) & 1);
+      unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
+      const uint32_t base = e0 + c * kKC;
+      const int cnt = int(min(uint32_t(kKC), e1 - base));
+      uint2 en = make_uint2(0, kPad);
+      uint32_t bytes = 0;
+      if (lane < cnt) {
+        en = ent[base + lane];
+        bytes = D * 4 + 2 * kTile * 4 + ((en.y != kSelf && en.y != kPad) ? 2 * 16 : 0);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
+      bytes += cnt * 8;  // entry records
+      if (lane == 0) mbar_arrive_expect_tx(&raw_full[r], bytes);
+      __syncwarp();
+      if (lane == 0) bulk_g2s(rw, ent + base, cnt * 8, &raw_full[r]);
+      if (lane < cnt) {
+        bulk_g2s(rw + Cfg::RAW_P + lane * D * 4, P + uint64_t(en.x) * D, D * 4, &raw_full[r]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float* isd_t = isd + (t0 + q) * uint64_t(V) * kTile;
+          bulk_g2s(rw + Cfg::RAW_ISD + (lane * kM + q * kTile) * 4, isd_t + uint64_t(en.x) * kTile, kTile * 4,
+                   &raw_full[r]);
+          if (en.y != kSelf && en.y != kPad)
+            bulk_g2s(rw + Cfg::RAW_W + (lane * 2 + q) * 16, maskt + (t0 + q) * Wp + (en.y & ~1u), 16,
+                     &raw_full[r]);
+        }
+      }
+    }
+  } else if (warp >= kEpiWarps && warp < kEpiWarps + kStgWarps) {
     // ------------------------------------------------------------ staging
     const int st_tid = tid - kEpiWarps * 32;  // 0..255
     for (uint32_t c = 0; c < nchunks; ++c) {
-      const int s = c % kStages;
-      if (c >= uint32_t(kStages)) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
+      const int r = c % kRawStages, s = c % kCanStages;
+      mbar_wait(&raw_full[r], (c / kRawStages) & 1);
+      if (c >= uint32_t(kCanStages)) mbar_wait(&can_empty[s], ((c / kCanStages) - 1) & 1);
+      const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
+      const uint2* recs = reinterpret_cast<const uint2*>(rw);
+      const float* Ps = reinterpret_cast<const float*>(rw + Cfg::RAW_P);
+      const float* isds = reinterpret_cast<const float*>(rw + Cfg::RAW_ISD);
+      const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
       unsigned char* st = smem + s * Cfg::STAGE;
-      const uint32_t base = e0 + c * kKC;
-      const int cnt = int(min(uint32_t(kKC), e1 - base));  // multiple of 8
-      // A: coefficients m_m(e) isd_m(x), K-major, unit (m, 4 entries)
+      const int cnt = int(min(uint32_t(kKC), e1 - (e0 + c * kKC)));  // multiple of 8
+      // A: coefficients m_m(e) isd_m(x), K-major, unit (coalition m, 4 entries)
       for (int J = st_tid; J < kM * (cnt / 4); J += kStgWarps * 32) {
-        const int m = J & (kM - 1), u = J >> 7;
-        const uint64_t tile = t0 + (m >> 6);
-        const int i = m & 63;
-        const uint64_t* mt = maskt + tile * Wp;
-        const float* isd_t = isd + tile * uint64_t(V) * kTile;
+        const int m = J & (kM - 1), u = J >> 7, q = m >> 6, i = m & 63;
         float c4[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint2 en = ent[base + 4 * u + q];
-          bool kept;
-          if (en.y == kSelf)
-            kept = true;
-          else if (en.y == kPad)
-            kept = false;
-          else
-            kept = (__ldg(&mt[en.y]) >> i) & 1ull;
-          c4[q] = kept ? __ldg(&isd_t[uint64_t(en.x) * kTile + i]) : 0.f;
+        for (int w = 0; w < 4; ++w) {
+          const int k = 4 * u + w;
+          const uint32_t y = recs[k].y;
+          const bool kept = y == kSelf || (y != kPad && ((ws[(k * 2 + q) * 2 + (y & 1u)] >> i) & 1ull));
+          c4[w] = kept ? isds[k * kM + m] : 0.f;
         }
         float4 hi, lo;
         hi.x = tf32_hi(c4[0]);
         hi.y = tf32_hi(c4[1]);
         hi.z = tf32_hi(c4[2]);
         hi.w = tf32_hi(c4[3]);
-        lo.x = c4[0] - hi.x;
-        lo.y = c4[1] - hi.y;
-        lo.z = c4[2] - hi.z;
-        lo.w = c4[3] - hi.w;
+        lo = make_float4(c4[0] - hi.x, c4[1] - hi.y, c4[2] - hi.z, c4[3] - hi.w);
         const uint32_t off = u * 2048 + (m >> 3) * 128 + (m & 7) * 16;
         *reinterpret_cast<float4*>(st + off) = hi;
         *reinterpret_cast<float4*>(st + Cfg::OFF_ALO + off) = lo;
       }
-      // B: gathered P rows transposed to K-major, unit (feature n, 4 entries)
+      // B: gathered P rows transposed to K-major, unit (feature n, 4 entries), hi/lo split
       for (int J = st_tid; J < D * (cnt / 4); J += kStgWarps * 32) {
         const int n = J % D, u = J / D;
-        float4 ph, pl;
-        const uint32_t x0 = ent[base + 4 * u].x, x1 = ent[base + 4 * u + 1].x;
-        const uint32_t x2 = ent[base + 4 * u + 2].x, x3 = ent[base + 4 * u + 3].x;
-        ph.x = __ldg(Phi + uint64_t(x0) * D + n);
-        ph.y = __ldg(Phi + uint64_t(x1) * D + n);
-        ph.z = __ldg(Phi + uint64_t(x2) * D + n);
-        ph.w = __ldg(Phi + uint64_t(x3) * D + n);
-        pl.x = __ldg(Plo + uint64_t(x0) * D + n);
-        pl.y = __ldg(Plo + uint64_t(x1) * D + n);
-        pl.z = __ldg(Plo + uint64_t(x2) * D + n);
-        pl.w = __ldg(Plo + uint64_t(x3) * D + n);
+        const float p0 = Ps[(4 * u) * D + n], p1 = Ps[(4 * u + 1) * D + n];
+        const float p2 = Ps[(4 * u + 2) * D + n], p3 = Ps[(4 * u + 3) * D + n];
+        float4 hi;
+        hi.x = tf32_hi(p0);
+        hi.y = tf32_hi(p1);
+        hi.z = tf32_hi(p2);
+        hi.w = tf32_hi(p3);
+        const float4 lo = make_float4(p0 - hi.x, p1 - hi.y, p2 - hi.z, p3 - hi.w);
         const uint32_t off = u * Cfg::B_LBO + (n >> 3) * 128 + (n & 7) * 16;
-        *reinterpret_cast<float4*>(st + Cfg::OFF_BHI + off) = ph;
-        *reinterpret_cast<float4*>(st + Cfg::OFF_BLO + off) = pl;
+        *reinterpret_cast<float4*>(st + Cfg::OFF_BHI + off) = hi;
+        *reinterpret_cast<float4*>(st + Cfg::OFF_BLO + off) = lo;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[s]);
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[r]);
+        mbar_arrive(&can_full[s]);
+      }
     }
-  } else if (warp == kEpiWarps + kStgWarps) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       // kind::tf32, D f32, A and B K-major, N = D, M = 128
@@ -251,8 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                              (uint32_t(kM >> 4) << 24);
       uint32_t sg = 0, b = 0, acc = 0;
       for (uint32_t c = 0; c < nchunks; ++c) {
-        const int s = c % kStages;
-        mbar_wait(&full[s], (c / kStages) & 1);
+        const int s = c % kCanStages;
+        mbar_wait(&can_full[s], (c / kCanStages) & 1);
         tc_fence_after();
         const uint32_t base = e0 + c * kKC;
         const int nk = int(min(uint32_t(kKC), e1 - base)) / 8;
@@ -281,10 +330,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++sg;
           }
         }
-        tc_commit(&empty[s]);
+        tc_commit(&can_empty[s]);
       }
     }
-  } else {
+  } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
     const int q = warp;  // TMEM lane quarter
     const int m = q * 32 + lane;
@@ -354,15 +403,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-__global__ void split_tf32_kernel(const float* __restrict__ x, uint64_t n, float* __restrict__ hi,
-                                  float* __restrict__ lo) {
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const float h = tf32_hi(x[i]);
-  hi[i] = h;
-  lo[i] = x[i] - h;
-}
-
 template <int D>
 void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
                uint64_t ntp, float* apart) {
@@ -374,7 +414,7 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
   }
   dim3 grid(e.tc_items, unsigned(ntp / 2));
   fused_tc_kernel<D><<<grid, kThreads, Cfg::SMEM, ctx.stream>>>(
-      maskt, Wp, isd, e.V, e.p0_hi.p, e.p0_lo.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
+      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
       e.tc_item_order.p, e.tc_items, apart);
   SF_LAUNCHED(ctx);
@@ -434,12 +474,6 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   e.tc_item_seg.upload(item_seg.data(), item_seg.size(), ctx.stream);
   e.tc_item_order.upload(order.data(), order.size(), ctx.stream);
   e.tc_u_items.upload(u_items.data(), u_items.size(), ctx.stream);
-  // P0 split into TF32 hi + residual lo (3xTF32)
-  const uint64_t np = uint64_t(e.V) * e.dims[1];
-  e.p0_hi.reserve(np);
-  e.p0_lo.reserve(np);
-  split_tf32_kernel<<<unsigned((np + 255) / 256), 256, 0, ctx.stream>>>(e.p0.p, np, e.p0_hi.p, e.p0_lo.p);
-  SF_LAUNCHED(ctx);
   ctx.h2d_bytes += ent.size() * 4 + kfl.size() + segs.size() * 4 +
                    (item_ent.size() + item_seg.size() + order.size() + u_items.size()) * 4;
   SF_CUDA(cudaStreamSynchronize(ctx.stream));

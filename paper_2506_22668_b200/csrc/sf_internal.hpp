@@ -147,7 +147,6 @@ struct Engine {
   uint32_t tc_items = 0;
   DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items;
   DevBuf<uint8_t> tc_kflags;
-  DevBuf<float> p0_hi, p0_lo;  // X W0 split for 3xTF32
 };
 
 struct CommStats {  // comm.hpp:13-19
