@@ -105,7 +105,7 @@ void comm_barrier(Ctx& ctx) {
   ++ctx.stats.barriers;
   if (ctx.world > 1) {
     if (!ctx.nccl) throw ProtocolError("multi-rank context without a communicator");
-    DevBuf<double> one;
+    DevBuf<double>& one = ctx.barrier_buf;
     one.reserve(1);
     SF_CUDA(cudaMemsetAsync(one.p, 0, sizeof(double), ctx.stream));
     ctx.nccl->check(ctx.nccl->all_reduce(one.p, one.p, 1, kFloat64, kSum, ctx.nccl->comm,
@@ -121,6 +121,7 @@ Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
   for (cudaEvent_t& e : events)
     if (e) cudaEventDestroy(e);
+  if (plan_ready) cudaEventDestroy(plan_ready);
   for (auto& pr : dom_events) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);

@@ -40,6 +40,7 @@ constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
 constexpr int kRawStages = 2, kCanStages = 2;
+constexpr int kMaxKsteps = 4096;  // per work item (host checks)
 constexpr int kEpiWarps = 4, kStgWarps = 8;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + 1;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
@@ -59,7 +60,8 @@ struct TcCfg {
   static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
   static constexpr int RAW = ((RAW_W + kKC * 2 * 16 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
-  static constexpr int OFF_BARS = OFF_RAW + kRawStages * RAW;
+  static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
+  static constexpr int OFF_BARS = OFF_KFL + kMaxKsteps;
   static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
   static constexpr uint32_t TMEM_COLS = 3 * D <= 256 ? 256 : 512;  // 2 H buffers + accumulator
   static_assert(D % 32 == 0 && D <= 256, "width");
@@ -294,6 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    uint8_t* sfl = smem + Cfg::OFF_KFL;
+    for (uint32_t j = lane; j < (e1 - e0) / 8; j += 32) sfl[j] = kflags[e0 / 8 + j];
+    __syncwarp();
     if (lane == 0) {
       // kind::tf32, D f32, A and B K-major, N = D, M = 128
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(D >> 3) << 17) |
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nk = int(min(uint32_t(kKC), e1 - base)) / 8;
         const uint32_t sa = su32(smem + s * Cfg::STAGE);
         for (int j = 0; j < nk; ++j) {
-          const uint8_t f = kflags[base / 8 + j];
+          const uint8_t f = sfl[(base - e0) / 8 + j];
           if (f & 1u) {
             b = sg & 1u;
             if (sg >= 2) {
@@ -350,11 +355,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int cc = 0; cc < D / 32; ++cc) TC_ST32(tmem + lane_base + acc_col + cc * 32, a);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     const uint32_t s0 = item_seg[item], s1 = item_seg[item + 1];
+    auto factors = [&](uint32_t k, float& svk, float& dvk) {
+      const uint2 se = seg[k];
+      svk = __ldg(&isd_t[uint64_t(se.x) * kTile + i]);
+      const bool muv = se.y == kSelf || ((__ldg(&mt[se.y]) >> i) & 1ull);
+      dvk = muv ? svk : 0.f;
+    };
+    float sv, dv;
+    factors(s0, sv, dv);
     for (uint32_t sg = 0; sg < s1 - s0; ++sg) {
-      const uint2 sv_e = seg[s0 + sg];
-      const float sv = __ldg(&isd_t[uint64_t(sv_e.x) * kTile + i]);
-      const bool muv = sv_e.y == kSelf || ((__ldg(&mt[sv_e.y]) >> i) & 1ull);
-      const float dv = muv ? sv : 0.f;
+      float sv_next = 0.f, dv_next = 0.f;
+      if (s0 + sg + 1 < s1) factors(s0 + sg + 1, sv_next, dv_next);  // in flight during the wait
       const uint32_t b = sg & 1u;
       mbar_wait(&hfull[b], (sg >> 1) & 1);
       tc_fence_after();
@@ -381,6 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&hfree[b]);
+      sv = sv_next;
+      dv = dv_next;
     }
     // write the accumulator: Apart[tile][item][i][:]
     float* out = Apart + ((tile * items + item) * kTile + i) * uint64_t(D);
@@ -463,6 +476,11 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
     close();
     u_items.push_back(uint32_t(item_ent.size() - 1));
   }
+  for (size_t it = 0; it + 1 < item_ent.size(); ++it)
+    if ((item_ent[it + 1] - item_ent[it]) / 8 > uint32_t(kMaxKsteps)) {
+      e.tc = false;  // a segment too long for the kernel's flag buffer: SIMT kernel
+      return;
+    }
   std::vector<uint32_t> order(work.size());
   for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return work[a] > work[b]; });

@@ -119,6 +119,25 @@ struct DevBuf {
   }
 };
 
+template <typename T>
+struct PinnedBuf {  // page-locked host staging
+  T* p = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void reserve(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    SF_CUDA(cudaMallocHost(&p, sizeof(T) * (count ? count : 1)));
+    n = count;
+  }
+};
+
 // Device-resident copy of one (subgraph, model) pair: the inputs of the
 // masked-inference engine.
 struct Engine {
@@ -178,6 +197,13 @@ struct Ctx {
   DevBuf<float> preds;
   DevBuf<unsigned char> work;  // engine workspace
   DevBuf<unsigned char> solver_work;
+  // sampler class table (pinned staging + device copy, reused per call)
+  PinnedBuf<uint64_t> plan_host;
+  PinnedBuf<uint32_t> plan_host32;
+  DevBuf<uint64_t> plan_dev64;
+  DevBuf<uint32_t> plan_dev32;
+  cudaEvent_t plan_ready = nullptr;
+  DevBuf<double> barrier_buf;
   Ctx();
   ~Ctx();
 };

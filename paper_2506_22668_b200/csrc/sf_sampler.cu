@@ -10,6 +10,8 @@
 // single-worker rows at the same global index.
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "sf_device.cuh"
 #include "sf_internal.hpp"
 
@@ -297,13 +299,24 @@ void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
     first[i] = plan.classes[i].first_pair;
     cnt[i] = plan.classes[i].pairs;
   }
-  // class table lives in the context's solver scratch for the launch
-  DevBuf<uint32_t> d_sizes;
-  DevBuf<uint64_t> d_first, d_cnt;
-  d_sizes.upload(sizes.data(), C, ctx.stream);
-  d_first.upload(first.data(), C, ctx.stream);
-  d_cnt.upload(cnt.data(), C, ctx.stream);
-  ClassTable ct{d_sizes.p, d_first.p, d_cnt.p, static_cast<uint32_t>(C)};
+  // class table: context-owned device buffers, filled from pinned staging
+  // (no per-call allocation, no host synchronization)
+  if (ctx.plan_ready) SF_CUDA(cudaEventSynchronize(ctx.plan_ready));  // staging free again
+  else SF_CUDA(cudaEventCreateWithFlags(&ctx.plan_ready, cudaEventDisableTiming));
+  ctx.plan_host.reserve(2 * C + 1);
+  uint64_t* h = ctx.plan_host.p;
+  for (size_t i = 0; i < C; ++i) {
+    h[i] = first[i];
+    h[C + i] = cnt[i];
+  }
+  ctx.plan_dev64.reserve(2 * C + 1);
+  ctx.plan_dev32.reserve(C + 1);
+  SF_CUDA(cudaMemcpyAsync(ctx.plan_dev64.p, h, 2 * C * 8, cudaMemcpyHostToDevice, ctx.stream));
+  ctx.plan_host32.reserve(C + 1);
+  std::memcpy(ctx.plan_host32.p, sizes.data(), C * 4);
+  SF_CUDA(cudaMemcpyAsync(ctx.plan_dev32.p, ctx.plan_host32.p, C * 4, cudaMemcpyHostToDevice, ctx.stream));
+  ctx.h2d_bytes += C * 20;
+  ClassTable ct{ctx.plan_dev32.p, ctx.plan_dev64.p, ctx.plan_dev64.p + C, static_cast<uint32_t>(C)};
   if (plan.exhaustive) {
     exhaustive_kernel<<<unsigned((pairs + 127) / 128), 128, 0, ctx.stream>>>(
         ct, n, rank, world, pairs, dev_rows);
@@ -329,8 +342,9 @@ void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
     }
     SF_LAUNCHED(ctx);
   }
-  // the class table must outlive the launch
-  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+  // the pinned staging copies are reused by the next call: order it after
+  // this launch's uploads
+  SF_CUDA(cudaEventRecord(ctx.plan_ready, ctx.stream));
 }
 
 void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
