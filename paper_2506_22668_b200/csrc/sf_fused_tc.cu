@@ -41,8 +41,8 @@ constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
 constexpr int kRawStages = 2, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 4, kStgWarps = 8;
-constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + 1;
+constexpr int kEpiWarps = 4, kStgWarps = 8, kProdWarps = 4;
+constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 
 template <int D>
@@ -94,6 +94,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    su32(dst)),
                "l"(src), "r"(bytes), "r"(su32(bar))
                : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+// arrives on the barrier once all of this thread's prior cp.async copies land
+__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (tid == 0) {
     for (int s = 0; s < kRawStages; ++s) {
-      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_full[s], kProdWarps * 32);
       mbar_init(&raw_empty[s], kStgWarps);
     }
     for (int s = 0; s < kCanStages; ++s) {
@@ -204,38 +211,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == kProducerWarp) {
-    // ------------------------------------------------------------ producer
+  if (warp >= kProducerWarp && warp < kMmaWarp) {
+    // ------------------------------------------------------------ producers
+    // 16-byte cp.async gathers (LDGSTS) of the chunk's records, P rows, isd
+    // rows (both tiles) and mask blocks; each producer thread arrives on
+    // raw_full once its own copies have landed.
+    const int pt = tid - kProducerWarp * 32;  // 0..127
+    uint2 rec_next = make_uint2(0, kPad);
+    if (lane < int(e1 - e0)) rec_next = ent[e0 + lane];
     for (uint32_t c = 0; c < nchunks; ++c) {
       const int r = c % kRawStages;
-      if (c >= uint32_t(kRawStages)) mbar_wait(&raw_empty[r], ((c / kRawStages) - 1) & 1);
-      unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       const uint32_t base = e0 + c * kKC;
       const int cnt = int(min(uint32_t(kKC), e1 - base));
-      uint2 en = make_uint2(0, kPad);
-      uint32_t bytes = 0;
-      if (lane < cnt) {
-        en = ent[base + lane];
-        bytes = D * 4 + 2 * kTile * 4 + ((en.y != kSelf && en.y != kPad) ? 2 * 16 : 0);
+      const uint2 rec = lane < cnt ? rec_next : make_uint2(0, kPad);
+      if (base + kKC + lane < e1) rec_next = ent[base + kKC + lane];
+      if (c >= uint32_t(kRawStages)) mbar_wait(&raw_empty[r], ((c / kRawStages) - 1) & 1);
+      unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
+      if (pt < cnt / 2) cp_async16(rw + pt * 16, ent + base + 2 * pt);  // records
+      for (int J = pt; J < cnt * (D / 4); J += kProdWarps * 32) {      // P rows
+        const int k = J / (D / 4), ng = J % (D / 4);
+        const uint32_t x = __shfl_sync(kFull, rec.x, k);
+        cp_async16(rw + Cfg::RAW_P + (k * D + ng * 4) * 4, P + uint64_t(x) * D + ng * 4);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
-      bytes += cnt * 8;  // entry records
-      if (lane == 0) mbar_arrive_expect_tx(&raw_full[r], bytes);
-      __syncwarp();
-      if (lane == 0) bulk_g2s(rw, ent + base, cnt * 8, &raw_full[r]);
-      if (lane < cnt) {
-        bulk_g2s(rw + Cfg::RAW_P + lane * D * 4, P + uint64_t(en.x) * D, D * 4, &raw_full[r]);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const float* isd_t = isd + (t0 + q) * uint64_t(V) * kTile;
-          bulk_g2s(rw + Cfg::RAW_ISD + (lane * kM + q * kTile) * 4, isd_t + uint64_t(en.x) * kTile, kTile * 4,
-                   &raw_full[r]);
-          if (en.y != kSelf && en.y != kPad)
-            bulk_g2s(rw + Cfg::RAW_W + (lane * 2 + q) * 16, maskt + (t0 + q) * Wp + (en.y & ~1u), 16,
-                     &raw_full[r]);
-        }
+      for (int J = pt; J < cnt * 2 * 16; J += kProdWarps * 32) {        // isd rows, 2 tiles
+        const int k = J >> 5, q = (J >> 4) & 1, ug = J & 15;
+        const uint32_t x = __shfl_sync(kFull, rec.x, k);
+        cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
+                   isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
       }
+      {                                                                    // mask blocks
+        const int k = pt >> 1, q = pt & 1;
+        const uint32_t y = __shfl_sync(kFull, rec.y, k & 31);
+        if (k < cnt && y != kSelf && y != kPad)
+          cp_async16(rw + Cfg::RAW_W + (k * 2 + q) * 16, maskt + (t0 + q) * Wp + (y & ~1u));
+      }
+      cp_async_arrive(&raw_full[r]);
     }
   } else if (warp >= kEpiWarps && warp < kEpiWarps + kStgWarps) {
     // ------------------------------------------------------------ staging
