@@ -64,6 +64,15 @@ int sf_ctx_io_bytes(const sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 int sf_ctx_event_record(sf_ctx* ctx, int slot);
 int sf_ctx_event_elapsed(sf_ctx* ctx, int from_slot, int to_slot, float* ms);
 int sf_ctx_synchronize(sf_ctx* ctx);
+/* Fused layer-0/1 kernel selection for this context (no reference
+ * counterpart; the reference has one CPU kernel, gcn.cpp:96-160):
+ * SF_KERNEL_AUTO = tcgen05 3xTF32 where the hidden width allows (env
+ * SF_FUSED_TC=0 forces SIMT), SF_KERNEL_SIMT = FP32 SIMT kernel,
+ * SF_KERNEL_TC = tcgen05 where possible. Takes effect on the next call. */
+enum { SF_KERNEL_AUTO = 0, SF_KERNEL_SIMT = 1, SF_KERNEL_TC = 2 };
+int sf_ctx_set_fused_kernel(sf_ctx* ctx, int kind);
+/* which fused kernel the last prediction used: 0 none, 1 SIMT, 2 tcgen05 */
+int sf_ctx_fused_kernel_used(const sf_ctx* ctx);
 /* Per-launch timing of the dominant kernel (layer-0 masked SpMM): enable,
  * run work, then read the summed duration (ms), launch count and the
  * complement pairs those launches covered. */

@@ -41,7 +41,7 @@ constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
 constexpr int kRawStages = 2, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 4, kStgWarps = 8, kProdWarps = 4;
+constexpr int kEpiWarps = 4, kStgWarps = 11, kProdWarps = 4;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 
@@ -58,7 +58,7 @@ struct TcCfg {
   static constexpr int RAW_P = kKC * 8;
   static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
   static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
-  static constexpr int RAW = ((RAW_W + kKC * 2 * 16 + 127) / 128) * 128;
+  static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
   static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
   static constexpr int OFF_BARS = OFF_KFL + kMaxKsteps;
@@ -94,6 +94,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    su32(dst)),
                "l"(src), "r"(bytes), "r"(su32(bar))
                : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
                     const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
-                    uint32_t items, float* __restrict__ Apart) {
+                    uint32_t items, const uint64_t* __restrict__ const_words, float* __restrict__ Apart) {
   using Cfg = TcCfg<D>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BARS);
@@ -239,17 +242,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
                    isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
       }
-      {                                                                    // mask blocks
+      {  // mask words, one u64 per (entry, tile); self -> all ones, pad -> zero
         const int k = pt >> 1, q = pt & 1;
         const uint32_t y = __shfl_sync(kFull, rec.y, k & 31);
-        if (k < cnt && y != kSelf && y != kPad)
-          cp_async16(rw + Cfg::RAW_W + (k * 2 + q) * 16, maskt + (t0 + q) * Wp + (y & ~1u));
+        if (k < cnt) {
+          const uint64_t* src = y == kSelf ? const_words : (y == kPad ? const_words + 1 : maskt + (t0 + q) * Wp + y);
+          cp_async8(rw + Cfg::RAW_W + (k * 2 + q) * 8, src);
+        }
       }
       cp_async_arrive(&raw_full[r]);
     }
   } else if (warp >= kEpiWarps && warp < kEpiWarps + kStgWarps) {
     // ------------------------------------------------------------ staging
-    const int st_tid = tid - kEpiWarps * 32;  // 0..255
+    const int st_tid = tid - kEpiWarps * 32;
     for (uint32_t c = 0; c < nchunks; ++c) {
       const int r = c % kRawStages, s = c % kCanStages;
       mbar_wait(&raw_full[r], (c / kRawStages) & 1);
@@ -268,9 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const int k = 4 * u + w;
-          const uint32_t y = recs[k].y;
-          const bool kept = y == kSelf || (y != kPad && ((ws[(k * 2 + q) * 2 + (y & 1u)] >> i) & 1ull));
-          c4[w] = kept ? isds[k * kM + m] : 0.f;
+          c4[w] = ((ws[k * 2 + q] >> i) & 1ull) ? isds[k * kM + m] : 0.f;
         }
         float4 hi, lo;
         hi.x = tf32_hi(c4[0]);
@@ -439,7 +442,7 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
   fused_tc_kernel<D><<<grid, kThreads, Cfg::SMEM, ctx.stream>>>(
       maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
-      e.tc_item_order.p, e.tc_items, apart);
+      e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart);
   SF_LAUNCHED(ctx);
 }
 
@@ -495,6 +498,8 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return work[a] > work[b]; });
   e.tc_items = uint32_t(work.size());
+  const uint32_t consts[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u};  // u64 all-ones, u64 zero
+  e.tc_const.upload(consts, 4, ctx.stream);
   e.tc_ent.upload(ent.data(), ent.size(), ctx.stream);
   e.tc_kflags.upload(kfl.data(), kfl.size(), ctx.stream);
   e.tc_seg.upload(segs.data(), segs.size(), ctx.stream);

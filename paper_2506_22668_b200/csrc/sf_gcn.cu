@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "sf_device.cuh"
 #include "sf_internal.hpp"
@@ -818,7 +819,7 @@ void build_fused_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
 
 void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   Engine& e = ctx.engine;
-  if (e.sg_id == sg.id && e.model_id == m.id) return;
+  if (e.sg_id == sg.id && e.model_id == m.id && e.kind == ctx.fused_kind) return;
   if (m.layers.empty()) throw DataError("model has no layers");
   if (m.layers.front().in != sg.feature_dim)
     throw DataError("model input dim " + std::to_string(m.layers.front().in) +
@@ -855,12 +856,17 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   SF_CUDA(cudaStreamSynchronize(ctx.stream));  // temporaries x, w0 die here
   e.fused = e.L >= 2 && fused_width(e.dims[1]) && e.n > 0;
   if (e.fused) build_fused_plan(ctx, e, sg);
-  // tensor-core fused kernel (A/B switch while it is validated)
-  static const bool use_tc = std::getenv("SF_FUSED_TC") != nullptr;
-  e.tc = e.fused && use_tc && tc_width(e.dims[1]);
+  // tcgen05 3xTF32 fused kernel by default; SF_FUSED_TC=0 selects the SIMT FP32 kernel
+  static const bool use_tc = [] {
+    const char* v = std::getenv("SF_FUSED_TC");
+    return v == nullptr || std::strcmp(v, "0") != 0;
+  }();
+  const bool want_tc = ctx.fused_kind == 2 || (ctx.fused_kind == 0 && use_tc);
+  e.tc = e.fused && want_tc && tc_width(e.dims[1]);
   if (e.tc) build_tc_plan(ctx, e, sg);
   e.sg_id = sg.id;
   e.model_id = m.id;
+  e.kind = ctx.fused_kind;
 }
 
 void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,

@@ -783,6 +783,20 @@ int sf_ctx_rank(const sf_ctx* ctx) { return ctx ? ctx->c.rank : -1; }
 int sf_ctx_world(const sf_ctx* ctx) { return ctx ? ctx->c.world : -1; }
 uint64_t sf_ctx_launches(const sf_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int sf_ctx_set_fused_kernel(sf_ctx* ctx, int kind) {
+  return guard([&] {
+    need(ctx, "context");
+    if (kind < 0 || kind > 2) throw DataError("fused kernel kind must be 0 (auto), 1 (simt) or 2 (tc)");
+    ctx->c.fused_kind = kind;
+  });
+}
+
+int sf_ctx_fused_kernel_used(const sf_ctx* ctx) {
+  if (!ctx) return -1;
+  const Engine& e = ctx->c.engine;
+  return e.fused ? (e.tc ? 2 : 1) : 0;
+}
+
 int sf_ctx_io_bytes(const sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
   return guard([&] {
     need(ctx, "context");

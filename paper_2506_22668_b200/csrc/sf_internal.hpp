@@ -142,6 +142,7 @@ struct PinnedBuf {  // page-locked host staging
 // masked-inference engine.
 struct Engine {
   uint64_t sg_id = 0, model_id = 0;
+  int kind = 0;  // Ctx::fused_kind the engine was prepared for
   uint32_t V = 0;
   uint64_t n = 0;
   uint32_t W = 0;  // u64 words per mask row
@@ -164,7 +165,7 @@ struct Engine {
   // tensor-core (tcgen05) plan: segments padded to 8 entries (sf_fused_tc.cu)
   bool tc = false;
   uint32_t tc_items = 0;
-  DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items;
+  DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items, tc_const;
   DevBuf<uint8_t> tc_kflags;
 };
 
@@ -182,6 +183,7 @@ struct Ctx {
   std::unique_ptr<Nccl> nccl;
   CommStats stats;
   uint64_t launches = 0;
+  int fused_kind = 0;  // SF_KERNEL_AUTO / SIMT / TC
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic issued
   cudaEvent_t events[8] = {};             // bench timers on `stream`
   // dominant-kernel (layer-0 masked SpMM) timing: event pairs per launch,

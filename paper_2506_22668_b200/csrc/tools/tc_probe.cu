@@ -25,11 +25,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 }
 
 __global__ void probe(const float* A, const float* B, float* D, int mode) {
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t bar;
   unsigned char* sa = smem;
-  unsigned char* sb = smem + M * K * 4;
+  unsigned char* sb = smem + M * K * 4;  // 16 KB offset: 1024-aligned
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // A[m][k]: offset (k/4)*2048 + (m/8)*128 + (m%8)*16 + (k%4)*4
   for (int idx = tid; idx < M * K; idx += blockDim.x) {
@@ -39,7 +39,9 @@ __global__ void probe(const float* A, const float* B, float* D, int mode) {
   for (int idx = tid; idx < K * N; idx += blockDim.x) {
     const int k = idx / N, n = idx % N;
     uint32_t off;
-    if (mode >= 2)  // K-major B (N x K): (k/4)*(N/8*128) + (n/8)*128 + (n%8)*16 + (k%4)*4
+    if (mode >= 3)  // MN-major SWIZZLE_128B: atom (32 n x 8 k) = 1024 B, [n/32][k/8][atom]
+      off = (n / 32) * (K / 8 * 1024) + (k / 8) * 1024 + (k % 8) * 128 + ((((n % 32) / 4) ^ (k % 8)) * 16) + (n % 4) * 4;
+    else if (mode == 2)  // K-major B (N x K): (k/4)*(N/8*128) + (n/8)*128 + (n%8)*16 + (k%4)*4
       off = (k / 4) * (N / 8 * 128) + (n / 8) * 128 + (n % 8) * 16 + (k % 4) * 4;
     else            // MN-major: (n/4)*B_SBO + (k/8)*128 + (k%8)*16 + (n%4)*4
       off = (n / 4) * B_SBO + (k / 8) * 128 + (k % 8) * 16 + (n % 4) * 4;
@@ -59,7 +61,7 @@ __global__ void probe(const float* A, const float* B, float* D, int mode) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot;
   if (tid == 0) {
-    const uint32_t b_major = mode >= 2 ? 0u : 1u;
+    const uint32_t b_major = mode == 2 ? 0u : 1u;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (b_major << 16) | (uint32_t(N >> 3) << 17) |
                            (uint32_t(M >> 4) << 24);
     for (int j = 0; j < K / 8; ++j) {
@@ -67,7 +69,9 @@ __global__ void probe(const float* A, const float* B, float* D, int mode) {
       uint64_t bd;
       if (mode == 0) bd = smem_desc(su32(sb) + j * 128, 128, B_SBO);
       else if (mode == 1) bd = smem_desc(su32(sb) + j * 128, B_SBO, 128);
-      else bd = smem_desc(su32(sb) + j * 2 * (N / 8 * 128), N / 8 * 128, 128);
+      else if (mode == 2) bd = smem_desc(su32(sb) + j * 2 * (N / 8 * 128), N / 8 * 128, 128);
+      else if (mode == 3) bd = smem_desc(su32(sb) + j * 1024, K / 8 * 1024, 1024) | (uint64_t(2) << 61);
+      else bd = smem_desc(su32(sb) + j * 1024, 1024, K / 8 * 1024) | (uint64_t(2) << 61);
       const uint32_t acc = j > 0;
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -114,9 +118,9 @@ int main() {
   cudaMalloc(&dD, D.size() * 4);
   cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
-  const int smem = M * K * 4 + (N / 4) * B_SBO + 1024;
+  const int smem = M * K * 4 + (N / 4) * B_SBO + 4096;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 5; ++mode) {
     cudaMemset(dD, 0, D.size() * 4);
     probe<<<1, 128, smem>>>(dA, dB, dD, mode);
     cudaError_t e = cudaDeviceSynchronize();
@@ -127,7 +131,7 @@ int main() {
       mx = std::max(mx, double(std::fabs(R[i])));
     }
     printf("mode %d (%s B): status=%s max_abs_err=%.3g max_ref=%.3g D[0]=%g R[0]=%g D[1]=%g R[1]=%g D[N]=%g R[N]=%g\n",
-           mode, mode == 2 ? "K-major" : (mode ? "MN-major swapped lbo/sbo" : "MN-major"), cudaGetErrorString(e), err, mx, D[0], R[0], D[1], R[1], D[N], R[N]);
+           mode, mode == 4 ? "MN-major SW128 swapped" : mode == 3 ? "MN-major SW128" : mode == 2 ? "K-major" : (mode ? "MN-major swapped lbo/sbo" : "MN-major"), cudaGetErrorString(e), err, mx, D[0], R[0], D[1], R[1], D[N], R[N]);
   }
   return 0;
 }

@@ -12,6 +12,22 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-5  # BASELINE north_star: predictions within 1e-5 relative
 
 
+@pytest.fixture(params=["simt", "tc"])
+def kernel(request, ctx):
+    """Run a parity case on both fused layer-0/1 kernels (FP32 SIMT and
+    tcgen05 3xTF32); the context goes back to "auto" afterwards."""
+    ctx.set_fused_kernel(request.param)
+    yield request.param
+    ctx.set_fused_kernel("auto")
+
+
+def _check_kernel(ctx, kernel, hidden):
+    if len(hidden) >= 1 and hidden[0] in (32, 64, 128):
+        assert ctx.fused_kernel_used() == kernel
+    elif len(hidden) >= 1 and hidden[0] in (16, 256):
+        assert ctx.fused_kernel_used() == "simt"
+
+
 def rel_err(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
@@ -50,7 +66,7 @@ def test_toy_all_masks(ctx, golden):
     ((128, 128), 3, 20, 41),  # C2 widths
     ((64, 32, 8), 4, 10, 6),  # 4 layers
 ])
-def test_random_graph_vs_reference(ctx, ref, port, hidden, hops, dim, classes):
+def test_random_graph_vs_reference(ctx, ref, port, kernel, hidden, hops, dim, classes):
     nodes, edges = 150, 520
     rg = ref.graph_random(nodes, edges, dim, 3, 5)
     rp, col = ref.graph_csr(rg)
@@ -71,6 +87,7 @@ def test_random_graph_vs_reference(ctx, ref, port, hidden, hops, dim, classes):
     bits = np.concatenate([bits, extra])
     cls = classes - 1
     got = ctx.predict_batched(m, sg, bits, cls)
+    _check_kernel(ctx, kernel, hidden)
     want = ref.predict_batched(rm, rg, 3, bits, cls, sg=sgr)
     assert rel_err(got, want) <= RTOL
     ref.cg_free(sgr)
@@ -114,7 +131,7 @@ def test_validation(ctx):
         ctx.predict_probs(wide, sg, np.array([1], np.uint64))
 
 
-def test_c1_all_coalitions_vs_reference(ctx, ref):
+def test_c1_all_coalitions_vs_reference(ctx, ref, kernel):
     """Config C1 end to end through predict_batched: all 10,000 sampled masks."""
     d = W.build("C1")
     cfg = d["cfg"]
@@ -127,12 +144,13 @@ def test_c1_all_coalitions_vs_reference(ctx, ref):
     seed = sf.node_sampling_seed(cfg.explain_seed, d["target"])
     bits, _ = ctx.generate_masks(p, seed)
     got = ctx.predict_batched(m, sg, bits, 2)
+    _check_kernel(ctx, kernel, cfg.hidden)
     want = ref.predict_batched(rm, rg, d["target"], bits, 2)
     assert rel_err(got, want) <= RTOL
 
 
 @pytest.mark.slow
-def test_c2_subset_vs_reference(ctx, ref):
+def test_c2_subset_vs_reference(ctx, ref, kernel):
     """Config C2 (3-layer, n ~ 50K): GPU predictions on the full rank shard are
     checked against the reference on a spread subset of rows."""
     d = W.build("C2")
@@ -145,6 +163,7 @@ def test_c2_subset_vs_reference(ctx, ref):
     p = sf.plan_sizes(sg.n, 20_000, True)
     bits, _ = ctx.generate_masks(p, 99)
     got = ctx.predict_batched(m, sg, bits, 5)
+    _check_kernel(ctx, kernel, cfg.hidden)
     pick = np.r_[0:16, 5000:5016, 19_980:20_000]
     want = ref.predict_batched(rm, rg, d["target"], bits[pick], 5)
     assert rel_err(got[pick], want) <= RTOL
