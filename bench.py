@@ -94,11 +94,23 @@ class Clocks:
 
 
 def measured_peaks():
+    """HBM GB/s and dense bf16 TFLOP/s (burst) from MEASURED_PEAKS.json, else
+    the B200_PROFILING.md fallbacks."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
-        return d.get("hbm_gbs", 6650.0), "measured"
-    return 6650.0, "fallback"
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 2250.0), "measured"
+    return 6650.0, 2250.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/roofline_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path)).get(kernel)
+    return None if d is None else d.get("dram_bytes_per_launch")
 
 
 def build_problem(name, sf):
@@ -271,19 +283,41 @@ def run_ours(args):
     # ---------------------------------------------------------------- roofline
     bpp, fpp = C.c_double(), C.c_double()
     sf.lib.sf_spmm_bytes_per_pair(m.h, sg.h, C.byref(bpp), C.byref(fpp))
-    peak, peak_kind = measured_peaks()
+    hbm_peak, bf16_peak, peak_kind = measured_peaks()
+    ent, pad, items, width = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32()
+    sf.lib.sf_ctx_fused_plan(ctx.h, C.byref(ent), C.byref(pad), C.byref(items), C.byref(width))
+    kernel_used = ctx.fused_kernel_used()
     roof = None
     if dom_n.value:
         avg_launch_s = dom_ms.value / 1000.0 / dom_n.value
         pairs_per_launch = dom_pairs.value / dom_n.value
-        achieved = bpp.value * pairs_per_launch / avg_launch_s / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "layer0_kernel (masked SpMM over X W0)",
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "algorithmic_bytes_per_pair": bpp.value, "flops_per_pair": fpp.value,
-                "achieved_fp32_tflops": fpp.value * pairs_per_launch / avg_launch_s / 1e12,
-                "avg_launch_ms": avg_launch_s * 1000.0, "launches": dom_n.value,
-                "share_of_step": dom_ms.value / max(ms.value, 1e-9)}
+        useful_tflops = fpp.value * pairs_per_launch / avg_launch_s / 1e12
+        common = {"algorithmic_flops_per_pair": fpp.value, "algorithmic_bytes_per_pair": bpp.value,
+                  "avg_launch_ms": avg_launch_s * 1000.0, "launches": dom_n.value,
+                  "pairs_per_launch": pairs_per_launch,
+                  "share_of_step": dom_ms.value / max(ms.value, 1e-9)}
+        if kernel_used == "tc":
+            # tcgen05 kind::tf32 dense peak = half the measured bf16 dense peak
+            peak = bf16_peak / 2.0
+            issued = 3 * 2.0 * 2 * pairs_per_launch * pad.value * width.value / avg_launch_s / 1e12
+            name = f"fused_tc_kernel<{width.value}>"
+            traffic = ncu_traffic(name)
+            roof = {"bound": "tensor", "achieved": useful_tflops, "peak": peak, "unit": "TFLOP/s",
+                    "frac": useful_tflops / peak, "traffic": traffic,
+                    "kernel": name + " (tcgen05 3xTF32: masked layer 0 + layer-1 aggregation)",
+                    "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}) / 2 for kind::tf32",
+                    "issued_mma_tflops": issued, "issued_frac": issued / peak,
+                    "note": "achieved counts the layer-0 masked SpMM flops (SURVEY 8(d)) once; the kernel "
+                            "issues 3 MMAs per product (3xTF32) over dense 128-coalition x K tiles with "
+                            "padded, recomputed entries (issued_mma_tflops)",
+                    **common}
+        else:
+            name = f"fused_kernel<{width.value}>" if kernel_used == "simt" else "agg_generic_kernel"
+            achieved = bpp.value * pairs_per_launch / avg_launch_s / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": ncu_traffic(name), "kernel": name,
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                    "achieved_fp32_tflops": useful_tflops, **common}
 
     # ---------------------------------------------------------------- e2e
     from paper_2506_22668_b200.api import ExplainOptions
@@ -323,7 +357,8 @@ def run_ours(args):
                 "ball_sizes": sg.ball_sizes(cfg.hops), "parallelism": f"coalition pairs g mod {world}",
                 "l2": "inputs larger than L2 (masks regenerated each step: "
                       f"{2 * ((k // 2 + world - 1) // world) * max(sg.words, 1) * 8 / 1e9:.2f} GB per rank)",
-                "accuracy_mode": "FP32 SIMT (CUDA cores), FP64 solver",
+                "accuracy_mode": ("tcgen05 3xTF32 (FP32-equivalent products, FP32 accumulate)"
+                                  if kernel_used == "tc" else "FP32 SIMT (CUDA cores)") + ", FP64 solver",
             },
             "stage_ms_per_step": {"sampling": stage[0] / args.steps, "prediction": stage[1] / args.steps},
             "e2e": None if not e2e_steps else {

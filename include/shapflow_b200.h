@@ -73,6 +73,12 @@ enum { SF_KERNEL_AUTO = 0, SF_KERNEL_SIMT = 1, SF_KERNEL_TC = 2 };
 int sf_ctx_set_fused_kernel(sf_ctx* ctx, int kind);
 /* which fused kernel the last prediction used: 0 none, 1 SIMT, 2 tcgen05 */
 int sf_ctx_fused_kernel_used(const sf_ctx* ctx);
+/* Plan of the fused kernel prepared by the last prediction: layer-0 entries
+ * gathered per coalition (with the fused recompute), the same padded to the
+ * tcgen05 K granularity (0 on the SIMT kernel), work items, hidden width. */
+int sf_ctx_fused_plan(const sf_ctx* ctx, uint64_t* entries,
+                      uint64_t* padded_entries, uint32_t* items,
+                      uint32_t* width);
 /* Per-launch timing of the dominant kernel (layer-0 masked SpMM): enable,
  * run work, then read the summed duration (ms), launch count and the
  * complement pairs those launches covered. */

@@ -498,6 +498,7 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return work[a] > work[b]; });
   e.tc_items = uint32_t(work.size());
+  e.tc_entries = ent.size() / 2;
   const uint32_t consts[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u};  // u64 all-ones, u64 zero
   e.tc_const.upload(consts, 4, ctx.stream);
   e.tc_ent.upload(ent.data(), ent.size(), ctx.stream);

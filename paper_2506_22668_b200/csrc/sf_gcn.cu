@@ -31,33 +31,72 @@ constexpr int kTile = 64;  // coalitions per tile
 
 // ---------------------------------------------------------------- degrees
 // deg_i(u) = 1 + sum over u's CSR entries of bit_i(edge_player) (the
-// self-loop counts, gcn.cpp:76-81). One warp per (tile, node); the warp
-// loads 32 incidences at once and broadcasts them with shuffles.
+// self-loop counts, gcn.cpp:76-81), isd = 1/sqrt(deg) read from a table of
+// the correctly rounded values (inv_sqrt_deg, bitwise equal to gcn.cpp:82).
+// One warp per (node, 2 tiles), nodes in descending degree order so hubs
+// start first. Lane l owns coalitions l and l+32 of each tile. A chunk of up
+// to 32 incidences is loaded one per lane; chunks longer than 8 are counted
+// by transposing the 32 x 64 bit block (rows = incidences) with a butterfly
+// and taking popc, shorter ones by broadcasting each word.
+__device__ __forceinline__ uint32_t bfly32(uint32_t x, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                     : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(kFull, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+  }
+  return x;  // lane l: bit j = bit l of lane j's input
+}
+
 __global__ void __launch_bounds__(256)
-    isd_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
+    isd_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, uint64_t ntiles,
                const uint32_t* __restrict__ row_ptr,
-               const uint32_t* __restrict__ ep, uint32_t V,
-               float* __restrict__ isd) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t u = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const uint64_t t = blockIdx.y;
-  if (u >= V) return;
-  const uint64_t* mt = maskt + t * Wp;
-  uint32_t d0 = 1, d1 = 1;
+               const uint32_t* __restrict__ ep, const uint32_t* __restrict__ order,
+               const float* __restrict__ tab, uint32_t V, float* __restrict__ isd) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t j = blockIdx.y * 8 + warp;
+  const uint64_t t0 = uint64_t(blockIdx.x) * 2;
+  if (j >= V) return;
+  const bool two = t0 + 1 < ntiles;
+  const uint32_t u = order[j];
+  const uint64_t* m0 = maskt + t0 * Wp;
+  const uint64_t* m1 = two ? m0 + Wp : m0;
+  uint32_t c0lo = 1, c0hi = 1, c1lo = 1, c1hi = 1;  // self loop
   const uint32_t beg = row_ptr[u], end = row_ptr[u + 1];
   for (uint32_t i0 = beg; i0 < end; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const uint64_t w = i < end ? __ldg(&mt[ep[i]]) : 0ull;
-    const uint32_t cnt = min(32u, end - i0);
-    for (uint32_t k = 0; k < cnt; ++k) {
-      const uint64_t wk = __shfl_sync(kFull, w, k);
-      d0 += (wk >> lane) & 1u;
-      d1 += (wk >> (lane + 32)) & 1u;
+    const uint32_t i = i0 + lane, cnt = min(32u, end - i0);
+    const uint32_t p = i < end ? __ldg(&ep[i]) : 0u;
+    const uint64_t w0 = i < end ? __ldg(&m0[p]) : 0ull;
+    const uint64_t w1 = i < end ? __ldg(&m1[p]) : 0ull;
+    if (cnt > 8) {
+      c0lo += __popc(bfly32(uint32_t(w0), lane));
+      c0hi += __popc(bfly32(uint32_t(w0 >> 32), lane));
+      c1lo += __popc(bfly32(uint32_t(w1), lane));
+      c1hi += __popc(bfly32(uint32_t(w1 >> 32), lane));
+    } else {
+      for (uint32_t k = 0; k < cnt; ++k) {
+        const uint64_t x0 = __shfl_sync(kFull, w0, k), x1 = __shfl_sync(kFull, w1, k);
+        c0lo += (uint32_t(x0) >> lane) & 1u;
+        c0hi += (uint32_t(x0 >> 32) >> lane) & 1u;
+        c1lo += (uint32_t(x1) >> lane) & 1u;
+        c1hi += (uint32_t(x1 >> 32) >> lane) & 1u;
+      }
     }
   }
-  float* out = isd + (t * V + u) * kTile;
-  out[lane] = inv_sqrt_deg(d0);
-  out[lane + 32] = inv_sqrt_deg(d1);
+  float* out = isd + (t0 * V + u) * kTile;
+  out[lane] = __ldg(&tab[c0lo]);
+  out[lane + 32] = __ldg(&tab[c0hi]);
+  if (two) {
+    out += uint64_t(V) * kTile;
+    out[lane] = __ldg(&tab[c1lo]);
+    out[lane + 32] = __ldg(&tab[c1hi]);
+  }
+}
+
+__global__ void isd_table_kernel(float* tab, uint32_t n) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) tab[d] = inv_sqrt_deg(d);
 }
 
 // ---------------------------------------------------------------- fused
@@ -709,6 +748,145 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
   }
 }
 
+// ---------------------------------------------------------------- fused tail
+// Everything after the fused layer-0/1 kernel, for one tile t and cpb
+// coalitions per CTA, in shared memory (replaces reduce_partials + sgemm +
+// last_kernel / softmax_rows with the same arithmetic order):
+//   A[u][i]  = isd_i(u) * sum over the items of u of Apart[t][item][i]
+//   H[u][i]  = act(sum_k A[u][i][k] W1[k] + b1)   (k ascending, as sgemm)
+//   L == 3:  a_i = isd_i(0)(isd_i(0) H[0][i] + sum_{kept v in N(0)} isd_i(v) H[v][i])
+//            z_i = b2 + a_i W2 (bias-first, gcn.cpp:116-123)
+//   L == 2:  z_i = H[0][i] (logits, no activation)
+//   p_i = softmax(z_i) (gcn.cpp:143-152); out = p_i[cls].
+// Rows of A and H are u-major: r = u * cpb + il.
+__global__ void __launch_bounds__(256)
+    tail_kernel(const float4* __restrict__ Apart, uint32_t items,
+                const uint32_t* __restrict__ u_items, const uint64_t* __restrict__ maskt,
+                uint64_t Wp, const uint32_t* __restrict__ row_ptr,
+                const uint32_t* __restrict__ col, const uint32_t* __restrict__ ep,
+                const float* __restrict__ isd, uint32_t V, uint32_t U, uint32_t K,
+                uint32_t N, const float* __restrict__ W1, const float* __restrict__ b1,
+                const float* __restrict__ W2, const float* __restrict__ b2, uint32_t C,
+                int three_layer, uint32_t cls, uint64_t row0, uint64_t rows, uint32_t cpb,
+                float* __restrict__ out, float* __restrict__ allprobs) {
+  extern __shared__ float4 sm4[];
+  const uint32_t R = U * cpb, K4 = K / 4;
+  float4* sA = sm4;                                    // [R][K4]
+  float* sW1 = reinterpret_cast<float*>(sA + R * K4);  // [K][N]
+  float* sW2 = sW1 + K * N;                            // [N][C] (three_layer)
+  float* sH = sW2 + (three_layer ? N * C : 0);         // [R][N]
+  float* sa = sH + R * N;                              // [cpb][N]
+  float* sz = sa + cpb * N;                            // [cpb][C]
+  const uint64_t t = blockIdx.x;
+  const uint32_t i0 = blockIdx.y * cpb;
+  const float* isd_t = isd + t * uint64_t(V) * kTile;
+  const int tid = threadIdx.x;
+  for (uint32_t idx = tid; idx < K * N / 4; idx += blockDim.x)
+    reinterpret_cast<float4*>(sW1)[idx] = __ldg(reinterpret_cast<const float4*>(W1) + idx);
+  if (three_layer)
+    for (uint32_t idx = tid; idx < N * C; idx += blockDim.x) sW2[idx] = __ldg(&W2[idx]);
+  // A (partials in item order, then isd_i(u)); loads batched 4 items deep
+  for (uint32_t idx = tid; idx < R * K4; idx += blockDim.x) {
+    const uint32_t r = idx / K4, k4 = idx % K4, u = r / cpb, i = i0 + r % cpb;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t ib = u_items[u], ie = u_items[u + 1];
+    const float4* src = Apart + ((t * items) * kTile + i) * K4 + k4;
+    const uint64_t stride = uint64_t(kTile) * K4;
+    uint32_t it = ib;
+    for (; it + 4 <= ie; it += 4) {
+      float4 p[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) p[q] = src[(it + q) * stride];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        s.x += p[q].x;
+        s.y += p[q].y;
+        s.z += p[q].z;
+        s.w += p[q].w;
+      }
+    }
+    for (; it < ie; ++it) {
+      const float4 p = src[it * stride];
+      s.x += p.x;
+      s.y += p.y;
+      s.z += p.z;
+      s.w += p.w;
+    }
+    const float sc = isd_t[uint64_t(u) * kTile + i];
+    sA[idx] = make_float4(sc * s.x, sc * s.y, sc * s.z, sc * s.w);
+  }
+  __syncthreads();
+  // H = act(A W1 + b1): job = (column n, 4 rows)
+  constexpr uint32_t RB = 4;
+  const uint32_t groups = (R + RB - 1) / RB;
+  for (uint32_t job = tid; job < N * groups; job += blockDim.x) {
+    const uint32_t n = job % N, r0 = (job / N) * RB;
+    float acc[RB] = {};
+    for (uint32_t k4 = 0; k4 < K4; ++k4) {
+      const float w0 = sW1[(4 * k4) * N + n], w1 = sW1[(4 * k4 + 1) * N + n];
+      const float w2 = sW1[(4 * k4 + 2) * N + n], w3 = sW1[(4 * k4 + 3) * N + n];
+#pragma unroll
+      for (uint32_t j = 0; j < RB; ++j) {
+        if (r0 + j >= R) break;
+        const float4 a = sA[(r0 + j) * K4 + k4];
+        acc[j] = fmaf(a.x, w0, acc[j]);
+        acc[j] = fmaf(a.y, w1, acc[j]);
+        acc[j] = fmaf(a.z, w2, acc[j]);
+        acc[j] = fmaf(a.w, w3, acc[j]);
+      }
+    }
+    const float bn = b1[n];
+#pragma unroll
+    for (uint32_t j = 0; j < RB; ++j) {
+      if (r0 + j >= R) break;
+      const float v = acc[j] + bn;
+      sH[(r0 + j) * N + n] = three_layer ? fmaxf(v, 0.f) : v;
+    }
+  }
+  __syncthreads();
+  if (three_layer) {
+    const uint64_t* mt = maskt + t * Wp;
+    const uint32_t beg = row_ptr[0], end = row_ptr[1];
+    for (uint32_t idx = tid; idx < cpb * N; idx += blockDim.x) {
+      const uint32_t il = idx / N, f = idx % N, i = i0 + il;
+      float acc = isd_t[i] * sH[il * N + f];
+      for (uint32_t e = beg; e < end; ++e) {
+        if (!((mt[ep[e]] >> i) & 1ull)) continue;
+        const uint32_t v = col[e];
+        acc = fmaf(isd_t[uint64_t(v) * kTile + i], sH[(v * cpb + il) * N + f], acc);
+      }
+      sa[idx] = isd_t[i] * acc;
+    }
+    __syncthreads();
+    for (uint32_t idx = tid; idx < cpb * C; idx += blockDim.x) {
+      const uint32_t il = idx / C, c = idx % C;
+      float v = b2[c];
+      for (uint32_t k = 0; k < N; ++k) v = __fadd_rn(v, __fmul_rn(sa[il * N + k], sW2[k * C + c]));
+      sz[idx] = v;
+    }
+  } else {
+    for (uint32_t idx = tid; idx < cpb * C; idx += blockDim.x) sz[idx] = sH[idx];  // U == 1: row il
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (uint32_t il = warp; il < cpb; il += nwarps) {
+    const uint64_t row = row0 + t * kTile + i0 + il;
+    if (row >= rows) continue;
+    if (lane == 0) {
+      softmax_row(sz + il * C, C);
+      out[row] = sz[il * C + cls];
+    }
+    __syncwarp();
+    if (allprobs)
+      for (uint32_t c = lane; c < C; c += 32) allprobs[row * C + c] = sz[il * C + c];
+  }
+}
+
+size_t tail_smem(uint32_t U, uint32_t K, uint32_t N, uint32_t C, uint32_t cpb, bool three_layer) {
+  return (size_t(U) * cpb * (K + N) + size_t(cpb) * (N + C) + size_t(K) * N +
+          (three_layer ? size_t(N) * C : 0)) * 4;
+}
+
 // X W0 for the whole subgraph (once per target)
 void gemm(Ctx& ctx, const float* A, const float* B, const float* bias, float* Cm,
           uint64_t M, uint32_t N, uint32_t K, bool relu) {
@@ -722,6 +900,7 @@ void gemm(Ctx& ctx, const float* A, const float* B, const float* bias, float* Cm
 
 namespace {
 constexpr uint32_t kItemEntries = 512;  // target staged entries per work item
+constexpr size_t kTailSmem = 200 * 1024;  // fused tail kernel shared-memory cap
 
 bool fused_width(uint64_t d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256; }
 
@@ -837,6 +1016,20 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   e.row_ptr.upload(rp.data(), rp.size(), ctx.stream);
   e.col.upload(sg.col.data(), sg.col.size(), ctx.stream);
   e.edge_player.upload(sg.edge_player.data(), sg.edge_player.size(), ctx.stream);
+  {  // isd_kernel: nodes by descending degree, 1/sqrt(deg) table
+    std::vector<uint32_t> order(e.V);
+    uint32_t maxdeg = 0;
+    for (uint32_t v = 0; v < e.V; ++v) {
+      order[v] = v;
+      maxdeg = std::max(maxdeg, rp[v + 1] - rp[v]);
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t a, uint32_t b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+    e.isd_order.upload(order.data(), order.size(), ctx.stream);
+    e.isd_tab.reserve(maxdeg + 2);
+    isd_table_kernel<<<(maxdeg + 2 + 255) / 256, 256, 0, ctx.stream>>>(e.isd_tab.p, maxdeg + 2);
+    SF_LAUNCHED(ctx);
+  }
   // P0 = X W0 on the device
   DevBuf<float> x, w0;
   x.upload(sg.features.data(), sg.features.size(), ctx.stream);
@@ -926,8 +1119,9 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
     const uint64_t ntp = wide ? (nt + 1) & ~uint64_t(1) : nt;  // tiles the fused kernel covers
     launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, ntp, maskt);
     {
-      dim3 grid((e.V + 7) / 8, unsigned(ntp));
-      isd_kernel<<<grid, 256, 0, ctx.stream>>>(maskt, Wp, e.row_ptr.p, e.edge_player.p, e.V, isd);
+      dim3 grid(unsigned((ntp + 1) / 2), (e.V + 7) / 8);
+      isd_kernel<<<grid, 256, 0, ctx.stream>>>(maskt, Wp, ntp, e.row_ptr.p, e.edge_player.p,
+                                               e.isd_order.p, e.isd_tab.p, e.V, isd);
       SF_LAUNCHED(ctx);
     }
     const float* X = e.p0.p;  // current layer input: P0 (shared) or per-coalition H
@@ -960,6 +1154,28 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       if (!ok) throw std::logic_error("fused width not instantiated");
       if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
+      if (L <= 3) {  // fused tail: reduce + layer 1 + last layer + softmax in one kernel
+        uint32_t cpb = 4;
+        while (cpb > 1 && tail_smem(e.U, K, N, C, cpb, L == 3) > kTailSmem) cpb /= 2;
+        if (tail_smem(e.U, K, N, C, cpb, L == 3) <= kTailSmem) {
+          const size_t smem = tail_smem(e.U, K, N, C, cpb, L == 3);
+          static bool attr = false;
+          if (!attr) {
+            SF_CUDA(cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kTailSmem)));
+            attr = true;
+          }
+          dim3 grid(unsigned(nt), kTile / cpb);
+          tail_kernel<<<grid, 256, smem, ctx.stream>>>(
+              reinterpret_cast<const float4*>(pbuf), e.tc ? e.tc_items : e.items,
+              e.tc ? e.tc_u_items.p : e.u_items.p, maskt, Wp, e.row_ptr.p, e.col.p,
+              e.edge_player.p, isd, e.V, e.U, K, N, e.w[1]->p, e.b[1]->p,
+              L == 3 ? e.w[2]->p : nullptr, L == 3 ? e.b[2]->p : nullptr, C, L == 3 ? 1 : 0, cls,
+              row0, rows, cpb, dev_out, dev_allprobs);
+          SF_LAUNCHED(ctx);
+          continue;
+        }
+      }
       {
         const uint64_t work = uint64_t(e.U) * kTile * (K / 4);
         dim3 grid(unsigned((work + 255) / 256), unsigned(nt));

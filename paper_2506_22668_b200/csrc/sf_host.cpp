@@ -791,6 +791,18 @@ int sf_ctx_set_fused_kernel(sf_ctx* ctx, int kind) {
   });
 }
 
+int sf_ctx_fused_plan(const sf_ctx* ctx, uint64_t* entries, uint64_t* padded_entries,
+                      uint32_t* items, uint32_t* width) {
+  return guard([&] {
+    need(ctx, "context");
+    const Engine& e = ctx->c.engine;
+    if (entries) *entries = e.fused ? e.entries : 0;
+    if (padded_entries) *padded_entries = e.tc ? e.tc_entries : 0;
+    if (items) *items = e.fused ? (e.tc ? e.tc_items : e.items) : 0;
+    if (width) *width = e.fused ? uint32_t(e.dims[1]) : 0;
+  });
+}
+
 int sf_ctx_fused_kernel_used(const sf_ctx* ctx) {
   if (!ctx) return -1;
   const Engine& e = ctx->c.engine;

@@ -150,6 +150,8 @@ struct Engine {
   std::vector<uint64_t> dims;       // d_0..d_L
   std::vector<uint64_t> ball;       // |B_h|, h = 0..L
   DevBuf<uint32_t> row_ptr, col, edge_player;
+  DevBuf<uint32_t> isd_order;  // nodes by descending degree (isd_kernel)
+  DevBuf<float> isd_tab;       // inv_sqrt_deg(d), d = 0..maxdeg+1
   DevBuf<float> p0;                 // X W_0, V x d_1 (layer-0 transform-first)
   std::vector<std::unique_ptr<DevBuf<float>>> w, b;  // per layer (w[0] unused)
   // Fused layer-0 + layer-1 aggregation plan:
@@ -165,6 +167,7 @@ struct Engine {
   // tensor-core (tcgen05) plan: segments padded to 8 entries (sf_fused_tc.cu)
   bool tc = false;
   uint32_t tc_items = 0;
+  uint64_t tc_entries = 0;  // padded entries (K of the per-tile MMA chain)
   DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items, tc_const;
   DevBuf<uint8_t> tc_kflags;
 };

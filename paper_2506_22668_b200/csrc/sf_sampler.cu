@@ -234,9 +234,16 @@ __global__ void philox_stream_kernel(uint64_t seed, uint64_t stream,
   if (2 * b + 1 < count) out[2 * b + 1] = s;
 }
 
-// rows (row-major, W words) -> tiles: out[t][e] u64 with bit i = bit e of
-// row t*64+i (rows past `rows` read as zero). One CTA per (tile, 32-word
-// chunk): stage 64 x 32 words in smem, then 64 ballots per half-tile.
+// Rows -> tile layout: out[t][e] bit i = bit e of row t*64+i (rows past
+// `rows` read as zero). One CTA per (tile, 32-word chunk) stages the
+// 64 x 32 words coalesced in shared memory; each warp then transposes 4
+// words, each a 64 x 64 bit block, as four 32 x 32 butterfly transposes
+// (5 shuffle stages each) and writes 256 contiguous bytes per output half.
+__device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t m, int lane) {
+  const uint32_t y = __shfl_xor_sync(kFull, x, s);
+  return (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+}
+
 __global__ void __launch_bounds__(256)
     transpose_tiles_kernel(const uint64_t* __restrict__ in, uint64_t rows,
                            uint32_t W, uint64_t* __restrict__ out) {
@@ -250,27 +257,24 @@ __global__ void __launch_bounds__(256)
     sm[r][w] = (row < rows && w0 + w < W) ? in[row * W + w0 + w] : 0ull;
   }
   __syncthreads();
-  uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
   const uint64_t Wp = uint64_t(W) * 64;  // players per tile, padded
-  // 8 warps x 8 (word, half) jobs = 32 words x 2 halves
-  for (int job = warp; job < 64; job += 8) {
-    const int w = job >> 1, h = job & 1;
-    if (w0 + w >= W) continue;
-    const uint64_t v = sm[h * 32 + lane][w];
-    uint32_t lo = 0, hi = 0;
+#pragma unroll 1
+  for (int w = warp * 4; w < warp * 4 + 4; ++w) {
+    if (w0 + w >= W) break;
+    const uint64_t r0 = sm[lane][w], r1 = sm[lane + 32][w];
+    uint32_t a = uint32_t(r0), b = uint32_t(r0 >> 32), c = uint32_t(r1), d = uint32_t(r1 >> 32);
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const uint32_t b = __ballot_sync(kFull, (v >> j) & 1ull);
-      if (lane == (j & 31)) {
-        if (j < 32)
-          lo = b;
-        else
-          hi = b;
-      }
+    for (int s = 16; s >= 1; s >>= 1) {
+      const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                       : s == 2 ? 0x33333333u : 0x55555555u;
+      a = bfly_step(a, s, m, lane);
+      b = bfly_step(b, s, m, lane);
+      c = bfly_step(c, s, m, lane);
+      d = bfly_step(d, s, m, lane);
     }
-    const uint64_t e = uint64_t(w0 + w) * 64 + lane;
-    out32[(t * Wp + e) * 2 + h] = lo;
-    out32[(t * Wp + e + 32) * 2 + h] = hi;
+    uint64_t* o = out + t * Wp + uint64_t(w0 + w) * 64;
+    o[lane] = (uint64_t(c) << 32) | a;
+    o[lane + 32] = (uint64_t(d) << 32) | b;
   }
 }
 
