@@ -10,15 +10,18 @@
 // plan (zero coefficients), so every segment is a whole number of MMA
 // k-steps.
 //
-// Warp roles (416 threads):
-//   warps 0-3   epilogue: per finished segment, tcgen05.ld H_v, fold it into
-//               the TMEM accumulator A_u, release the H buffer
-//   warps 4-11  staging: per 32-entry chunk build the A (coefficients) and
+// Warp roles (640 threads):
+//   warps 0-7   epilogue: per finished segment, tcgen05.ld H_v, fold it into
+//               the TMEM accumulator A_u, release the H buffer; warps q and
+//               q+4 share TMEM lane quarter q and split the columns
+//   warps 8-14  staging: per 32-entry chunk build the A (coefficients) and
 //               B (gathered P rows, transposed) operand tiles, hi/lo split,
 //               both K-major in the canonical no-swizzle layout (MN-major
 //               tf32 without swizzle produced no output on B200; see
 //               csrc/tools/tc_probe.cu, which checks the layouts exactly)
-//   warp 12     one elected thread issues the MMAs and the commits
+//   warps 15-18 producers: cp.async gathers of entry records, P rows, isd
+//               rows and mask words into a raw ring
+//   warp 19     one elected thread issues the MMAs and the commits
 // Pipelines: kStages smem stages (full/empty mbarriers), two TMEM H buffers
 // (hfull/hfree mbarriers).
 #include <cuda_runtime.h>
@@ -41,7 +44,7 @@ constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
 constexpr int kRawStages = 2, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 4, kStgWarps = 11, kProdWarps = 4;
+constexpr int kEpiWarps = 8, kStgWarps = 7, kProdWarps = 4;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 
@@ -61,7 +64,8 @@ struct TcCfg {
   static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
   static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
-  static constexpr int OFF_BARS = OFF_KFL + kMaxKsteps;
+  static constexpr int OFF_BIAS = OFF_KFL + kMaxKsteps;      // b0 (D floats)
+  static constexpr int OFF_BARS = OFF_BIAS + D * 4;
   static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
   static constexpr uint32_t TMEM_COLS = 3 * D <= 256 ? 256 : 512;  // 2 H buffers + accumulator
   static_assert(D % 32 == 0 && D <= 256, "width");
@@ -156,6 +160,32 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
       "r"(r[30]), "r"(r[31])                                                                       \
       : "memory")
 
+#define TC_LD16(taddr, r)                                                                          \
+  asm volatile(                                                                                    \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+      "%15}, [%16];"                                                                               \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
+        "=r"(r[14]), "=r"(r[15])                                                                   \
+      : "r"(taddr))
+#define TC_ST16(taddr, r)                                                                          \
+  asm volatile(                                                                                    \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+      "%14,%15,%16};" ::"r"(taddr),                                                                \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),      \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) \
+      : "memory")
+
+// (d0, d1) = (a0 b0 + c0, a1 b1 + c1), one packed FFMA2 (each lane fma.rn)
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
+                                      float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -204,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int j = tid; j < D; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_BIAS)[j] = bias[j];
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "r"(Cfg::TMEM_COLS));
@@ -353,19 +384,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp;  // TMEM lane quarter
+    // warp w: TMEM lane quarter w % 4 (coalitions), columns [hb, hb + D/2)
+    constexpr int HALF = D / 2, CW = HALF >= 32 ? 32 : 16, NCH = HALF / CW;
+    const int q = warp & 3;
+    const int hb = (warp >> 2) * HALF;
     const int m = q * 32 + lane;
     const uint64_t tile = t0 + (m >> 6);
     const int i = m & 63;
     const uint64_t* mt = maskt + tile * Wp;
     const float* isd_t = isd + tile * uint64_t(V) * kTile;
+    const float* sbias = reinterpret_cast<const float*>(smem + Cfg::OFF_BIAS);
     const uint32_t lane_base = uint32_t(q * 32) << 16;
-    const uint32_t acc_col = 2 * D;
-    uint32_t r[32], a[32];
+    const uint32_t acc_col = 2 * D + hb;
+    uint32_t r[CW], a[CW];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) a[j] = 0u;
+    for (int j = 0; j < CW; ++j) a[j] = 0u;
 #pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) TC_ST32(tmem + lane_base + acc_col + cc * 32, a);
+    for (int cc = 0; cc < NCH; ++cc) {
+      if constexpr (CW == 32) TC_ST32(tmem + lane_base + acc_col + cc * CW, a);
+      else TC_ST16(tmem + lane_base + acc_col + cc * CW, a);
+    }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     const uint32_t s0 = item_seg[item], s1 = item_seg[item + 1];
     auto factors = [&](uint32_t k, float& svk, float& dvk) {
@@ -383,23 +421,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&hfull[b], (sg >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc) {
-        TC_LD32(tmem + lane_base + b * D + cc * 32, r);
-        TC_LD32(tmem + lane_base + acc_col + cc * 32, a);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const float4* b4 = reinterpret_cast<const float4*>(bias + cc * 32);
-#pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 bb = __ldg(b4 + j4);
-          const float bj[4] = {bb.x, bb.y, bb.z, bb.w};
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int j = 4 * j4 + w;
-            const float hv = fmaxf(fmaf(sv, __uint_as_float(r[j]), bj[w]), 0.f);
-            a[j] = __float_as_uint(fmaf(dv, hv, __uint_as_float(a[j])));
-          }
+      for (int cc = 0; cc < NCH; ++cc) {
+        const uint32_t hcol = tmem + lane_base + b * D + hb + cc * CW;
+        const uint32_t acol = tmem + lane_base + acc_col + cc * CW;
+        if constexpr (CW == 32) {
+          TC_LD32(hcol, r);
+          TC_LD32(acol, a);
+        } else {
+          TC_LD16(hcol, r);
+          TC_LD16(acol, a);
         }
-        TC_ST32(tmem + lane_base + acc_col + cc * 32, a);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const float4* b4 = reinterpret_cast<const float4*>(sbias + hb + cc * CW);
+#pragma unroll
+        for (int j4 = 0; j4 < CW / 4; ++j4) {
+          const float4 bb = b4[j4];
+          const int j = 4 * j4;
+          float h0, h1, h2, h3;
+          ffma2(h0, h1, sv, sv, __uint_as_float(r[j]), __uint_as_float(r[j + 1]), bb.x, bb.y);
+          ffma2(h2, h3, sv, sv, __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]), bb.z, bb.w);
+          h0 = fmaxf(h0, 0.f);
+          h1 = fmaxf(h1, 0.f);
+          h2 = fmaxf(h2, 0.f);
+          h3 = fmaxf(h3, 0.f);
+          float a0, a1, a2, a3;
+          ffma2(a0, a1, dv, dv, h0, h1, __uint_as_float(a[j]), __uint_as_float(a[j + 1]));
+          ffma2(a2, a3, dv, dv, h2, h3, __uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+          a[j] = __float_as_uint(a0);
+          a[j + 1] = __float_as_uint(a1);
+          a[j + 2] = __float_as_uint(a2);
+          a[j + 3] = __float_as_uint(a3);
+        }
+        if constexpr (CW == 32) TC_ST32(acol, a);
+        else TC_ST16(acol, a);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
@@ -408,15 +462,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       sv = sv_next;
       dv = dv_next;
     }
-    // write the accumulator: Apart[tile][item][i][:]
-    float* out = Apart + ((tile * items + item) * kTile + i) * uint64_t(D);
+    // write the accumulator: Apart[tile][item][i][hb ..]
+    float* out = Apart + ((tile * items + item) * kTile + i) * uint64_t(D) + hb;
 #pragma unroll 1
-    for (int cc = 0; cc < D / 32; ++cc) {
-      TC_LD32(tmem + lane_base + acc_col + cc * 32, a);
+    for (int cc = 0; cc < NCH; ++cc) {
+      if constexpr (CW == 32) TC_LD32(tmem + lane_base + acc_col + cc * CW, a);
+      else TC_LD16(tmem + lane_base + acc_col + cc * CW, a);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4)
-        reinterpret_cast<float4*>(out + cc * 32)[j4] =
+      for (int j4 = 0; j4 < CW / 4; ++j4)
+        reinterpret_cast<float4*>(out + cc * CW)[j4] =
             make_float4(__uint_as_float(a[4 * j4]), __uint_as_float(a[4 * j4 + 1]),
                         __uint_as_float(a[4 * j4 + 2]), __uint_as_float(a[4 * j4 + 3]));
     }

@@ -33,11 +33,14 @@ constexpr int kTile = 64;  // coalitions per tile
 // deg_i(u) = 1 + sum over u's CSR entries of bit_i(edge_player) (the
 // self-loop counts, gcn.cpp:76-81), isd = 1/sqrt(deg) read from a table of
 // the correctly rounded values (inv_sqrt_deg, bitwise equal to gcn.cpp:82).
-// One warp per (node, 2 tiles), nodes in descending degree order so hubs
-// start first. Lane l owns coalitions l and l+32 of each tile. A chunk of up
-// to 32 incidences is loaded one per lane; chunks longer than 8 are counted
-// by transposing the 32 x 64 bit block (rows = incidences) with a butterfly
-// and taking popc, shorter ones by broadcasting each word.
+// Nodes are taken in descending degree order (hubs first). A node with more
+// than 32 incidences ("big", the first nbig in that order) gets one warp per
+// tile and counts 32-incidence chunks; any other node gets one warp for all
+// tiles, with G = next power of two >= degree incidence slots per tile and
+// 32/G tiles per pass. Each pass loads one mask word per lane (row j = tile
+// j/G, incidence j%G), transposes the 32 x 64 bit block with a butterfly so
+// lane l holds coalitions l and l+32, and counts each tile's G-bit field
+// with popc.
 __device__ __forceinline__ uint32_t bfly32(uint32_t x, int lane) {
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) {
@@ -50,47 +53,58 @@ __device__ __forceinline__ uint32_t bfly32(uint32_t x, int lane) {
 }
 
 __global__ void __launch_bounds__(256)
-    isd_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, uint64_t ntiles,
+    isd_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, uint32_t ntiles,
                const uint32_t* __restrict__ row_ptr,
                const uint32_t* __restrict__ ep, const uint32_t* __restrict__ order,
-               const float* __restrict__ tab, uint32_t V, float* __restrict__ isd) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t j = blockIdx.y * 8 + warp;
-  const uint64_t t0 = uint64_t(blockIdx.x) * 2;
-  if (j >= V) return;
-  const bool two = t0 + 1 < ntiles;
-  const uint32_t u = order[j];
-  const uint64_t* m0 = maskt + t0 * Wp;
-  const uint64_t* m1 = two ? m0 + Wp : m0;
-  uint32_t c0lo = 1, c0hi = 1, c1lo = 1, c1hi = 1;  // self loop
-  const uint32_t beg = row_ptr[u], end = row_ptr[u + 1];
-  for (uint32_t i0 = beg; i0 < end; i0 += 32) {
-    const uint32_t i = i0 + lane, cnt = min(32u, end - i0);
-    const uint32_t p = i < end ? __ldg(&ep[i]) : 0u;
-    const uint64_t w0 = i < end ? __ldg(&m0[p]) : 0ull;
-    const uint64_t w1 = i < end ? __ldg(&m1[p]) : 0ull;
-    if (cnt > 8) {
-      c0lo += __popc(bfly32(uint32_t(w0), lane));
-      c0hi += __popc(bfly32(uint32_t(w0 >> 32), lane));
-      c1lo += __popc(bfly32(uint32_t(w1), lane));
-      c1hi += __popc(bfly32(uint32_t(w1 >> 32), lane));
-    } else {
-      for (uint32_t k = 0; k < cnt; ++k) {
-        const uint64_t x0 = __shfl_sync(kFull, w0, k), x1 = __shfl_sync(kFull, w1, k);
-        c0lo += (uint32_t(x0) >> lane) & 1u;
-        c0hi += (uint32_t(x0 >> 32) >> lane) & 1u;
-        c1lo += (uint32_t(x1) >> lane) & 1u;
-        c1hi += (uint32_t(x1 >> 32) >> lane) & 1u;
-      }
+               uint32_t nbig, const float* __restrict__ tab, uint32_t V,
+               float* __restrict__ isd) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const uint32_t big_warps = nbig * ntiles;
+  if (w < big_warps) {  // hub: one tile, 32-incidence chunks
+    const uint32_t u = order[w / ntiles];
+    const uint64_t t = w % ntiles;
+    const uint64_t* mt = maskt + t * Wp;
+    uint32_t clo = 1, chi = 1;
+    const uint32_t beg = row_ptr[u], end = row_ptr[u + 1];
+    for (uint32_t i = beg + lane; i - lane < end; i += 32) {
+      const uint64_t x = i < end ? __ldg(&mt[__ldg(&ep[i])]) : 0ull;
+      clo += __popc(bfly32(uint32_t(x), lane));
+      chi += __popc(bfly32(uint32_t(x >> 32), lane));
     }
+    float* out = isd + (t * V + u) * kTile;
+    out[lane] = __ldg(&tab[clo]);
+    out[lane + 32] = __ldg(&tab[chi]);
+    return;
   }
-  float* out = isd + (t0 * V + u) * kTile;
-  out[lane] = __ldg(&tab[c0lo]);
-  out[lane + 32] = __ldg(&tab[c0hi]);
-  if (two) {
-    out += uint64_t(V) * kTile;
-    out[lane] = __ldg(&tab[c1lo]);
-    out[lane + 32] = __ldg(&tab[c1hi]);
+  const uint32_t j = nbig + (w - big_warps);
+  if (j >= V) return;
+  const uint32_t u = order[j];
+  const uint32_t beg = row_ptr[u], deg = row_ptr[u + 1] - beg;
+  if (deg == 0) {
+    const float one = __ldg(&tab[1]);
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      float* out = isd + (uint64_t(t) * V + u) * kTile;
+      out[lane] = one;
+      out[lane + 32] = one;
+    }
+    return;
+  }
+  const int lg = deg <= 1 ? 0 : 32 - __clz(deg - 1);  // G = 1 << lg >= deg
+  const uint32_t G = 1u << lg, per = 32u >> lg;
+  const uint32_t slot = lane & (G - 1), sub = lane >> lg;
+  const uint32_t p = slot < deg ? __ldg(&ep[beg + slot]) : 0u;
+  const uint32_t fmask = G == 32 ? 0xFFFFFFFFu : (1u << G) - 1u;
+  for (uint32_t t0 = 0; t0 < ntiles; t0 += per) {
+    const uint32_t t = t0 + sub;
+    const uint64_t x = (slot < deg && t < ntiles) ? __ldg(&maskt[uint64_t(t) * Wp + p]) : 0ull;
+    const uint32_t lo = bfly32(uint32_t(x), lane), hi = bfly32(uint32_t(x >> 32), lane);
+    for (uint32_t q = 0; q < per && t0 + q < ntiles; ++q) {
+      const uint32_t sh = q << lg;
+      float* out = isd + (uint64_t(t0 + q) * V + u) * kTile;
+      out[lane] = __ldg(&tab[1 + __popc((lo >> sh) & fmask)]);
+      out[lane + 32] = __ldg(&tab[1 + __popc((hi >> sh) & fmask)]);
+    }
   }
 }
 
@@ -781,11 +795,23 @@ __global__ void __launch_bounds__(256)
   const uint32_t i0 = blockIdx.y * cpb;
   const float* isd_t = isd + t * uint64_t(V) * kTile;
   const int tid = threadIdx.x;
-  for (uint32_t idx = tid; idx < K * N / 4; idx += blockDim.x)
-    reinterpret_cast<float4*>(sW1)[idx] = __ldg(reinterpret_cast<const float4*>(W1) + idx);
-  if (three_layer)
-    for (uint32_t idx = tid; idx < N * C; idx += blockDim.x) sW2[idx] = __ldg(&W2[idx]);
-  // A (partials in item order, then isd_i(u)); loads batched 4 items deep
+  {  // weights -> shared memory with cp.async, overlapped with the partial sums below
+    const uint32_t n1 = K * N / 4;
+    for (uint32_t idx = tid; idx < n1; idx += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(sW1 + 4 * idx))),
+                   "l"(W1 + 4 * idx) : "memory");
+    if (three_layer) {
+      const uint32_t n2 = N * C / 4;
+      for (uint32_t idx = tid; idx < n2; idx += blockDim.x)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(sW2 + 4 * idx))),
+                     "l"(W2 + 4 * idx) : "memory");
+      for (uint32_t idx = 4 * n2 + tid; idx < N * C; idx += blockDim.x) sW2[idx] = __ldg(&W2[idx]);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // A (partials in item order, then isd_i(u)); loads batched 8 items deep
   for (uint32_t idx = tid; idx < R * K4; idx += blockDim.x) {
     const uint32_t r = idx / K4, k4 = idx % K4, u = r / cpb, i = i0 + r % cpb;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -793,12 +819,12 @@ __global__ void __launch_bounds__(256)
     const float4* src = Apart + ((t * items) * kTile + i) * K4 + k4;
     const uint64_t stride = uint64_t(kTile) * K4;
     uint32_t it = ib;
-    for (; it + 4 <= ie; it += 4) {
-      float4 p[4];
+    for (; it + 8 <= ie; it += 8) {
+      float4 p[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) p[q] = src[(it + q) * stride];
+      for (int q = 0; q < 8; ++q) p[q] = src[(it + q) * stride];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         s.x += p[q].x;
         s.y += p[q].y;
         s.z += p[q].z;
@@ -815,6 +841,7 @@ __global__ void __launch_bounds__(256)
     const float sc = isd_t[uint64_t(u) * kTile + i];
     sA[idx] = make_float4(sc * s.x, sc * s.y, sc * s.z, sc * s.w);
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   // H = act(A W1 + b1): job = (column n, 4 rows)
   constexpr uint32_t RB = 4;
@@ -1026,6 +1053,8 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     std::stable_sort(order.begin(), order.end(),
                      [&](uint32_t a, uint32_t b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
     e.isd_order.upload(order.data(), order.size(), ctx.stream);
+    e.isd_nbig = 0;
+    while (e.isd_nbig < e.V && rp[order[e.isd_nbig] + 1] - rp[order[e.isd_nbig]] > 32) ++e.isd_nbig;
     e.isd_tab.reserve(maxdeg + 2);
     isd_table_kernel<<<(maxdeg + 2 + 255) / 256, 256, 0, ctx.stream>>>(e.isd_tab.p, maxdeg + 2);
     SF_LAUNCHED(ctx);
@@ -1119,9 +1148,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
     const uint64_t ntp = wide ? (nt + 1) & ~uint64_t(1) : nt;  // tiles the fused kernel covers
     launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, ntp, maskt);
     {
-      dim3 grid(unsigned((ntp + 1) / 2), (e.V + 7) / 8);
-      isd_kernel<<<grid, 256, 0, ctx.stream>>>(maskt, Wp, ntp, e.row_ptr.p, e.edge_player.p,
-                                               e.isd_order.p, e.isd_tab.p, e.V, isd);
+      const uint64_t warps = uint64_t(e.isd_nbig) * ntp + (e.V - e.isd_nbig);
+      isd_kernel<<<unsigned((warps + 7) / 8), 256, 0, ctx.stream>>>(
+          maskt, Wp, uint32_t(ntp), e.row_ptr.p, e.edge_player.p, e.isd_order.p, e.isd_nbig,
+          e.isd_tab.p, e.V, isd);
       SF_LAUNCHED(ctx);
     }
     const float* X = e.p0.p;  // current layer input: P0 (shared) or per-coalition H

@@ -151,6 +151,7 @@ struct Engine {
   std::vector<uint64_t> ball;       // |B_h|, h = 0..L
   DevBuf<uint32_t> row_ptr, col, edge_player;
   DevBuf<uint32_t> isd_order;  // nodes by descending degree (isd_kernel)
+  uint32_t isd_nbig = 0;       // nodes with more than 32 incidences
   DevBuf<float> isd_tab;       // inv_sqrt_deg(d), d = 0..maxdeg+1
   DevBuf<float> p0;                 // X W_0, V x d_1 (layer-0 transform-first)
   std::vector<std::unique_ptr<DevBuf<float>>> w, b;  // per layer (w[0] unused)
