@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "sf_device.cuh"
@@ -42,21 +43,20 @@ constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
 constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
-constexpr int kRawStages = 2, kCanStages = 2;
+constexpr int kRawStages = 3, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 8, kStgWarps = 7, kProdWarps = 4;
+constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 3;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 
 template <int D>
 struct TcCfg {
-  static constexpr int A_BYTES = kM * kKC * 4;        // one of hi / lo
+  // smem stage: B (gathered P rows, K-major) hi | lo; A lives in TMEM
   static constexpr int B_LBO = (D / 8) * 128;          // k-unit stride (n-groups of 8 rows)
   static constexpr int B_BYTES = D * kKC * 4;
-  static constexpr int OFF_ALO = A_BYTES;
-  static constexpr int OFF_BHI = 2 * A_BYTES;
-  static constexpr int OFF_BLO = 2 * A_BYTES + B_BYTES;
-  static constexpr int STAGE = ((2 * A_BYTES + 2 * B_BYTES + 1023) / 1024) * 1024;  // canonical tiles
+  static constexpr int OFF_BHI = 0;
+  static constexpr int OFF_BLO = B_BYTES;
+  static constexpr int STAGE = ((2 * B_BYTES + 1023) / 1024) * 1024;
   // raw stage (bulk copies): records | P rows | isd rows (2 tiles) | mask blocks (2 tiles)
   static constexpr int RAW_P = kKC * 8;
   static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
@@ -67,7 +67,10 @@ struct TcCfg {
   static constexpr int OFF_BIAS = OFF_KFL + kMaxKsteps;      // b0 (D floats)
   static constexpr int OFF_BARS = OFF_BIAS + D * 4;
   static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
-  static constexpr uint32_t TMEM_COLS = 3 * D <= 256 ? 256 : 512;  // 2 H buffers + accumulator
+  // TMEM columns: H buffers [0, 2D), accumulator [2D, 3D), A stages (hi 32 | lo 32) from 3D
+  static constexpr uint32_t A_COL = 3 * D;
+  static constexpr uint32_t TMEM_COLS = 3 * D + kCanStages * 2 * kKC <= 256 ? 256 : 512;
+  static_assert(3 * D + kCanStages * 2 * kKC <= 512, "TMEM columns");
   static_assert(D % 32 == 0 && D <= 256, "width");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
@@ -127,6 +130,17 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem] (A: lane = row m, column = k; see
+// csrc/tools/tc_ts_probe.cu)
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 // Shared-memory matrix descriptor, no swizzle (SmemDescriptor, version 1)
@@ -195,15 +209,40 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // entry: (x, e) — P / isd row x, mask player e (kSelf: always kept, kPad:
 // coefficient 0). kflags[k-step]: bit0 segment start, bit1 segment end.
 // seg: (v, e_uv) per segment in item order.
-template <int D>
+// PROF instantiation (env SF_TC_PROF): clock64 cycles spent in each
+// mbarrier wait and per role, summed over warps into prof[kProfSites].
+constexpr int kProfSites = 16;
+#define TC_WAIT(site, bar, par)                        \
+  do {                                                 \
+    if constexpr (PROF) {                              \
+      const long long _t = clock64();                  \
+      mbar_wait(bar, par);                             \
+      pw[site] += uint64_t(clock64() - _t);            \
+    } else {                                           \
+      mbar_wait(bar, par);                             \
+    }                                                  \
+  } while (0)
+
+template <int D, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
                     uint32_t V, const float* __restrict__ P, const float* __restrict__ bias,
                     const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
                     const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
-                    uint32_t items, const uint64_t* __restrict__ const_words, float* __restrict__ Apart) {
+                    uint32_t items, const uint64_t* __restrict__ const_words, float* __restrict__ Apart,
+                    unsigned long long* __restrict__ prof, int exp) {
   using Cfg = TcCfg<D>;
+  uint64_t pw[3] = {0, 0, 0};
+  const long long t_begin = PROF ? clock64() : 0;
+  auto prof_flush = [&](int base, int n) {
+    if constexpr (PROF) {
+      if ((threadIdx.x & 31) == 0) {
+        for (int k = 0; k < n; ++k) atomicAdd(&prof[base + k], (unsigned long long)pw[k]);
+        atomicAdd(&prof[base + n], (unsigned long long)(clock64() - t_begin));
+      }
+    }
+  };
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BARS);
   uint64_t* raw_full = bars;                   // producer (expect_tx) -> staging
@@ -250,7 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 16-byte cp.async gathers (LDGSTS) of the chunk's records, P rows, isd
     // rows (both tiles) and mask blocks; each producer thread arrives on
     // raw_full once its own copies have landed.
-    const int pt = tid - kProducerWarp * 32;  // 0..127
+    const int pt = tid - kProducerWarp * 32;
+    const int pw_base = pt - lane;  // first J of this warp  // 0..127
     uint2 rec_next = make_uint2(0, kPad);
     if (lane < int(e1 - e0)) rec_next = ent[e0 + lane];
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -259,20 +299,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cnt = int(min(uint32_t(kKC), e1 - base));
       const uint2 rec = lane < cnt ? rec_next : make_uint2(0, kPad);
       if (base + kKC + lane < e1) rec_next = ent[base + kKC + lane];
-      if (c >= uint32_t(kRawStages)) mbar_wait(&raw_empty[r], ((c / kRawStages) - 1) & 1);
+      if (c >= uint32_t(kRawStages)) TC_WAIT(0, &raw_empty[r], ((c / kRawStages) - 1) & 1);
       unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       if (pt < cnt / 2) cp_async16(rw + pt * 16, ent + base + 2 * pt);  // records
-      for (int J = pt; J < cnt * (D / 4); J += kProdWarps * 32) {      // P rows
-        const int k = J / (D / 4), ng = J % (D / 4);
-        const uint32_t x = __shfl_sync(kFull, rec.x, k);
-        cp_async16(rw + Cfg::RAW_P + (k * D + ng * 4) * 4, P + uint64_t(x) * D + ng * 4);
-      }
-      for (int J = pt; J < cnt * 2 * 16; J += kProdWarps * 32) {        // isd rows, 2 tiles
-        const int k = J >> 5, q = (J >> 4) & 1, ug = J & 15;
-        const uint32_t x = __shfl_sync(kFull, rec.x, k);
-        cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
-                   isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
-      }
+      // trip counts are warp-uniform (J0 steps by whole warps), so every lane
+      // takes part in the shuffles
+      if (!PROF || !(exp & 2))
+        for (int J0 = pw_base; J0 < cnt * (D / 4); J0 += kProdWarps * 32) {  // P rows
+          const int J = J0 + lane, k = min(J / (D / 4), 31), ng = J % (D / 4);
+          const uint32_t x = __shfl_sync(kFull, rec.x, k);
+          if (J < cnt * (D / 4)) cp_async16(rw + Cfg::RAW_P + (k * D + ng * 4) * 4, P + uint64_t(x) * D + ng * 4);
+        }
+      if (!PROF || !(exp & 1))
+        for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
+          const int J = J0 + lane, k = min(J >> 5, 31), q = (J >> 4) & 1, ug = J & 15;
+          const uint32_t x = __shfl_sync(kFull, rec.x, k);
+          if (J < cnt * 2 * 16)
+            cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
+                       isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
+        }
       {  // mask words, one u64 per (entry, tile); self -> all ones, pad -> zero
         const int k = pt >> 1, q = pt & 1;
         const uint32_t y = __shfl_sync(kFull, rec.y, k & 31);
@@ -283,13 +328,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       cp_async_arrive(&raw_full[r]);
     }
+    prof_flush(0, 1);  // 0 wait raw_empty, 1 total
   } else if (warp >= kEpiWarps && warp < kEpiWarps + kStgWarps) {
     // ------------------------------------------------------------ staging
     const int st_tid = tid - kEpiWarps * 32;
     for (uint32_t c = 0; c < nchunks; ++c) {
       const int r = c % kRawStages, s = c % kCanStages;
-      mbar_wait(&raw_full[r], (c / kRawStages) & 1);
-      if (c >= uint32_t(kCanStages)) mbar_wait(&can_empty[s], ((c / kCanStages) - 1) & 1);
+      TC_WAIT(0, &raw_full[r], (c / kRawStages) & 1);
+      if (c >= uint32_t(kCanStages)) TC_WAIT(1, &can_empty[s], ((c / kCanStages) - 1) & 1);
+      tc_fence_after();  // the A stage in TMEM is rewritten after the MMAs that read it
       const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       const uint2* recs = reinterpret_cast<const uint2*>(rw);
       const float* Ps = reinterpret_cast<const float*>(rw + Cfg::RAW_P);
@@ -297,27 +344,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
       unsigned char* st = smem + s * Cfg::STAGE;
       const int cnt = int(min(uint32_t(kKC), e1 - (e0 + c * kKC)));  // multiple of 8
-      // A: coefficients m_m(e) isd_m(x), K-major, unit (coalition m, 4 entries)
-      for (int J = st_tid; J < kM * (cnt / 4); J += kStgWarps * 32) {
-        const int m = J & (kM - 1), u = J >> 7, q = m >> 6, i = m & 63;
-        float c4[4];
+      // A: coefficients m_m(e) isd_m(x) into TMEM (lane = coalition m, column
+      // = entry k), hi/lo split. Warp sw covers lane quarter sw % 4 and
+      // entries [16 (sw / 4), +16).
+      {
+        const int sw = warp - kEpiWarps, q = sw & 3, k0 = (sw >> 2) * 16;
+        if (k0 < cnt) {
+          const int m = q * 32 + lane, tq = m >> 6, i = m & 63;
+          uint32_t hv[16], lv[16];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int k = 4 * u + w;
-          c4[w] = ((ws[k * 2 + q] >> i) & 1ull) ? isds[k * kM + m] : 0.f;
+          for (int w = 0; w < 16; ++w) {
+            const int k = k0 + w;
+            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? isds[k * kM + m] : 0.f;
+            const float h = tf32_hi(cf);
+            hv[w] = __float_as_uint(h);
+            lv[w] = __float_as_uint(cf - h);
+          }
+          const uint32_t ta = tmem + (uint32_t(q * 32) << 16) + Cfg::A_COL + s * 2 * kKC + k0;
+          TC_ST16(ta, hv);
+          TC_ST16(ta + kKC, lv);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-        float4 hi, lo;
-        hi.x = tf32_hi(c4[0]);
-        hi.y = tf32_hi(c4[1]);
-        hi.z = tf32_hi(c4[2]);
-        hi.w = tf32_hi(c4[3]);
-        lo = make_float4(c4[0] - hi.x, c4[1] - hi.y, c4[2] - hi.z, c4[3] - hi.w);
-        const uint32_t off = u * 2048 + (m >> 3) * 128 + (m & 7) * 16;
-        *reinterpret_cast<float4*>(st + off) = hi;
-        *reinterpret_cast<float4*>(st + Cfg::OFF_ALO + off) = lo;
       }
       // B: gathered P rows transposed to K-major, unit (feature n, 4 entries), hi/lo split
-      for (int J = st_tid; J < D * (cnt / 4); J += kStgWarps * 32) {
+      for (int J = st_tid; J < ((PROF && (exp & 4)) ? 0 : D * (cnt / 4)); J += kStgWarps * 32) {
         const int n = J % D, u = J / D;
         const float p0 = Ps[(4 * u) * D + n], p1 = Ps[(4 * u + 1) * D + n];
         const float p2 = Ps[(4 * u + 2) * D + n], p3 = Ps[(4 * u + 3) * D + n];
@@ -332,12 +382,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<float4*>(st + Cfg::OFF_BLO + off) = lo;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&raw_empty[r]);
         mbar_arrive(&can_full[s]);
       }
     }
+    prof_flush(2, 2);  // 2 wait raw_full, 3 wait can_empty, 4 total
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     uint8_t* sfl = smem + Cfg::OFF_KFL;
@@ -350,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t sg = 0, b = 0, acc = 0;
       for (uint32_t c = 0; c < nchunks; ++c) {
         const int s = c % kCanStages;
-        mbar_wait(&can_full[s], (c / kCanStages) & 1);
+        TC_WAIT(0, &can_full[s], (c / kCanStages) & 1);
         tc_fence_after();
         const uint32_t base = e0 + c * kKC;
         const int nk = int(min(uint32_t(kKC), e1 - base)) / 8;
@@ -360,19 +412,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (f & 1u) {
             b = sg & 1u;
             if (sg >= 2) {
-              mbar_wait(&hfree[b], ((sg >> 1) - 1) & 1);
+              TC_WAIT(1, &hfree[b], ((sg >> 1) - 1) & 1);
               tc_fence_after();
             }
             acc = 0;
           }
           const uint32_t d = tmem + b * D;
-          const uint64_t ahi = smem_desc(sa + j * 4096, 2048, 128);
-          const uint64_t alo = smem_desc(sa + Cfg::OFF_ALO + j * 4096, 2048, 128);
+          const uint32_t ahi = tmem + Cfg::A_COL + s * 2 * kKC + j * 8, alo = ahi + kKC;
           const uint64_t bhi = smem_desc(sa + Cfg::OFF_BHI + j * 2 * Cfg::B_LBO, Cfg::B_LBO, 128);
           const uint64_t blo = smem_desc(sa + Cfg::OFF_BLO + j * 2 * Cfg::B_LBO, Cfg::B_LBO, 128);
-          tc_mma(d, ahi, bhi, idesc, acc);
-          tc_mma(d, ahi, blo, idesc, 1);
-          tc_mma(d, alo, bhi, idesc, 1);
+          tc_mma_ts(d, ahi, bhi, idesc, acc);
+          tc_mma_ts(d, ahi, blo, idesc, 1);
+          tc_mma_ts(d, alo, bhi, idesc, 1);
           acc = 1;
           if (f & 2u) {
             tc_commit(&hfull[b]);
@@ -381,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_commit(&can_empty[s]);
       }
+      prof_flush(6, 2);  // 6 wait can_full, 7 wait hfree, 8 total
     }
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
@@ -418,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sv_next = 0.f, dv_next = 0.f;
       if (s0 + sg + 1 < s1) factors(s0 + sg + 1, sv_next, dv_next);  // in flight during the wait
       const uint32_t b = sg & 1u;
-      mbar_wait(&hfull[b], (sg >> 1) & 1);
+      TC_WAIT(0, &hfull[b], (sg >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int cc = 0; cc < NCH; ++cc) {
@@ -462,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sv = sv_next;
       dv = dv_next;
     }
+    prof_flush(9, 1);  // 9 wait hfull, 10 total before the write-out
     // write the accumulator: Apart[tile][item][i][hb ..]
     float* out = Apart + ((tile * items + item) * kTile + i) * uint64_t(D) + hb;
 #pragma unroll 1
@@ -476,29 +529,79 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __uint_as_float(a[4 * j4 + 2]), __uint_as_float(a[4 * j4 + 3]));
     }
   }
+  if constexpr (PROF) {  // 11 epilogue incl. write-out, 12 CTAs, 13 kernel
+    if (warp < kEpiWarps && lane == 0) atomicAdd(&prof[11], (unsigned long long)(clock64() - t_begin));
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PROF) {
+    if (tid == 0) {
+      atomicAdd(&prof[12], 1ull);
+      atomicAdd(&prof[13], (unsigned long long)(clock64() - t_begin));
+    }
+  }
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::TMEM_COLS));
   }
 }
 
-template <int D>
-void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
-               uint64_t ntp, float* apart) {
+// SF_TC_EXP (PROF only, results invalid): bit 0 skips the isd-row gathers,
+// bit 1 the P-row gathers, bit 2 the B transposition
+int exp_flags() {
+  static const int f = std::getenv("SF_TC_EXP") ? std::atoi(std::getenv("SF_TC_EXP")) : 0;
+  return f;
+}
+
+template <int D, bool PROF>
+void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
+                    uint64_t ntp, float* apart, unsigned long long* prof) {
   using Cfg = TcCfg<D>;
   static bool configured = false;
   if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    SF_CUDA(cudaFuncSetAttribute(fused_tc_kernel<D, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM));
     configured = true;
   }
   dim3 grid(e.tc_items, unsigned(ntp / 2));
-  fused_tc_kernel<D><<<grid, kThreads, Cfg::SMEM, ctx.stream>>>(
+  fused_tc_kernel<D, PROF><<<grid, kThreads, Cfg::SMEM, ctx.stream>>>(
       maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
-      e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart);
+      e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof,
+      PROF ? exp_flags() : 0);
   SF_LAUNCHED(ctx);
+}
+
+// SF_TC_PROF=1: run the PROF instantiation and print the per-role wait
+// breakdown (cycles per warp per CTA) every 100 launches to stderr.
+template <int D>
+void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
+               uint64_t ntp, float* apart) {
+  static const bool prof_on = std::getenv("SF_TC_PROF") != nullptr;
+  if (!prof_on) {
+    launch_tc_impl<D, false>(ctx, e, maskt, Wp, isd, ntp, apart, nullptr);
+    return;
+  }
+  static unsigned long long* dprof = nullptr;
+  static uint64_t nlaunch = 0;
+  if (!dprof) {
+    SF_CUDA(cudaMalloc(&dprof, kProfSites * sizeof(unsigned long long)));
+    SF_CUDA(cudaMemset(dprof, 0, kProfSites * sizeof(unsigned long long)));
+  }
+  launch_tc_impl<D, true>(ctx, e, maskt, Wp, isd, ntp, apart, dprof);
+  if (++nlaunch % 100 == 0) {
+    unsigned long long h[kProfSites];
+    SF_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+    const double ctas = double(h[12] ? h[12] : 1);
+    auto per = [&](int k, int warps) { return double(h[k]) / ctas / warps; };
+    std::fprintf(stderr,
+                 "[tc prof] launches %llu CTAs %llu kernel %.0f cyc/CTA | producer wait raw_empty %.0f total %.0f | "
+                 "staging wait raw_full %.0f can_empty %.0f total %.0f | mma wait can_full %.0f hfree %.0f total %.0f | "
+                 "epilogue wait hfull %.0f loop %.0f with write %.0f\n",
+                 (unsigned long long)nlaunch, h[12], double(h[13]) / ctas, per(0, kProdWarps), per(1, kProdWarps),
+                 per(2, kStgWarps), per(3, kStgWarps), per(4, kStgWarps), per(6, 1), per(7, 1), per(8, 1),
+                 per(9, kEpiWarps), per(10, kEpiWarps), per(11, kEpiWarps));
+  }
 }
 
 }  // namespace

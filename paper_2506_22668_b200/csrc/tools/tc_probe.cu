@@ -38,14 +38,15 @@ __global__ void probe(const float* A, const float* B, float* D, int mode) {
   }
   for (int idx = tid; idx < K * N; idx += blockDim.x) {
     const int k = idx / N, n = idx % N;
+    const float bv = mode >= 6 ? (n == k ? 1.f : 0.f) : B[k * N + n];
     uint32_t off;
-    if (mode >= 3)  // MN-major SWIZZLE_128B: atom (32 n x 8 k) = 1024 B, [n/32][k/8][atom]
+    if (mode == 3 || mode == 4)  // MN-major SWIZZLE_128B: atom (32 n x 8 k) = 1024 B, [n/32][k/8][atom]
       off = (n / 32) * (K / 8 * 1024) + (k / 8) * 1024 + (k % 8) * 128 + ((((n % 32) / 4) ^ (k % 8)) * 16) + (n % 4) * 4;
     else if (mode == 2)  // K-major B (N x K): (k/4)*(N/8*128) + (n/8)*128 + (n%8)*16 + (k%4)*4
       off = (k / 4) * (N / 8 * 128) + (n / 8) * 128 + (n % 8) * 16 + (k % 4) * 4;
     else            // MN-major: (n/4)*B_SBO + (k/8)*128 + (k%8)*16 + (n%4)*4
       off = (n / 4) * B_SBO + (k / 8) * 128 + (k % 8) * 16 + (n % 4) * 4;
-    *reinterpret_cast<float*>(sb + off) = B[k * N + n];
+    *reinterpret_cast<float*>(sb + off) = bv;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid == 0) {
@@ -53,14 +54,39 @@ __global__ void probe(const float* A, const float* B, float* D, int mode) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot;
-  if (tid == 0) {
+  if (mode >= 5 && warp < 4) {  // A -> TMEM columns 256.. (lane m = row, column k)
+    const uint32_t lb = uint32_t(warp * 32) << 16;
+    for (int k = 0; k < K; ++k) {
+      const float f = mode == 6 ? float(warp * 32 + lane + 1) : mode == 7 ? float(k + 1) : A[(warp * 32 + lane) * K + k];
+      const uint32_t v = __float_as_uint(f);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lb + 256 + k), "r"(v) : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0 && mode >= 5) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+    for (int j = 0; j < K / 8; ++j) {
+      const uint64_t bd = smem_desc(su32(sb) + j * 2 * (N / 8 * 128), N / 8 * 128, 128);
+      const uint32_t acc = j > 0;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+          "r"(tmem + 256 + j * 8), "l"(bd), "r"(idesc), "r"(acc)
+          : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar))
+                 : "memory");
+  } else if (tid == 0) {
     const uint32_t b_major = mode == 2 ? 0u : 1u;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (b_major << 16) | (uint32_t(N >> 3) << 17) |
                            (uint32_t(M >> 4) << 24);
@@ -101,7 +127,7 @@ __global__ void probe(const float* A, const float* B, float* D, int mode) {
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -120,7 +146,7 @@ int main() {
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   const int smem = M * K * 4 + (N / 4) * B_SBO + 4096;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 5; ++mode) {
+  for (int mode = 5; mode < 8; ++mode) {
     cudaMemset(dD, 0, D.size() * 4);
     probe<<<1, 128, smem>>>(dA, dB, dD, mode);
     cudaError_t e = cudaDeviceSynchronize();
@@ -130,8 +156,17 @@ int main() {
       err = std::max(err, double(std::fabs(D[i] - R[i])));
       mx = std::max(mx, double(std::fabs(R[i])));
     }
+    if (mode >= 6) {
+      printf("mode %d (%s): D[m][k] for m in {0,1,2,31,32,64,127}, k = 0..31\n", mode, mode == 6 ? "TMEM lane+1" : "TMEM column+1");
+      for (int m : {0, 1, 2, 31, 32, 64, 127}) {
+        printf("  m=%3d:", m);
+        for (int k = 0; k < K; ++k) printf(" %g", D[m * N + k]);
+        printf("\n");
+      }
+      continue;
+    }
     printf("mode %d (%s B): status=%s max_abs_err=%.3g max_ref=%.3g D[0]=%g R[0]=%g D[1]=%g R[1]=%g D[N]=%g R[N]=%g\n",
-           mode, mode == 4 ? "MN-major SW128 swapped" : mode == 3 ? "MN-major SW128" : mode == 2 ? "K-major" : (mode ? "MN-major swapped lbo/sbo" : "MN-major"), cudaGetErrorString(e), err, mx, D[0], R[0], D[1], R[1], D[N], R[N]);
+           mode, mode == 5 ? "A in TMEM, K-major" : mode == 4 ? "MN-major SW128 swapped" : mode == 3 ? "MN-major SW128" : mode == 2 ? "K-major" : (mode ? "MN-major swapped lbo/sbo" : "MN-major"), cudaGetErrorString(e), err, mx, D[0], R[0], D[1], R[1], D[N], R[N]);
   }
   return 0;
 }
