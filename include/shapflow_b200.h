@@ -259,6 +259,9 @@ typedef struct sf_explanation {
   double* fid_minus;
   double* fid_minus_random;
   double sampling_ms, prediction_ms, solve_ms, total_ms;
+  /* host-side stage timings: subgraph extraction, full/empty scores (engine
+   * preparation included), Fidelity+ evaluation */
+  double extract_ms, setup_ms, fidelity_ms;
   char warning[512];
 } sf_explanation;
 

@@ -303,7 +303,8 @@ class _ExplanationC(C.Structure):
         ("num_sparsities", C.c_uint32), ("fid_sparsities", C.POINTER(C.c_double)),
         ("fid_minus", C.POINTER(C.c_double)), ("fid_minus_random", C.POINTER(C.c_double)),
         ("sampling_ms", C.c_double), ("prediction_ms", C.c_double), ("solve_ms", C.c_double),
-        ("total_ms", C.c_double), ("warning", C.c_char * 512),
+        ("total_ms", C.c_double), ("extract_ms", C.c_double), ("setup_ms", C.c_double),
+        ("fidelity_ms", C.c_double), ("warning", C.c_char * 512),
     ]
 
 
@@ -536,7 +537,8 @@ class Context:
                 full_score=e.full_score, players=_arr(e.players_global, 2 * n, np.uint32).reshape(-1, 2), phi=phi,
                 exhaustive=bool(e.exhaustive), rows=e.rows, iterations=e.iterations, residual=e.residual,
                 converged=bool(e.converged), top=top, fidelity=fid,
-                timings=dict(sampling_ms=e.sampling_ms, prediction_ms=e.prediction_ms, solve_ms=e.solve_ms,
+                timings=dict(extract_ms=e.extract_ms, setup_ms=e.setup_ms, sampling_ms=e.sampling_ms,
+                             prediction_ms=e.prediction_ms, solve_ms=e.solve_ms, fidelity_ms=e.fidelity_ms,
                              total_ms=e.total_ms),
                 warning=e.warning.decode())
         finally:

@@ -6,7 +6,8 @@
 // weight constraint_weight and target constraint_target. M stays bit-packed
 // in HBM in two layouts:
 //   rows   row-major u64 words (the sampler's output) -> M u  (forward)
-//   maskt  64-row tiles, u64 per player, bit i = row t*64+i -> M^T r
+//   mte    tiles of 64 pairs over the even rows (odd rows of non-complement
+//          pairs in a second layout), u64 per player, bit i = pair t*64+i -> M^T r
 // Complement pairs (row 2j+1 = ~row 2j) take the reference's shortcut
 // (solver.cpp:188-198, 209-223, 261-263): the odd dot is sum(u) - dot and
 // the odd row contributes a constant plus a difference on the even row, so
@@ -28,7 +29,6 @@ namespace {
 
 constexpr int kRedBlocks = 256;
 constexpr int kRedThreads = 256;
-constexpr uint32_t kChunk = 8192;  // players per forward chunk (64 KB of u in smem)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -113,33 +113,47 @@ __global__ void init_r_kernel(const double* __restrict__ sw,
 }
 
 // ---------------------------------------------------------------- M u
-// One CTA per block of rows (whole complement pairs; block boundaries
-// balance the set-bit count, rows are ordered by coalition size). The player
-// axis is walked in chunks of kChunk; each chunk of u is staged in shared
-// memory once per CTA and every row of the block adds the u values of its
-// set bits in that chunk (warp per row, set-bit iteration), so each mask
-// word is read exactly once. Rows whose dot is not needed (odd rows of
-// complement pairs) are skipped. The epilogue applies the complement
-// shortcut (solver.cpp:261-263), writes v, and leaves the block's partial
-// sum of v^2 for a fixed-order reduction.
-constexpr uint32_t kFwdRows = 1024;
+// acc += su[base + b] over the set bits b of a 32-bit half word (FLO from
+// the top: one instruction per bit instead of a 64-bit find-first-set)
+__device__ __forceinline__ void add_bits(uint32_t x, const double* __restrict__ su, int base,
+                                         double& acc) {
+  while (x) {
+    const int b = 31 - __clz(x);
+    x ^= 1u << b;
+    acc += su[base + b];
+  }
+}
 
-__global__ void __launch_bounds__(256)
+// One CTA (32 warps) per block of rows (whole complement pairs; block
+// boundaries balance the set-bit count, rows are ordered by coalition size).
+// The player axis is walked in word-aligned chunks of up to kFwdChunk
+// doubles of u staged in shared memory (one chunk when n <= kFwdChunk);
+// every needed row of the block adds the u values of its set bits in the
+// chunk (warp per row, dynamic fetch, largest coalitions first), so each
+// mask word is read exactly once. Odd rows of complement pairs are skipped:
+// the epilogue applies the complement shortcut (solver.cpp:261-263), writes
+// v and leaves the block's partial sum of v^2 for a fixed-order reduction.
+constexpr uint32_t kFwdRows = 1024;
+constexpr int kFwdThreads = 1024;
+constexpr uint32_t kFwdChunk = 24576;  // doubles (192 KB), a multiple of 64
+constexpr int kFwdWordsPerLane = kFwdChunk / 64 / 32;  // 12
+
+__global__ void __launch_bounds__(kFwdThreads)
     forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, const uint32_t* __restrict__ row_start,
                    const uint8_t* __restrict__ is_comp, const double* __restrict__ u,
                    uint32_t n, const double* __restrict__ sw,
                    const double* __restrict__ sum_u, double* __restrict__ v,
                    double* __restrict__ dsq_part) {
-  extern __shared__ double su[];  // kChunk doubles
+  extern __shared__ double su[];  // min(n, kFwdChunk) doubles
   __shared__ double rowsum[kFwdRows];
-  __shared__ double red[8];
+  __shared__ double red[kFwdThreads / 32];
   __shared__ unsigned next_row;
   const uint64_t r0 = row_start[blockIdx.x];
   const uint32_t nr = row_start[blockIdx.x + 1] - uint32_t(r0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) rowsum[i] = 0.0;
-  for (uint32_t e0 = 0; e0 < n; e0 += kChunk) {
-    const uint32_t ce = min(n - e0, kChunk);
+  for (uint32_t e0 = 0; e0 < n; e0 += kFwdChunk) {
+    const uint32_t ce = min(n - e0, kFwdChunk);
     __syncthreads();  // the previous chunk's lookups are done
     if (threadIdx.x == 0) next_row = 0;
 #pragma unroll 4
@@ -147,7 +161,6 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const uint32_t w0 = e0 / 64, w1 = min(W, (e0 + ce + 63) / 64);
     for (;;) {
-      // dynamic row fetch, largest coalitions (end of the block) first
       unsigned f = 0;
       if (lane == 0) f = atomicAdd(&next_row, 1u);
       f = __shfl_sync(kFull, f, 0);
@@ -156,17 +169,21 @@ __global__ void __launch_bounds__(256)
       const uint64_t row = r0 + rl;
       if ((row & 1) && is_comp[row >> 1]) continue;
       const uint64_t* rp = rows + row * W;
-      double acc = 0.0;
-      for (uint32_t w = w0 + lane; w < w1; w += 32) {
-        uint64_t x = rp[w];
-        const uint32_t base = w * 64 - e0;
-        while (x) {
-          const int b = __ffsll(static_cast<long long>(x)) - 1;
-          x &= x - 1;
-          acc += su[base + b];
-        }
+      double acc0 = 0.0, acc1 = 0.0;
+      // all of this lane's words of the chunk are loaded before any is used
+      uint64_t xs[kFwdWordsPerLane];
+#pragma unroll
+      for (int q = 0; q < kFwdWordsPerLane; ++q) {
+        const uint32_t w = w0 + lane + 32 * q;
+        xs[q] = w < w1 ? __ldcs(rp + w) : 0ull;
       }
-      acc = warp_sum(acc);
+#pragma unroll
+      for (int q = 0; q < kFwdWordsPerLane; ++q) {
+        const int base = int((w0 + lane + 32 * q) * 64 - e0);
+        add_bits(uint32_t(xs[q]), su, base, acc0);
+        add_bits(uint32_t(xs[q] >> 32), su, base + 32, acc1);
+      }
+      double acc = warp_sum(acc0 + acc1);
       if (lane == 0) rowsum[rl] += acc;
     }
   }
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < 8; ++i) t += red[i];
+    for (int i = 0; i < kFwdThreads / 32; ++i) t += red[i];
     dsq_part[blockIdx.x] = t;
   }
 }
@@ -213,86 +230,71 @@ __global__ void direction_kernel(double* __restrict__ u, const double* __restric
 }
 
 // ---------------------------------------------------------------- M^T r
-// coefficients per row: c = sw * r; complement pairs fold into a constant
-// co (every player) plus (ce - co) on the even row (solver.cpp:209-217).
+// Pair coefficients (solver.cpp:209-217): a complement pair contributes
+// c_o to every player (kconst) plus (c_e - c_o) on the even row's bits; a
+// non-complement pair contributes c_e on the even row and c_o on the odd
+// row (second tile layout). Entries past `pairs` are zero.
 __global__ void coef_kernel(const double* __restrict__ sw, const double* __restrict__ r,
-                            const uint8_t* __restrict__ is_comp, uint64_t nrows,
-                            double* __restrict__ coef, double* __restrict__ kconst,
-                            uint64_t* __restrict__ nzmask) {
-  const uint64_t row = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  double cf = 0.0, kc = 0.0;
-  if (row < nrows) {
-    const uint64_t j = row >> 1;
-    const double c = sw[row] * r[row];
+                            const uint8_t* __restrict__ is_comp, uint64_t pairs, uint64_t padded,
+                            double* __restrict__ coef_e, double* __restrict__ coef_o,
+                            double* __restrict__ kconst) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (j >= padded) return;
+  double ce = 0.0, co = 0.0, kc = 0.0;
+  if (j < pairs) {
+    const double e = sw[2 * j] * r[2 * j], o = sw[2 * j + 1] * r[2 * j + 1];
     if (is_comp[j]) {
-      if (row & 1) {
-        cf = 0.0;
-        kc = c;
-      } else {
-        cf = c - sw[row + 1] * r[row + 1];
-      }
+      ce = e - o;
+      kc = o;
     } else {
-      cf = c;
+      ce = e;
+      co = o;
     }
-    coef[row] = cf;
-    if (row & 1) kconst[j] = kc;
+    kconst[j] = kc;
   }
-  // tile mask of rows with a nonzero coefficient (64 rows = 2 warps)
-  const unsigned b = __ballot_sync(kFull, cf != 0.0);
-  const uint64_t tile = row >> 6;
-  uint32_t* nz32 = reinterpret_cast<uint32_t*>(nzmask);
-  if ((threadIdx.x & 31) == 0)
-    nz32[tile * 2 + ((row >> 5) & 1)] = b;
+  coef_e[j] = ce;
+  coef_o[j] = co;
 }
 
-// s_part[split][e] = sum over the split's tiles, over set bits i of
-// (maskt[t][e] & nz[t]), of coef[t*64+i]. Each thread owns two players;
-// kTT tiles are processed per step: their coefficients are staged in shared
-// memory while all 2*kTT mask words are already in flight.
+// s_part[split][e] (+)= sum over the split's pair tiles, over set bits i of
+// mt[t][e], of coef[t*64+i]. Each thread owns two players; kTT tiles per
+// step: their coefficients are staged in shared memory while all 2*kTT
+// mask words are in flight.
 constexpr int kTT = 8;
 
 __global__ void __launch_bounds__(256)
-    transpose_partial_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
+    transpose_partial_kernel(const uint64_t* __restrict__ mt, uint64_t Wp,
                              uint32_t n, const uint32_t* __restrict__ split_start,
-                             const double* __restrict__ coef,
-                             const uint64_t* __restrict__ nzmask,
+                             const double* __restrict__ coef, int accumulate,
                              double* __restrict__ s_part) {
   __shared__ double sc[kTT][64];
-  __shared__ uint64_t snz[kTT];
   const uint32_t ea = blockIdx.x * 512 + threadIdx.x, eb = ea + 256;
   const uint64_t t0 = split_start[blockIdx.y], t1 = split_start[blockIdx.y + 1];
-  double acc_a = 0.0, acc_b = 0.0;
+  double acc_a = 0.0, acc_b = 0.0, acc_a2 = 0.0, acc_b2 = 0.0;
   for (uint64_t tb = t0; tb < t1; tb += kTT) {
     const int nt = (t1 - tb) < uint64_t(kTT) ? int(t1 - tb) : kTT;
     uint64_t wa[kTT], wb[kTT];
 #pragma unroll
     for (int q = 0; q < kTT; ++q) {
-      wa[q] = (q < nt && ea < n) ? maskt[(tb + q) * Wp + ea] : 0ull;
-      wb[q] = (q < nt && eb < n) ? maskt[(tb + q) * Wp + eb] : 0ull;
+      wa[q] = (q < nt && ea < n) ? mt[(tb + q) * Wp + ea] : 0ull;
+      wb[q] = (q < nt && eb < n) ? mt[(tb + q) * Wp + eb] : 0ull;
     }
     __syncthreads();  // the previous step's coefficients are consumed
     for (int idx = threadIdx.x; idx < nt * 64; idx += blockDim.x) sc[idx >> 6][idx & 63] = coef[tb * 64 + idx];
-    if (threadIdx.x < nt) snz[threadIdx.x] = nzmask[tb + threadIdx.x];
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kTT; ++q) {
-      const uint64_t nz = q < nt ? snz[q] : 0ull;
-      uint64_t x = wa[q] & nz;
-      while (x) {
-        const int b = __ffsll(static_cast<long long>(x)) - 1;
-        x &= x - 1;
-        acc_a += sc[q][b];
-      }
-      x = wb[q] & nz;
-      while (x) {
-        const int b = __ffsll(static_cast<long long>(x)) - 1;
-        x &= x - 1;
-        acc_b += sc[q][b];
-      }
+      add_bits(uint32_t(wa[q]), sc[q], 0, acc_a);
+      add_bits(uint32_t(wa[q] >> 32), sc[q], 32, acc_a2);
+      add_bits(uint32_t(wb[q]), sc[q], 0, acc_b);
+      add_bits(uint32_t(wb[q] >> 32), sc[q], 32, acc_b2);
     }
   }
-  if (ea < n) s_part[uint64_t(blockIdx.y) * n + ea] = acc_a;
-  if (eb < n) s_part[uint64_t(blockIdx.y) * n + eb] = acc_b;
+  acc_a += acc_a2;
+  acc_b += acc_b2;
+  double* pa = s_part + uint64_t(blockIdx.y) * n;
+  if (ea < n) pa[ea] = (accumulate ? pa[ea] : 0.0) + acc_a;
+  if (eb < n) pa[eb] = (accumulate ? pa[eb] : 0.0) + acc_b;
 }
 
 // s_e = K + sum_split s_part[split][e]
@@ -423,25 +425,25 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   if (in.rows % 2) throw DataError("local rows must come in adjacent pairs");
   const uint64_t rows = in.rows, pairs = rows / 2;
   const uint32_t W = in.W;
-  const uint64_t tiles = (rows + 63) / 64;
+  const uint64_t ptiles = (pairs + 63) / 64;  // tiles of 64 pairs (even / odd row layouts)
   const uint64_t Wp = uint64_t(W) * 64;
   int sms = 148;
   SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
   const uint64_t pblocks = (n + 511) / 512;  // transpose: 512 players per CTA
   const uint64_t max_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
   const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2;
-  const uint64_t bytes = tiles * Wp * 8 + pairs + rows * 8 * 3 + fblocks_max * 8 + rows * 4 +
-                         (fblocks_max + max_splits + 2) * 4 + tiles * 64 * 8 + tiles * 8 + pairs * 8 * 2 +
-                         max_splits * n * 8 +
-                         uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
+  const uint64_t bytes = 2 * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
+                         (fblocks_max + max_splits + 2) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
+                         max_splits * n * 8 + uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
   ctx.solver_work.reserve(bytes);
   Scratch sc{ctx.solver_work.p, 0};
-  uint64_t* maskt = sc.take<uint64_t>(tiles * Wp);
+  uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
+  uint64_t* mto = sc.take<uint64_t>(ptiles * Wp);  // odd rows (non-complement pairs only)
   uint8_t* is_comp = sc.take<uint8_t>(pairs);
   double* r = sc.take<double>(rows);
   double* v = sc.take<double>(rows);
-  double* coef = sc.take<double>(tiles * 64);
-  uint64_t* nz = sc.take<uint64_t>(tiles);
+  double* coef_e = sc.take<double>(ptiles * 64);
+  double* coef_o = sc.take<double>(ptiles * 64);
   double* dsq = sc.take<double>(fblocks_max);
   uint32_t* pop = sc.take<uint32_t>(rows);
   uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + 2);
@@ -475,7 +477,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     ~HostFree() { cudaFreeHost(p); }
   } host_guard{host};
 
-  launch_transpose_tiles(ctx, in.dev_rows, rows, W, tiles, maskt);
+  launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, 2ull * W);
   if (pairs) {
     comp_flags_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, is_comp);
     SF_LAUNCHED(ctx);
@@ -496,6 +498,9 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     ctx.d2h_bytes += rows * 4 + pairs;
   }
   auto needed = [&](uint64_t row) { return !((row & 1) && h_comp[row >> 1]); };
+  bool any_noncomp = false;
+  for (uint64_t j = 0; j < pairs; ++j) any_noncomp |= !h_comp[j];
+  if (any_noncomp) launch_transpose_tiles(ctx, in.dev_rows + W, pairs, W, ptiles, mto, 2ull * W);
   std::vector<uint32_t> bounds{0};
   {
     const uint64_t wcost = (W + 31) / 32 * 4 + 16;  // word loads + row overhead per needed row
@@ -516,21 +521,21 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t fblocks = bounds.size() - 1;
   std::vector<uint32_t> sbounds{0};
   {
-    std::vector<uint64_t> tcost(tiles, n / 8 + 64);
+    std::vector<uint64_t> tcost(ptiles, (any_noncomp ? 2 : 1) * (n / 8 + 64));
     for (uint64_t i = 0; i < rows; ++i)
-      if (needed(i)) tcost[i / 64] += h_pop[i];
+      if (needed(i)) tcost[i / 128] += h_pop[i];
     uint64_t total = 0;
     for (uint64_t c : tcost) total += c;
     const uint64_t target = std::max<uint64_t>(1, (total + max_splits - 1) / max_splits);
     uint64_t acc = 0;
-    for (uint64_t t = 0; t < tiles; ++t) {
+    for (uint64_t t = 0; t < ptiles; ++t) {
       acc += tcost[t];
       if (acc >= target && sbounds.size() < max_splits) {
         sbounds.push_back(uint32_t(t + 1));
         acc = 0;
       }
     }
-    if (sbounds.back() != tiles) sbounds.push_back(uint32_t(tiles));
+    if (sbounds.back() != ptiles) sbounds.push_back(uint32_t(ptiles));
   }
   const uint32_t splits = uint32_t(sbounds.size() - 1);
   const uint32_t* row_start = d_bounds;
@@ -546,16 +551,19 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
   auto transpose_product = [&]() {
     SF_CUDA(cudaMemsetAsync(kc, 0, pairs * 8 + 8, st));
-    if (rows) {
-      coef_kernel<<<blocks_for(tiles * 64, 64), 64, 0, st>>>(in.dev_sw, r, is_comp, rows, coef,
-                                                              kc, nz);
+    if (pairs) {
+      coef_kernel<<<blocks_for(ptiles * 64), 256, 0, st>>>(in.dev_sw, r, is_comp, pairs, ptiles * 64,
+                                                          coef_e, coef_o, kc);
       SF_LAUNCHED(ctx);
     }
     reduce(kc, pairs, 0, 0.0, scal + 4);
     dim3 grid(unsigned(pblocks), splits);
-    transpose_partial_kernel<<<grid, 256, 0, st>>>(maskt, Wp, n, split_start, coef,
-                                                   nz, s_part);
+    transpose_partial_kernel<<<grid, 256, 0, st>>>(mte, Wp, n, split_start, coef_e, 0, s_part);
     SF_LAUNCHED(ctx);
+    if (any_noncomp) {
+      transpose_partial_kernel<<<grid, 256, 0, st>>>(mto, Wp, n, split_start, coef_o, 1, s_part);
+      SF_LAUNCHED(ctx);
+    }
     transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits, n, scal + 4, s);
     SF_LAUNCHED(ctx);
     comm_allreduce_sum(ctx, s, n);
@@ -566,11 +574,11 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   auto forward_product = [&](double& delta, double& v_c) {
     reduce(u, n, 0, 0.0, scal + 0);  // sum_u
     if (rows) {
-      const size_t smem = size_t(std::min<uint32_t>(n, kChunk)) * 8;
+      const size_t smem = size_t(std::min<uint32_t>(n, kFwdChunk)) * 8;
       SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kChunk * 8)));
-      forward_kernel<<<unsigned(fblocks), 256, smem, st>>>(in.dev_rows, W, row_start, is_comp, u, n,
-                                                           in.dev_sw, scal + 0, v, dsq);
+                                   int(kFwdChunk * 8)));
+      forward_kernel<<<unsigned(fblocks), kFwdThreads, smem, st>>>(in.dev_rows, W, row_start, is_comp, u,
+                                                                   n, in.dev_sw, scal + 0, v, dsq);
       SF_LAUNCHED(ctx);
     }
     reduce(dsq, fblocks, 0, 0.0, scal + 1);

@@ -1030,6 +1030,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   if (m.layers.front().in != sg.feature_dim)
     throw DataError("model input dim " + std::to_string(m.layers.front().in) +
                     " does not match feature dim " + std::to_string(sg.feature_dim));
+  DebugTimer dt("engine_prepare");
   e.sg_id = 0;
   e.V = sg.num_nodes();
   e.n = sg.num_players();
@@ -1043,6 +1044,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   e.row_ptr.upload(rp.data(), rp.size(), ctx.stream);
   e.col.upload(sg.col.data(), sg.col.size(), ctx.stream);
   e.edge_player.upload(sg.edge_player.data(), sg.edge_player.size(), ctx.stream);
+  dt.lap("csr upload");
   {  // isd_kernel: nodes by descending degree, 1/sqrt(deg) table
     std::vector<uint32_t> order(e.V);
     uint32_t maxdeg = 0;
@@ -1076,8 +1078,10 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   ctx.h2d_bytes += (rp.size() + sg.col.size() + sg.edge_player.size()) * 4 + sg.features.size() * 4;
   for (const Layer& l : m.layers) ctx.h2d_bytes += (l.weight.size() + l.bias.size()) * 4;
   SF_CUDA(cudaStreamSynchronize(ctx.stream));  // temporaries x, w0 die here
+  dt.lap("p0 gemm + weights");
   e.fused = e.L >= 2 && fused_width(e.dims[1]) && e.n > 0;
   if (e.fused) build_fused_plan(ctx, e, sg);
+  dt.lap("fused plan");
   // tcgen05 3xTF32 fused kernel by default; SF_FUSED_TC=0 selects the SIMT FP32 kernel
   static const bool use_tc = [] {
     const char* v = std::getenv("SF_FUSED_TC");
@@ -1086,6 +1090,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   const bool want_tc = ctx.fused_kind == 2 || (ctx.fused_kind == 0 && use_tc);
   e.tc = e.fused && want_tc && tc_width(e.dims[1]);
   if (e.tc) build_tc_plan(ctx, e, sg);
+  dt.lap("tc plan");
   e.sg_id = sg.id;
   e.model_id = m.id;
   e.kind = ctx.fused_kind;

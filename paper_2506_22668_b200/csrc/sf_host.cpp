@@ -542,7 +542,9 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
   if (m.layers.front().in != g.feature_dim)
     throw DataError("model expects " + std::to_string(m.layers.front().in) +
                     " input features but the graph has " + std::to_string(g.feature_dim));
+  DebugTimer("explain").lap("start");
   const Subgraph sg = extract(g, node, m.depth());
+  out->extract_ms = ms_since(t_start);
   const uint64_t n_raw = sg.num_players();
   if (o.player_cap != 0 && n_raw > o.player_cap) {
     out->skipped = 1;
@@ -559,6 +561,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
 
   // full-mask probabilities -> class (first argmax), empty-mask base score
   {
+    const auto t_setup = Clock::now();
     std::vector<uint64_t> two(2 * W, 0);
     for (uint32_t w = 0; w < W; ++w) two[w] = ~uint64_t{0};
     if (n % 64) two[W - 1] = (uint64_t{1} << (n % 64)) - 1;
@@ -567,9 +570,11 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     std::vector<float> probs(2 * C);
     predict_rows(ctx, sg, m, ctx.masks.p, 2, 0, nullptr, probs.data());
     const uint32_t cls = uint32_t(std::max_element(probs.begin(), probs.begin() + C) - probs.begin());
+    DebugTimer("explain").lap("full/empty scores done");
     out->predicted_class = cls;
     out->full_score = double(probs[cls]);
     out->base_score = double(probs[C + cls]);
+    out->setup_ms = ms_since(t_setup);
   }
   std::vector<uint32_t> players_global;
   players_global.reserve(2 * n);
@@ -636,6 +641,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     in.constraint_target = out->full_score - out->base_score;
     in.constraint_weight = o.constraint_scale;
     in.global_pair_count = plan.total_pairs();
+    DebugTimer("explain").lap("assemble done");
     CglsResult res = cgls_solve(ctx, in, o.tol, o.max_iter, o.solver_mode, false);
     comm_barrier(ctx);
     out->solve_ms = ms_since(t_stage);
@@ -651,8 +657,10 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
       std::snprintf(out->warning, sizeof(out->warning), "%s", msg.str().c_str());
     }
   }
+  DebugTimer tail("explain tail");
   out->phi = dup_array(phi);
   const std::vector<uint32_t> ranked = ranking(phi);
+  tail.lap("ranking");
   const size_t keep = std::min<size_t>(o.top_k, ranked.size());
   std::vector<uint32_t> tp(ranked.begin(), ranked.begin() + keep);
   std::vector<double> tv(keep);
@@ -661,6 +669,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
   out->top_player = dup_array(tp);
   out->top_phi = dup_array(tv);
   if (o.fidelity) {
+    const auto t_fid = Clock::now();
     std::vector<uint32_t> counts = o.top_counts ? std::vector<uint32_t>(o.top_counts, o.top_counts + o.num_top_counts)
                                                 : std::vector<uint32_t>{5, 10, 20};
     std::vector<double> sp = o.sparsities ? std::vector<double>(o.sparsities, o.sparsities + o.num_sparsities)
@@ -675,8 +684,10 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     out->fid_sparsities = dup_array(f.sparsities);
     out->fid_minus = dup_array(f.minus);
     out->fid_minus_random = dup_array(f.minus_random);
+    out->fidelity_ms = ms_since(t_fid);
   }
   out->total_ms = ms_since(t_start);
+  DebugTimer("explain").lap("end");
 }
 
 }  // namespace sfb

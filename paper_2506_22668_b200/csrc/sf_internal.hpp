@@ -12,6 +12,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <cstdlib>
+#include <chrono>
 
 namespace sfb {
 
@@ -173,6 +175,23 @@ struct Engine {
   DevBuf<uint8_t> tc_kflags;
 };
 
+// SF_TIMING=1: host-side stage timings to stderr (debug aid, off by default)
+struct DebugTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  const char* scope;
+  explicit DebugTimer(const char* sc) : on(std::getenv("SF_TIMING") != nullptr), t(std::chrono::steady_clock::now()), scope(sc) {}
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    static const auto epoch = now;
+    std::fprintf(stderr, "[timing] %10.3f %s %s %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(now - epoch).count(), scope, what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 struct CommStats {  // comm.hpp:13-19
   uint64_t scalar_allreduce = 0, vector_allreduce = 0, barriers = 0,
            doubles_reduced = 0;
@@ -258,7 +277,8 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
 // Row-major rows -> tile layout: maskt[t][e] bit i = row (row0+t*64+i)
 // bit e, for all 64 rows of the tile (u32 pairs: low = rows 0..31).
 void launch_transpose_tiles(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
-                            uint32_t W, uint64_t tiles, uint64_t* dev_maskt);
+                            uint32_t W, uint64_t tiles, uint64_t* dev_maskt,
+                            uint64_t stride = 0);  // words between rows (0: W)
 
 // sf_gcn.cu
 void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m);

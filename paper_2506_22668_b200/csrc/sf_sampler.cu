@@ -246,7 +246,7 @@ __device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t m, int
 
 __global__ void __launch_bounds__(256)
     transpose_tiles_kernel(const uint64_t* __restrict__ in, uint64_t rows,
-                           uint32_t W, uint64_t* __restrict__ out) {
+                           uint32_t W, uint64_t stride, uint64_t* __restrict__ out) {
   __shared__ uint64_t sm[64][33];
   const uint64_t t = blockIdx.y;
   const uint32_t w0 = blockIdx.x * 32;
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256)
   for (int i = tid; i < 64 * 32; i += 256) {
     const int r = i >> 5, w = i & 31;
     const uint64_t row = t * 64 + r;
-    sm[r][w] = (row < rows && w0 + w < W) ? in[row * W + w0 + w] : 0ull;
+    sm[r][w] = (row < rows && w0 + w < W) ? in[row * stride + w0 + w] : 0ull;
   }
   __syncthreads();
   const uint64_t Wp = uint64_t(W) * 64;  // players per tile, padded
@@ -363,10 +363,10 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
 }
 
 void launch_transpose_tiles(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
-                            uint32_t W, uint64_t tiles, uint64_t* dev_maskt) {
+                            uint32_t W, uint64_t tiles, uint64_t* dev_maskt, uint64_t stride) {
   if (tiles == 0) return;
   dim3 grid((W + 31) / 32, unsigned(tiles));
-  transpose_tiles_kernel<<<grid, 256, 0, ctx.stream>>>(dev_rows, rows, W, dev_maskt);
+  transpose_tiles_kernel<<<grid, 256, 0, ctx.stream>>>(dev_rows, rows, W, stride ? stride : W, dev_maskt);
   SF_LAUNCHED(ctx);
 }
 

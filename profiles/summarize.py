@@ -78,7 +78,7 @@ def report(path, regex=None):
                 if key.endswith("bytes.sum") or key.endswith("bytes_read.sum") or key.endswith("bytes_write.sum"):
                     f = f * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
                 if key == "gpu__time_duration.sum":
-                    f = f * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+                    f = f * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
                 x = f"{f:.2f}"
             except ValueError:
                 pass
