@@ -271,6 +271,20 @@ int sf_explain_node(sf_ctx* ctx, const sf_graph* g, const sf_model* m,
                     sf_explanation* out);
 int sf_explanation_free(sf_explanation* e);
 
+/* explain.hpp:54-57 explain_nodes: explain_node per node in order (each
+ * collective over the context's ranks); errors are prefixed "node N: "
+ * (explain.cpp:168-180) and every filled entry is freed on error. `out`
+ * holds `count` entries, each released with sf_explanation_free. */
+int sf_explain_nodes(sf_ctx* ctx, const sf_graph* g, const sf_model* m,
+                     const uint32_t* nodes, uint64_t count,
+                     const sf_explain_options* opts, sf_explanation* out);
+
+/* explain.hpp:59-64 select_nodes: "degree-range:[lo,hi]:count" (first
+ * `count` ids in ascending order with degree in [lo, hi]) or a comma
+ * separated id list. Writes up to `cap` ids, *count = number selected. */
+int sf_select_nodes(const sf_graph* g, const char* rule, uint32_t* out,
+                    uint64_t cap, uint64_t* count);
+
 /* fidelity.hpp:45-51 evaluate_fidelity on the device engine */
 int sf_evaluate_fidelity(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
                          uint32_t class_index, const double* phi,

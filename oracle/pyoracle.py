@@ -153,6 +153,13 @@ class Ref:
             raise OracleError(2, self.L.ref_last_error().decode())
         return C.c_void_p(h)
 
+    def select_nodes(self, g, rule):
+        cnt = C.c_uint64()
+        self._chk(self.L.ref_select_nodes(g, rule.encode(), None, C.c_uint64(0), C.byref(cnt)))
+        out = np.zeros(cnt.value, np.uint32)
+        self._chk(self.L.ref_select_nodes(g, rule.encode(), _p(out), C.c_uint64(len(out)), C.byref(cnt)))
+        return out
+
     def graph_save(self, g, path):
         self._chk(self.L.ref_graph_save(g, path.encode()))
 

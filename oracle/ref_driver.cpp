@@ -491,4 +491,13 @@ int ref_sample_predict(void* m, void* cg, uint32_t cls, uint64_t k,
   });
 }
 
+// explain.cpp:183-230 select_nodes
+int ref_select_nodes(void* g, const char* rule, uint32_t* out, uint64_t cap, uint64_t* count) {
+  return guard([&] {
+    const std::vector<uint32_t> sel = select_nodes(*static_cast<Graph*>(g), std::string(rule));
+    *count = sel.size();
+    for (uint64_t i = 0; i < sel.size() && i < cap; ++i) out[i] = sel[i];
+  });
+}
+
 }  // extern "C"

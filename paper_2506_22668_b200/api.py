@@ -182,6 +182,16 @@ class Graph:
         _chk(lib.sf_graph_csr(self.h, _p(rp), _p(col)))
         return rp, col
 
+    def select_nodes(self, rule):
+        """explain.hpp:59-64 select_nodes: "degree-range:[lo,hi]:count" or
+        a comma-separated id list."""
+        cnt = C.c_uint64()
+        rb = rule.encode()
+        _chk(lib.sf_select_nodes(self.h, rb, None, C.c_uint64(0), C.byref(cnt)))
+        out = np.zeros(cnt.value, np.uint32)
+        _chk(lib.sf_select_nodes(self.h, rb, _p(out), C.c_uint64(len(out)), C.byref(cnt)))
+        return out
+
     def extract(self, target, hops):
         h = C.c_void_p()
         _chk(lib.sf_extract(self.h, C.c_uint32(target), C.c_int(hops), C.byref(h)))
@@ -345,6 +355,29 @@ def _arr(ptr, n, dtype):
     if n == 0 or not ptr:
         return np.zeros(0, dtype)
     return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
+
+
+def _explanation(e):
+    n = e.num_players
+    fid = None
+    if e.has_fidelity:
+        fid = dict(top_counts=_arr(e.fid_counts, e.num_counts, np.uint32),
+                   plus=_arr(e.fid_plus, e.num_counts, np.float64),
+                   plus_random=_arr(e.fid_plus_random, e.num_counts, np.float64),
+                   sparsities=_arr(e.fid_sparsities, e.num_sparsities, np.float64),
+                   minus=_arr(e.fid_minus, e.num_sparsities, np.float64),
+                   minus_random=_arr(e.fid_minus_random, e.num_sparsities, np.float64))
+    top = list(zip(_arr(e.top_player, e.num_top, np.uint32).tolist(),
+                   _arr(e.top_phi, e.num_top, np.float64).tolist()))
+    return Explanation(
+        node=e.node, skipped=bool(e.skipped), predicted_class=e.predicted_class, base_score=e.base_score,
+        full_score=e.full_score, players=_arr(e.players_global, 2 * n, np.uint32).reshape(-1, 2),
+        phi=_arr(e.phi, n, np.float64), exhaustive=bool(e.exhaustive), rows=e.rows, iterations=e.iterations,
+        residual=e.residual, converged=bool(e.converged), top=top, fidelity=fid,
+        timings=dict(extract_ms=e.extract_ms, setup_ms=e.setup_ms, sampling_ms=e.sampling_ms,
+                     prediction_ms=e.prediction_ms, solve_ms=e.solve_ms, fidelity_ms=e.fidelity_ms,
+                     total_ms=e.total_ms),
+        warning=e.warning.decode())
 
 
 @dataclass
@@ -515,34 +548,32 @@ class Context:
 
     # ---- pipeline
     def explain_node(self, graph, model, node, opts: ExplainOptions | None = None):
+        """explain.hpp:47-49 explain_node (collective over the context's ranks)."""
         opts = opts or ExplainOptions()
         co = opts.c()
         e = _ExplanationC()
         _chk(lib.sf_explain_node(self.h, graph.h, model.h, C.c_uint32(node), C.byref(co), C.byref(e)))
         try:
-            n = e.num_players
-            phi = _arr(e.phi, n, np.float64)
-            fid = None
-            if e.has_fidelity:
-                fid = dict(top_counts=_arr(e.fid_counts, e.num_counts, np.uint32),
-                           plus=_arr(e.fid_plus, e.num_counts, np.float64),
-                           plus_random=_arr(e.fid_plus_random, e.num_counts, np.float64),
-                           sparsities=_arr(e.fid_sparsities, e.num_sparsities, np.float64),
-                           minus=_arr(e.fid_minus, e.num_sparsities, np.float64),
-                           minus_random=_arr(e.fid_minus_random, e.num_sparsities, np.float64))
-            top = list(zip(_arr(e.top_player, e.num_top, np.uint32).tolist(),
-                           _arr(e.top_phi, e.num_top, np.float64).tolist()))
-            return Explanation(
-                node=e.node, skipped=bool(e.skipped), predicted_class=e.predicted_class, base_score=e.base_score,
-                full_score=e.full_score, players=_arr(e.players_global, 2 * n, np.uint32).reshape(-1, 2), phi=phi,
-                exhaustive=bool(e.exhaustive), rows=e.rows, iterations=e.iterations, residual=e.residual,
-                converged=bool(e.converged), top=top, fidelity=fid,
-                timings=dict(extract_ms=e.extract_ms, setup_ms=e.setup_ms, sampling_ms=e.sampling_ms,
-                             prediction_ms=e.prediction_ms, solve_ms=e.solve_ms, fidelity_ms=e.fidelity_ms,
-                             total_ms=e.total_ms),
-                warning=e.warning.decode())
+            return _explanation(e)
         finally:
             lib.sf_explanation_free(C.byref(e))
+
+    def explain_nodes(self, graph, model, nodes, opts: ExplainOptions | None = None):
+        """explain.hpp:54-57 explain_nodes: one Explanation per node, in order;
+        errors carry a "node N: " prefix (explain.cpp:168-180)."""
+        opts = opts or ExplainOptions()
+        co = opts.c()
+        ids = np.ascontiguousarray(nodes, np.uint32)
+        arr = (_ExplanationC * max(len(ids), 1))()
+        _chk(lib.sf_explain_nodes(self.h, graph.h, model.h, _p(ids), C.c_uint64(len(ids)), C.byref(co), arr))
+        out = []
+        try:
+            for i in range(len(ids)):
+                out.append(_explanation(arr[i]))
+        finally:
+            for i in range(len(ids)):
+                lib.sf_explanation_free(C.byref(arr[i]))
+        return out
 
     def evaluate_fidelity(self, model, sg, class_index, phi, top_counts=(5, 10, 20),
                           sparsities=(0.1, 0.3, 0.5, 0.7, 0.9), seed=0, trials=8):

@@ -415,7 +415,7 @@ void launch_assemble(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
 
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace) {
-  (void)mode;  // round 1: reference protocol for both modes
+  if (mode != 0 && mode != 1) throw DataError("solver mode must be 0 (reference protocol) or 1 (fused)");
   CglsResult res;
   const uint32_t n = in.n;
   if (n == 0) {
@@ -434,7 +434,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2;
   const uint64_t bytes = 2 * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
                          (fblocks_max + max_splits + 2) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
-                         max_splits * n * 8 + uint64_t(n) * 8 * 4 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
+                         max_splits * n * 8 + uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
   ctx.solver_work.reserve(bytes);
   Scratch sc{ctx.solver_work.p, 0};
   uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
@@ -450,6 +450,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* kc = sc.take<double>(pairs);
   double* s_part = sc.take<double>(max_splits * n);
   double* s = sc.take<double>(n);
+  double* tv = sc.take<double>(n + 1);  // fused mode: [A^T v ; ||v||^2]
   double* u = sc.take<double>(n);
   double* phi = sc.take<double>(n);
   double* red = sc.take<double>(kRedBlocks);
@@ -548,11 +549,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const double scw = std::sqrt(in.constraint_weight);
   double r_c = scw * in.constraint_target;
 
-  // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
-  auto transpose_product = [&]() {
+  // out = M^T (sw x) (+ the pair constants); x = r (reference protocol) or
+  // v (fused mode, coefficients sw * v). Local: no collective here.
+  auto transpose_local = [&](const double* x, double* out) {
     SF_CUDA(cudaMemsetAsync(kc, 0, pairs * 8 + 8, st));
     if (pairs) {
-      coef_kernel<<<blocks_for(ptiles * 64), 256, 0, st>>>(in.dev_sw, r, is_comp, pairs, ptiles * 64,
+      coef_kernel<<<blocks_for(ptiles * 64), 256, 0, st>>>(in.dev_sw, x, is_comp, pairs, ptiles * 64,
                                                           coef_e, coef_o, kc);
       SF_LAUNCHED(ctx);
     }
@@ -564,8 +566,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       transpose_partial_kernel<<<grid, 256, 0, st>>>(mto, Wp, n, split_start, coef_o, 1, s_part);
       SF_LAUNCHED(ctx);
     }
-    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits, n, scal + 4, s);
+    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits, n, scal + 4, out);
     SF_LAUNCHED(ctx);
+  };
+  // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
+  auto transpose_product = [&]() {
+    transpose_local(r, s);
     comm_allreduce_sum(ctx, s, n);
     add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw * r_c, n);
     SF_LAUNCHED(ctx);
@@ -613,6 +619,71 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   SF_CUDA(cudaMemcpyAsync(u, s, uint64_t(n) * 8, cudaMemcpyDeviceToDevice, st));
   const double blowup = 1.0e12 * std::max(res.relative_residual, 1.0);
   const uint64_t maxit = max_iter ? max_iter : std::min<uint64_t>(n, 5000);
+  if (mode == 1) {
+    // Fused protocol: per iteration one (n+1)-double
+    // all-reduce of [A^T v ; ||v||^2]; s follows the recurrence
+    // s <- s - theta A^T A u instead of s = A^T r (same math, different
+    // rounding; r is not formed). Stop rule and error semantics unchanged.
+    while (res.iterations < maxit) {
+      reduce(u, n, 0, 0.0, scal + 0);  // sum_u (pin row: v_c = scw sum_u)
+      if (rows) {
+        const size_t smem = size_t(std::min<uint32_t>(n, kFwdChunk)) * 8;
+        SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kFwdChunk * 8)));
+        forward_kernel<<<unsigned(fblocks), kFwdThreads, smem, st>>>(in.dev_rows, W, row_start, is_comp, u,
+                                                                     n, in.dev_sw, scal + 0, v, dsq);
+        SF_LAUNCHED(ctx);
+        transpose_local(v, tv);
+      } else {
+        SF_CUDA(cudaMemsetAsync(tv, 0, uint64_t(n) * 8, st));
+      }
+      reduce(dsq, rows ? fblocks : 0, 0, 0.0, tv + n);
+      comm_allreduce_sum(ctx, tv, uint64_t(n) + 1);
+      fetch(0, 1);
+      SF_CUDA(cudaMemcpyAsync(host + 1, tv + n, sizeof(double), cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaStreamSynchronize(st));
+      ctx.d2h_bytes += sizeof(double);
+      const double v_c = scw * host[0];
+      const double delta = host[1] + v_c * v_c;
+      if (!std::isfinite(delta))
+        throw NumericalError("iterative solve diverged at iteration " +
+                             std::to_string(res.iterations) + ": non-finite step norm");
+      if (delta <= 0.0) break;
+      const double theta = gamma / delta;
+      host[8] = gamma;
+      host[9] = delta;
+      SF_CUDA(cudaMemcpyAsync(scal + 8, host + 8, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+      axpy_kernel<<<blocks_for(n), 256, 0, st>>>(phi, u, scal + 8, scal + 9, 1.0, n);
+      SF_LAUNCHED(ctx);
+      // s -= theta (A^T v + scw v_c)
+      add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(tv, scw * v_c, n);
+      SF_LAUNCHED(ctx);
+      axpy_kernel<<<blocks_for(n), 256, 0, st>>>(s, tv, scal + 8, scal + 9, -1.0, n);
+      SF_LAUNCHED(ctx);
+      r_c -= theta * v_c;
+      reduce(s, n, 1, 0.0, scal + 3);
+      fetch(3, 1);
+      const double gamma_next = host[3];
+      ++res.iterations;
+      res.relative_residual = std::sqrt(gamma_next / reference);
+      if (trace) res.trace.push_back(res.relative_residual);
+      if (!std::isfinite(gamma_next) || res.relative_residual > blowup)
+        throw NumericalError("iterative solve diverged at iteration " +
+                             std::to_string(res.iterations) + ": residual exploded");
+      if (res.relative_residual <= tol) {
+        res.converged = true;
+        break;
+      }
+      host[10] = gamma_next;
+      host[11] = gamma;
+      SF_CUDA(cudaMemcpyAsync(scal + 10, host + 10, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+      direction_kernel<<<blocks_for(n), 256, 0, st>>>(u, s, scal + 10, scal + 11, n);
+      SF_LAUNCHED(ctx);
+      gamma = gamma_next;
+    }
+    download_phi();
+    return res;
+  }
   while (res.iterations < maxit) {
     double delta = 0.0, v_c = 0.0;
     forward_product(delta, v_c);

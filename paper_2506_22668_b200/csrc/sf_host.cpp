@@ -7,6 +7,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cinttypes>
+#include <charconv>
 #include <fstream>
 #include <numeric>
 #include <sstream>
@@ -1362,13 +1364,95 @@ int sf_explain_node(sf_ctx* ctx, const sf_graph* g, const sf_model* m, uint32_t 
     else
       sf_explain_options_default(&o);
     SF_CUDA(cudaSetDevice(ctx->c.device));
-    try {
-      explain_node(ctx->c, g->g, m->m, node, o, out);
-    } catch (const DataError& e) {  // explain.cpp:171-175
-      throw DataError("node " + std::to_string(node) + ": " + e.what());
-    } catch (const NumericalError& e) {
-      throw NumericalError("node " + std::to_string(node) + ": " + e.what());
+    explain_node(ctx->c, g->g, m->m, node, o, out);
+  });
+}
+
+int sf_explain_nodes(sf_ctx* ctx, const sf_graph* g, const sf_model* m, const uint32_t* nodes,
+                     uint64_t count, const sf_explain_options* opts, sf_explanation* out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(g, "graph");
+    need(m, "model");
+    if (count) {
+      need(nodes, "nodes");
+      need(out, "output");
     }
+    if (m->m.layers.front().in != g->g.feature_dim)  // explain.cpp:149-153
+      throw DataError("model expects " + std::to_string(m->m.layers.front().in) +
+                      " input features but the graph has " + std::to_string(g->g.feature_dim));
+    sf_explain_options o;
+    if (opts)
+      o = *opts;
+    else
+      sf_explain_options_default(&o);
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    uint64_t done = 0;
+    try {
+      for (; done < count; ++done) {
+        const uint32_t node = nodes[done];
+        try {
+          explain_node(ctx->c, g->g, m->m, node, o, &out[done]);
+        } catch (const DataError& e) {  // explain.cpp:171-175
+          throw DataError("node " + std::to_string(node) + ": " + e.what());
+        } catch (const NumericalError& e) {
+          throw NumericalError("node " + std::to_string(node) + ": " + e.what());
+        }
+      }
+    } catch (...) {
+      for (uint64_t i = 0; i <= done && i < count; ++i) sf_explanation_free(&out[i]);
+      throw;
+    }
+  });
+}
+
+// explain.cpp:183-230: "degree-range:[lo,hi]:count" or a comma-separated id list
+int sf_select_nodes(const sf_graph* g, const char* rule, uint32_t* out, uint64_t cap,
+                    uint64_t* count) {
+  return guard([&] {
+    need(g, "graph");
+    need(rule, "rule");
+    need(count, "count");
+    const Graph& gr = g->g;
+    const std::string r(rule);
+    std::vector<uint32_t> sel;
+    const std::string pre = "degree-range:[";
+    if (r.rfind("degree-range", 0) == 0) {
+      uint64_t lo = 0, hi = 0, want = 0;
+      char tail = 0;
+      const bool ok = r.rfind(pre, 0) == 0 &&
+                      std::sscanf(r.c_str() + pre.size(), "%20" SCNu64 ",%20" SCNu64 "]:%20" SCNu64 "%c", &lo, &hi,
+                                  &want, &tail) == 3 &&
+                      r.find_first_not_of("0123456789,]:", pre.size()) == std::string::npos;
+      if (!ok)
+        throw DataError("malformed selection rule '" + r + "' (expected degree-range:[lo,hi]:count)");
+      if (lo > hi)
+        throw DataError("degree range [" + std::to_string(lo) + "," + std::to_string(hi) + "] is empty");
+      for (uint32_t u = 0; u < gr.num_nodes && sel.size() < want; ++u) {
+        const uint64_t deg = gr.row_ptr[u + 1] - gr.row_ptr[u];
+        if (deg >= lo && deg <= hi) sel.push_back(u);
+      }
+    } else {
+      size_t pos = 0;
+      while (pos <= r.size()) {
+        size_t comma = r.find(',', pos);
+        if (comma == std::string::npos) comma = r.size();
+        size_t b = pos, e = comma;
+        while (b < e && r[b] == ' ') ++b;
+        while (e > b && r[e - 1] == ' ') --e;
+        uint64_t id = 0;
+        const auto [ptr, ec] = std::from_chars(r.data() + b, r.data() + e, id);
+        if (ec != std::errc{} || ptr != r.data() + e || b == e)
+          throw DataError("cannot parse node id '" + r.substr(pos, comma - pos) + "' in selection '" + r + "'");
+        if (id >= gr.num_nodes)
+          throw DataError("node id " + std::to_string(id) + " out of range for a graph with " +
+                          std::to_string(gr.num_nodes) + " nodes");
+        sel.push_back(uint32_t(id));
+        pos = comma + 1;
+      }
+    }
+    *count = sel.size();
+    if (out) std::memcpy(out, sel.data(), std::min<uint64_t>(cap, sel.size()) * 4);
   });
 }
 

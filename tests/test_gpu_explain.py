@@ -92,3 +92,54 @@ def test_c1_end_to_end_vs_reference(ctx, ref, port):
     assert [p for p, _ in ex.top] == top_ref.tolist()
     np.testing.assert_allclose(ex.fidelity["plus"], rx["fidelity_plus"], rtol=1e-4, atol=1e-6)
     assert ex.converged == bool(rx["converged"])
+
+
+def test_explain_nodes_matches_explain_node(ctx):
+    """explain.cpp:145-181 explain_nodes: per-node results identical to
+    explain_node; an error names the node ("node N: ")."""
+    d = W.build("C1")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+    nodes = g.select_nodes("degree-range:[4,6]:3")
+    assert len(nodes) == 3
+    opts = ExplainOptions(samples=2000, seed=3, baseline_trials=2)
+    batch = ctx.explain_nodes(g, m, nodes, opts)
+    assert [e.node for e in batch] == nodes.tolist()
+    for e in batch:
+        one = ctx.explain_node(g, m, e.node, opts)
+        assert np.array_equal(one.phi, e.phi)
+        assert one.top == e.top
+    bad = sf.Model.random(cfg.feature_dim + 1, cfg.hidden, cfg.classes, 1)
+    with pytest.raises(sf.DataError, match="input features"):
+        ctx.explain_nodes(g, bad, nodes, opts)
+    small = sf.Graph.build(3, np.array([[0, 1]], np.uint64), np.ones((3, cfg.feature_dim), np.float32))
+    with pytest.raises(sf.DataError, match="^node 7: "):
+        ctx.explain_nodes(small, m, [0, 7], opts)
+    assert ctx.explain_nodes(g, m, [], opts) == []
+
+
+@pytest.mark.parametrize("n", [40, 300])
+def test_fused_solver_mode_matches_reference_protocol(ctx, port, n):
+    """solver_mode 1 (one (n+1)-double all-reduce per iteration, s by
+    recurrence) reaches the same phi as the reference protocol (mode 0)
+    within the 1e-3 bar and uses exactly one vector all-reduce per
+    iteration (+1 at init)."""
+    d = W.build("C1")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+    res = {}
+    for mode in (0, 1):
+        s0 = ctx.stats()
+        ex = ctx.explain_node(g, m, d["target"], ExplainOptions(samples=cfg.samples, seed=n, solver_mode=mode,
+                                                                fidelity=False))
+        s1 = ctx.stats()
+        res[mode] = (ex, {k: s1[k] - s0[k] for k in s1})
+    e0, e1 = res[0][0], res[1][0]
+    assert np.linalg.norm(e1.phi - e0.phi) <= 1e-3 * np.linalg.norm(e0.phi)
+    assert [p for p, _ in e1.top] == [p for p, _ in e0.top]
+    assert abs(e1.iterations - e0.iterations) <= 2
+    st = res[1][1]
+    assert st["vector_allreduce"] == e1.iterations + 1
+    assert st["scalar_allreduce"] == 0

@@ -33,8 +33,14 @@ g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
 m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
 ex = ctx.explain_node(g, m, d["target"], ExplainOptions(samples=cfg.samples, seed=cfg.explain_seed))
 st = ctx.stats()
+fx = ctx.explain_node(g, m, d["target"], ExplainOptions(samples=cfg.samples, seed=cfg.explain_seed, solver_mode=1,
+                                                        fidelity=False))
+st2 = ctx.stats()
 out = {"rank": rank, "phi": ex.phi.tolist(), "iterations": ex.iterations, "top": [p for p, _ in ex.top],
-       "converged": ex.converged, "stats": st, "fid": ex.fidelity["plus"].tolist()}
+       "converged": ex.converged, "stats": st, "fid": ex.fidelity["plus"].tolist(),
+       "fused_phi": fx.phi.tolist(), "fused_iterations": fx.iterations,
+       "fused_vec": st2["vector_allreduce"] - st["vector_allreduce"],
+       "fused_scalar": st2["scalar_allreduce"] - st["scalar_allreduce"]}
 with open(os.path.join(os.environ["SF_OUT"], f"rank{rank}.json"), "w") as f:
     json.dump(out, f)
 ctx.close()
@@ -84,3 +90,9 @@ def test_two_gpu_explain_matches_single(tmp_path, ctx, ref):
     for r in res:
         it = r["iterations"]
         assert r["stats"]["scalar_allreduce"] >= it and r["stats"]["vector_allreduce"] >= it + 1
+    # fused protocol: one (n+1)-double all-reduce per iteration (+1 at init), replicated phi
+    assert res[0]["fused_phi"] == res[1]["fused_phi"]
+    fphi = np.array(res[0]["fused_phi"])
+    assert np.linalg.norm(fphi - rx["phi"]) <= 1e-3 * np.linalg.norm(rx["phi"])
+    for r in res:
+        assert r["fused_vec"] == r["fused_iterations"] + 1 and r["fused_scalar"] == 0

@@ -10,6 +10,7 @@ import pytest
 import paper_2506_22668_b200 as sf
 from conftest import toy_graph_arrays
 from paper_2506_22668_b200 import workloads as W
+from oracle.pyoracle import OracleError
 
 
 def test_library_exports_every_header_symbol():
@@ -144,3 +145,23 @@ def test_context_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(sf.ShapflowError):
         sf.Context(0)
+
+
+def test_select_nodes_matches_reference(ref):
+    """explain.cpp:183-230 select_nodes: degree-range rule and id lists,
+    results and DataError messages identical to the compiled reference."""
+    d = W.build("C1")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    rg = ref.graph_build(cfg.nodes, d["edges"], d["features"])
+    for rule in ("degree-range:[3,10]:50", "degree-range:[0,0]:5", "degree-range:[1,100000]:7",
+                 "degree-range:[40,41]:1000", "5", "1, 5 ,7", "0,0,2707"):
+        assert g.select_nodes(rule).tolist() == ref.select_nodes(rg, rule).tolist(), rule
+    for rule in ("degree-range:[5,2]:3", "degree-range:[1,2]", "degree-range:[a,2]:3", "1,x", "2708",
+                 "", "3,,4", " -1"):
+        with pytest.raises(sf.DataError) as ours:
+            g.select_nodes(rule)
+        with pytest.raises(OracleError) as theirs:
+            ref.select_nodes(rg, rule)
+        assert theirs.value.code == 2
+        assert str(ours.value).endswith(str(theirs.value).split("] ", 1)[1]), rule
