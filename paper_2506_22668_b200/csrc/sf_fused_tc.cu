@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // entries [16 (sw / 4), +16).
       {
         const int sw = warp - kEpiWarps, q = sw & 3, k0 = (sw >> 2) * 16;
-        if (k0 < cnt) {
+        if (k0 < cnt && !(PROF && (exp & 8))) {
           const int m = q * 32 + lane, tq = m >> 6, i = m & 63;
           uint32_t hv[16], lv[16];
 #pragma unroll
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TC_WAIT(0, &hfull[b], (sg >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < NCH; ++cc) {
+      for (int cc = 0; cc < ((PROF && (exp & 16)) ? 0 : NCH); ++cc) {
         const uint32_t hcol = tmem + lane_base + b * D + hb + cc * CW;
         const uint32_t acol = tmem + lane_base + acc_col + cc * CW;
         if constexpr (CW == 32) {
@@ -547,7 +547,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // SF_TC_EXP (PROF only, results invalid): bit 0 skips the isd-row gathers,
-// bit 1 the P-row gathers, bit 2 the B transposition
+// bit 1 the P-row gathers, bit 2 the B transposition, bit 3 the A stores to
+// TMEM, bit 4 the epilogue's TMEM loads/stores and math
 int exp_flags() {
   static const int f = std::getenv("SF_TC_EXP") ? std::atoi(std::getenv("SF_TC_EXP")) : 0;
   return f;
