@@ -45,7 +45,7 @@ constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
 constexpr int kRawStages = 3, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 3;
+constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 7;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 
@@ -58,7 +58,7 @@ struct TcCfg {
   static constexpr int OFF_BLO = B_BYTES;
   static constexpr int STAGE = ((2 * B_BYTES + 1023) / 1024) * 1024;
   // raw stage (bulk copies): records | P rows | isd rows (2 tiles) | mask blocks (2 tiles)
-  static constexpr int RAW_P = kKC * 8;
+  static constexpr int RAW_P = 0;
   static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
   static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
   static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
@@ -141,6 +141,24 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Warp-converged variants: every lane of the warp executes them, one
+// elected lane issues (keeps the operands warp-uniform, no per-MMA elect loop)
+__device__ __forceinline__ void tc_mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(b))
       : "memory");
 }
 // Shared-memory matrix descriptor, no swizzle (SmemDescriptor, version 1)
@@ -286,11 +304,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= kProducerWarp && warp < kMmaWarp) {
     // ------------------------------------------------------------ producers
-    // 16-byte cp.async gathers (LDGSTS) of the chunk's records, P rows, isd
-    // rows (both tiles) and mask blocks; each producer thread arrives on
-    // raw_full once its own copies have landed.
+    // 16-byte cp.async gathers (LDGSTS) of the chunk's P rows, isd rows
+    // (both tiles) and mask words; each producer thread arrives on raw_full
+    // once its own copies have landed. (Lane-parallel cp.async.bulk from one
+    // warp was measured 2x slower: bulk-copy issue serializes.)
     const int pt = tid - kProducerWarp * 32;
-    const int pw_base = pt - lane;  // first J of this warp  // 0..127
+    const int pw_base = pt - lane;  // first J of this warp
     uint2 rec_next = make_uint2(0, kPad);
     if (lane < int(e1 - e0)) rec_next = ent[e0 + lane];
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -301,7 +320,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (base + kKC + lane < e1) rec_next = ent[base + kKC + lane];
       if (c >= uint32_t(kRawStages)) TC_WAIT(0, &raw_empty[r], ((c / kRawStages) - 1) & 1);
       unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
-      if (pt < cnt / 2) cp_async16(rw + pt * 16, ent + base + 2 * pt);  // records
       // trip counts are warp-uniform (J0 steps by whole warps), so every lane
       // takes part in the shuffles
       if (!PROF || !(exp & 2))
@@ -338,7 +356,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (c >= uint32_t(kCanStages)) TC_WAIT(1, &can_empty[s], ((c / kCanStages) - 1) & 1);
       tc_fence_after();  // the A stage in TMEM is rewritten after the MMAs that read it
       const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
-      const uint2* recs = reinterpret_cast<const uint2*>(rw);
       const float* Ps = reinterpret_cast<const float*>(rw + Cfg::RAW_P);
       const float* isds = reinterpret_cast<const float*>(rw + Cfg::RAW_ISD);
       const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
@@ -395,49 +412,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sfl = smem + Cfg::OFF_KFL;
     for (uint32_t j = lane; j < (e1 - e0) / 8; j += 32) sfl[j] = kflags[e0 / 8 + j];
     __syncwarp();
-    if (lane == 0) {
-      // kind::tf32, D f32, A and B K-major, N = D, M = 128
+    {
+      // The whole warp runs the loop (warp-uniform values), one elected lane
+      // issues each MMA / commit. kind::tf32, D f32, A (TMEM) and B (smem) K-major, N = D, M = 128.
+      // The issue loop is kept short (MMA issue latency, not the tensor
+      // pipe, bounds a looped issuer; csrc/tools/tc_rate_probe.cu):
+      // descriptors are per-stage bases plus constant k-step offsets, the
+      // chunk's four k-step flags come from one 32-bit load.
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(D >> 3) << 17) |
                              (uint32_t(kM >> 4) << 24);
+      uint64_t bhi0[kCanStages], blo0[kCanStages];
+#pragma unroll
+      for (int st2 = 0; st2 < kCanStages; ++st2) {
+        const uint32_t sa = su32(smem + st2 * Cfg::STAGE);
+        bhi0[st2] = smem_desc(sa + Cfg::OFF_BHI, Cfg::B_LBO, 128);
+        blo0[st2] = smem_desc(sa + Cfg::OFF_BLO, Cfg::B_LBO, 128);
+      }
+      constexpr uint64_t kStep = uint64_t(2 * Cfg::B_LBO) >> 4;  // descriptor address units per k-step
+      const uint32_t* sfl32 = reinterpret_cast<const uint32_t*>(sfl);
       uint32_t sg = 0, b = 0, acc = 0;
       for (uint32_t c = 0; c < nchunks; ++c) {
         const int s = c % kCanStages;
         TC_WAIT(0, &can_full[s], (c / kCanStages) & 1);
         tc_fence_after();
-        const uint32_t base = e0 + c * kKC;
-        const int nk = int(min(uint32_t(kKC), e1 - base)) / 8;
-        const uint32_t sa = su32(smem + s * Cfg::STAGE);
-        for (int j = 0; j < nk; ++j) {
-          const uint8_t f = sfl[(base - e0) / 8 + j];
-          if (f & 1u) {
-            b = sg & 1u;
-            if (sg >= 2) {
-              TC_WAIT(1, &hfree[b], ((sg >> 1) - 1) & 1);
-              tc_fence_after();
+        const int nk = int(min(uint32_t(kKC), e1 - (e0 + c * kKC))) / 8;
+        const uint32_t fw = sfl32[c];
+        const uint32_t a0 = tmem + Cfg::A_COL + s * 2 * kKC;
+        static_assert(kCanStages == 2, "stage select below");
+        const uint64_t bhs = s ? bhi0[1] : bhi0[0], bls = s ? blo0[1] : blo0[0];
+#pragma unroll
+        for (int j = 0; j < kKC / 8; ++j) {
+          if (j < nk) {
+            const uint32_t f = (fw >> (8 * j)) & 0xFFu;
+            if (f & 1u) {
+              b = sg & 1u;
+              if (sg >= 2) {
+                TC_WAIT(1, &hfree[b], ((sg >> 1) - 1) & 1);
+                tc_fence_after();
+              }
+              acc = 0;
             }
-            acc = 0;
-          }
-          const uint32_t d = tmem + b * D;
-          const uint32_t ahi = tmem + Cfg::A_COL + s * 2 * kKC + j * 8, alo = ahi + kKC;
-          const uint64_t bhi = smem_desc(sa + Cfg::OFF_BHI + j * 2 * Cfg::B_LBO, Cfg::B_LBO, 128);
-          const uint64_t blo = smem_desc(sa + Cfg::OFF_BLO + j * 2 * Cfg::B_LBO, Cfg::B_LBO, 128);
-          tc_mma_ts(d, ahi, bhi, idesc, acc);
-          tc_mma_ts(d, ahi, blo, idesc, 1);
-          tc_mma_ts(d, alo, bhi, idesc, 1);
-          acc = 1;
-          if (f & 2u) {
-            tc_commit(&hfull[b]);
-            ++sg;
+            const uint32_t d = tmem + b * D, ahi = a0 + j * 8;
+            const uint64_t bh = bhs + j * kStep, bl = bls + j * kStep;
+            tc_mma_ts_elect(d, ahi, bh, idesc, acc);
+            tc_mma_ts_elect(d, ahi, bl, idesc, 1);
+            tc_mma_ts_elect(d, ahi + kKC, bh, idesc, 1);
+            acc = 1;
+            if (f & 2u) {
+              tc_commit_elect(&hfull[b]);
+              ++sg;
+            }
           }
         }
-        tc_commit(&can_empty[s]);
+        tc_commit_elect(&can_empty[s]);
       }
       prof_flush(6, 2);  // 6 wait can_full, 7 wait hfree, 8 total
     }
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
     // warp w: TMEM lane quarter w % 4 (coalitions), columns [hb, hb + D/2)
-    constexpr int HALF = D / 2, CW = HALF >= 32 ? 32 : 16, NCH = HALF / CW;
+    constexpr int HALF = D / 2, CW = 16, NCH = HALF / CW;
     const int q = warp & 3;
     const int hb = (warp >> 2) * HALF;
     const int m = q * 32 + lane;
