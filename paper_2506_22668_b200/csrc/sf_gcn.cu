@@ -41,16 +41,31 @@ constexpr int kTile = 64;  // coalitions per tile
 // j/G, incidence j%G), transposes the 32 x 64 bit block with a butterfly so
 // lane l holds coalitions l and l+32, and counts each tile's G-bit field
 // with popc.
-__device__ __forceinline__ uint32_t bfly32(uint32_t x, int lane) {
+// 32x32 bit transpose across a warp: lane l ends with bit j = bit l of lane
+// j's input. Per stage s each lane sends rot(x) & keep (rotate right by s,
+// or by 32 - s on lanes with bit s set) and keeps x & keep; the per-lane
+// rotate amounts and keep masks are computed once (Bfly).
+struct Bfly {
+  uint32_t keep[5], amt[5];
+  __device__ __forceinline__ explicit Bfly(int lane) {
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
-                     : s == 2 ? 0x33333333u : 0x55555555u;
-    const uint32_t y = __shfl_xor_sync(kFull, x, s);
-    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+    for (int q = 0; q < 5; ++q) {
+      const int sh = 16 >> q;
+      const uint32_t m = sh == 16 ? 0x0000FFFFu : sh == 8 ? 0x00FF00FFu : sh == 4 ? 0x0F0F0F0Fu
+                       : sh == 2 ? 0x33333333u : 0x55555555u;
+      keep[q] = (lane & sh) ? ~m : m;
+      amt[q] = (lane & sh) ? 32 - sh : sh;
+    }
   }
-  return x;  // lane l: bit j = bit l of lane j's input
-}
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const uint32_t send = __funnelshift_r(x, x, amt[q]) & keep[q];
+      x = (x & keep[q]) | __shfl_xor_sync(kFull, send, 16 >> q);
+    }
+    return x;
+  }
+};
 
 __global__ void __launch_bounds__(256)
     isd_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, uint32_t ntiles,
@@ -59,6 +74,7 @@ __global__ void __launch_bounds__(256)
                uint32_t nbig, const float* __restrict__ tab, uint32_t V,
                float* __restrict__ isd) {
   const int lane = threadIdx.x & 31;
+  const Bfly bfly32(lane);
   const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
   const uint32_t big_warps = nbig * ntiles;
   if (w < big_warps) {  // hub: one tile, 32-incidence chunks
@@ -69,8 +85,8 @@ __global__ void __launch_bounds__(256)
     const uint32_t beg = row_ptr[u], end = row_ptr[u + 1];
     for (uint32_t i = beg + lane; i - lane < end; i += 32) {
       const uint64_t x = i < end ? __ldg(&mt[__ldg(&ep[i])]) : 0ull;
-      clo += __popc(bfly32(uint32_t(x), lane));
-      chi += __popc(bfly32(uint32_t(x >> 32), lane));
+      clo += __popc(bfly32(uint32_t(x)));
+      chi += __popc(bfly32(uint32_t(x >> 32)));
     }
     float* out = isd + (t * V + u) * kTile;
     out[lane] = __ldg(&tab[clo]);
@@ -98,7 +114,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t t0 = 0; t0 < ntiles; t0 += per) {
     const uint32_t t = t0 + sub;
     const uint64_t x = (slot < deg && t < ntiles) ? __ldg(&maskt[uint64_t(t) * Wp + p]) : 0ull;
-    const uint32_t lo = bfly32(uint32_t(x), lane), hi = bfly32(uint32_t(x >> 32), lane);
+    const uint32_t lo = bfly32(uint32_t(x)), hi = bfly32(uint32_t(x >> 32));
     for (uint32_t q = 0; q < per && t0 + q < ntiles; ++q) {
       const uint32_t sh = q << lg;
       float* out = isd + (uint64_t(t0 + q) * V + u) * kTile;
@@ -558,6 +574,26 @@ __device__ __forceinline__ void softmax_row(float* zi, uint32_t C) {
   for (uint32_t c = 0; c < C; ++c) zi[c] = zi[c] / sum;
 }
 
+// The same float softmax with the warp's lanes over the classes: max and
+// sum by butterfly reductions (sum order differs from the sequential
+// reference loop by float rounding only), exp and divide per lane.
+__device__ __forceinline__ void softmax_row_warp(float* zi, uint32_t C, int lane) {
+  float mx = -INFINITY;
+  for (uint32_t c = lane; c < C; c += 32) mx = fmaxf(mx, zi[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+  for (uint32_t c = lane; c < C; c += 32) {
+    const float e = expf(zi[c] - mx);
+    zi[c] = e;
+    sum += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  for (uint32_t c = lane; c < C; c += 32) zi[c] = zi[c] / sum;
+  __syncwarp();
+}
+
 // A[t][u][i][:] = isd_i(u) * sum over the items of u of Apart[t][item][i][:]
 // (fixed item order, deterministic), one float4 per thread.
 __global__ void __launch_bounds__(256)
@@ -762,6 +798,8 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
   }
 }
 
+constexpr int kTailThreads = 512;
+
 // ---------------------------------------------------------------- fused tail
 // Everything after the fused layer-0/1 kernel, for one tile t and cpb
 // coalitions per CTA, in shared memory (replaces reduce_partials + sgemm +
@@ -773,7 +811,7 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
 //   L == 2:  z_i = H[0][i] (logits, no activation)
 //   p_i = softmax(z_i) (gcn.cpp:143-152); out = p_i[cls].
 // Rows of A and H are u-major: r = u * cpb + il.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kTailThreads, 2)
     tail_kernel(const float4* __restrict__ Apart, uint32_t items,
                 const uint32_t* __restrict__ u_items, const uint64_t* __restrict__ maskt,
                 uint64_t Wp, const uint32_t* __restrict__ row_ptr,
@@ -843,31 +881,40 @@ __global__ void __launch_bounds__(256)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // H = act(A W1 + b1): job = (column n, 4 rows)
-  constexpr uint32_t RB = 4;
-  const uint32_t groups = (R + RB - 1) / RB;
-  for (uint32_t job = tid; job < N * groups; job += blockDim.x) {
-    const uint32_t n = job % N, r0 = (job / N) * RB;
-    float acc[RB] = {};
-    for (uint32_t k4 = 0; k4 < K4; ++k4) {
-      const float w0 = sW1[(4 * k4) * N + n], w1 = sW1[(4 * k4 + 1) * N + n];
-      const float w2 = sW1[(4 * k4 + 2) * N + n], w3 = sW1[(4 * k4 + 3) * N + n];
+  // H = act(A W1 + b1): thread = (column n, row group of up to kRB rows),
+  // one job per thread when N * ceil(R / kRB) <= blockDim.x
+  constexpr uint32_t kRB = 8;
+  const uint32_t rgroups = max(1u, min(R, blockDim.x / N));
+  const uint32_t RB = (R + rgroups - 1) / rgroups;
+  for (uint32_t job = tid; job < N * rgroups; job += blockDim.x) {
+    const uint32_t n = job % N, g = job / N;
+    for (uint32_t rb0 = g * RB; rb0 < min(R, (g + 1) * RB); rb0 += kRB) {
+      const uint32_t nr = min(kRB, min(R, (g + 1) * RB) - rb0);
+      float acc[kRB];
 #pragma unroll
-      for (uint32_t j = 0; j < RB; ++j) {
-        if (r0 + j >= R) break;
-        const float4 a = sA[(r0 + j) * K4 + k4];
-        acc[j] = fmaf(a.x, w0, acc[j]);
-        acc[j] = fmaf(a.y, w1, acc[j]);
-        acc[j] = fmaf(a.z, w2, acc[j]);
-        acc[j] = fmaf(a.w, w3, acc[j]);
+      for (uint32_t j = 0; j < kRB; ++j) acc[j] = 0.f;
+      for (uint32_t k4 = 0; k4 < K4; ++k4) {
+        const float w0 = sW1[(4 * k4) * N + n], w1 = sW1[(4 * k4 + 1) * N + n];
+        const float w2 = sW1[(4 * k4 + 2) * N + n], w3 = sW1[(4 * k4 + 3) * N + n];
+#pragma unroll
+        for (uint32_t j = 0; j < kRB; ++j) {
+          if (j < nr) {
+            const float4 a = sA[(rb0 + j) * K4 + k4];
+            acc[j] = fmaf(a.x, w0, acc[j]);
+            acc[j] = fmaf(a.y, w1, acc[j]);
+            acc[j] = fmaf(a.z, w2, acc[j]);
+            acc[j] = fmaf(a.w, w3, acc[j]);
+          }
+        }
       }
-    }
-    const float bn = b1[n];
+      const float bn = b1[n];
 #pragma unroll
-    for (uint32_t j = 0; j < RB; ++j) {
-      if (r0 + j >= R) break;
-      const float v = acc[j] + bn;
-      sH[(r0 + j) * N + n] = three_layer ? fmaxf(v, 0.f) : v;
+      for (uint32_t j = 0; j < kRB; ++j) {
+        if (j < nr) {
+          const float v = acc[j] + bn;
+          sH[(rb0 + j) * N + n] = three_layer ? fmaxf(v, 0.f) : v;
+        }
+      }
     }
   }
   __syncthreads();
@@ -887,9 +934,15 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     for (uint32_t idx = tid; idx < cpb * C; idx += blockDim.x) {
       const uint32_t il = idx / C, c = idx % C;
-      float v = b2[c];
-      for (uint32_t k = 0; k < N; ++k) v = __fadd_rn(v, __fmul_rn(sa[il * N + k], sW2[k * C + c]));
-      sz[idx] = v;
+      // bias-first (gcn.cpp:116-123), even and odd k in two chains
+      float v0 = b2[c], v1 = 0.f;
+      uint32_t k = 0;
+      for (; k + 1 < N; k += 2) {
+        v0 = __fadd_rn(v0, __fmul_rn(sa[il * N + k], sW2[k * C + c]));
+        v1 = __fadd_rn(v1, __fmul_rn(sa[il * N + k + 1], sW2[(k + 1) * C + c]));
+      }
+      if (k < N) v0 = __fadd_rn(v0, __fmul_rn(sa[il * N + k], sW2[k * C + c]));
+      sz[idx] = __fadd_rn(v0, v1);
     }
   } else {
     for (uint32_t idx = tid; idx < cpb * C; idx += blockDim.x) sz[idx] = sH[idx];  // U == 1: row il
@@ -899,10 +952,8 @@ __global__ void __launch_bounds__(256)
   for (uint32_t il = warp; il < cpb; il += nwarps) {
     const uint64_t row = row0 + t * kTile + i0 + il;
     if (row >= rows) continue;
-    if (lane == 0) {
-      softmax_row(sz + il * C, C);
-      out[row] = sz[il * C + cls];
-    }
+    softmax_row_warp(sz + il * C, C, lane);
+    if (lane == 0) out[row] = sz[il * C + cls];
     __syncwarp();
     if (allprobs)
       for (uint32_t c = lane; c < C; c += 32) allprobs[row * C + c] = sz[il * C + c];
@@ -1201,7 +1252,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
             attr = true;
           }
           dim3 grid(unsigned(nt), kTile / cpb);
-          tail_kernel<<<grid, 256, smem, ctx.stream>>>(
+          tail_kernel<<<grid, kTailThreads, smem, ctx.stream>>>(
               reinterpret_cast<const float4*>(pbuf), e.tc ? e.tc_items : e.items,
               e.tc ? e.tc_u_items.p : e.u_items.p, maskt, Wp, e.row_ptr.p, e.col.p,
               e.edge_player.p, isd, e.V, e.U, K, N, e.w[1]->p, e.b[1]->p,

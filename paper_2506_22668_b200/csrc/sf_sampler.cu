@@ -235,31 +235,34 @@ __global__ void philox_stream_kernel(uint64_t seed, uint64_t stream,
 }
 
 // Rows -> tile layout: out[t][e] bit i = bit e of row t*64+i (rows past
-// `rows` read as zero). One CTA per (tile, 32-word chunk) stages the
-// 64 x 32 words coalesced in shared memory; each warp then transposes 4
-// words, each a 64 x 64 bit block, as four 32 x 32 butterfly transposes
+// `rows` read as zero). One CTA per (tile, kTWords-word chunk) stages the
+// 64 x kTWords words coalesced in shared memory; each warp then transposes
+// kTWords/8 words, each a 64 x 64 bit block, as four 32 x 32 butterfly transposes
 // (5 shuffle stages each) and writes 256 contiguous bytes per output half.
-__device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t m, int lane) {
-  const uint32_t y = __shfl_xor_sync(kFull, x, s);
-  return (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+// one butterfly stage (see Bfly in sf_gcn.cu): send rot(x) & keep, keep x & keep
+__device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t keep, uint32_t amt) {
+  const uint32_t send = __funnelshift_r(x, x, amt) & keep;
+  return (x & keep) | __shfl_xor_sync(kFull, send, s);
 }
+
+constexpr int kTWords = 16;  // words per CTA (a multiple of 8: one or more per warp)
 
 __global__ void __launch_bounds__(256)
     transpose_tiles_kernel(const uint64_t* __restrict__ in, uint64_t rows,
                            uint32_t W, uint64_t stride, uint64_t* __restrict__ out) {
-  __shared__ uint64_t sm[64][33];
+  __shared__ uint64_t sm[64][kTWords + 1];
   const uint64_t t = blockIdx.y;
-  const uint32_t w0 = blockIdx.x * 32;
+  const uint32_t w0 = blockIdx.x * kTWords;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 64 * 32; i += 256) {
-    const int r = i >> 5, w = i & 31;
+  for (int i = tid; i < 64 * kTWords; i += 256) {
+    const int r = i / kTWords, w = i % kTWords;
     const uint64_t row = t * 64 + r;
     sm[r][w] = (row < rows && w0 + w < W) ? in[row * stride + w0 + w] : 0ull;
   }
   __syncthreads();
   const uint64_t Wp = uint64_t(W) * 64;  // players per tile, padded
 #pragma unroll 1
-  for (int w = warp * 4; w < warp * 4 + 4; ++w) {
+  for (int w = warp * (kTWords / 8); w < (warp + 1) * (kTWords / 8); ++w) {
     if (w0 + w >= W) break;
     const uint64_t r0 = sm[lane][w], r1 = sm[lane + 32][w];
     uint32_t a = uint32_t(r0), b = uint32_t(r0 >> 32), c = uint32_t(r1), d = uint32_t(r1 >> 32);
@@ -267,10 +270,11 @@ __global__ void __launch_bounds__(256)
     for (int s = 16; s >= 1; s >>= 1) {
       const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
                        : s == 2 ? 0x33333333u : 0x55555555u;
-      a = bfly_step(a, s, m, lane);
-      b = bfly_step(b, s, m, lane);
-      c = bfly_step(c, s, m, lane);
-      d = bfly_step(d, s, m, lane);
+      const uint32_t keep = (lane & s) ? ~m : m, amt = (lane & s) ? 32 - s : s;
+      a = bfly_step(a, s, keep, amt);
+      b = bfly_step(b, s, keep, amt);
+      c = bfly_step(c, s, keep, amt);
+      d = bfly_step(d, s, keep, amt);
     }
     uint64_t* o = out + t * Wp + uint64_t(w0 + w) * 64;
     o[lane] = (uint64_t(c) << 32) | a;
@@ -365,7 +369,7 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
 void launch_transpose_tiles(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                             uint32_t W, uint64_t tiles, uint64_t* dev_maskt, uint64_t stride) {
   if (tiles == 0) return;
-  dim3 grid((W + 31) / 32, unsigned(tiles));
+  dim3 grid((W + kTWords - 1) / kTWords, unsigned(tiles));
   transpose_tiles_kernel<<<grid, 256, 0, ctx.stream>>>(dev_rows, rows, W, stride ? stride : W, dev_maskt);
   SF_LAUNCHED(ctx);
 }
