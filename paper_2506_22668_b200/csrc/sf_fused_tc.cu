@@ -43,8 +43,9 @@ constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
 constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
-constexpr int kRawStages = 3, kCanStages = 2;
+constexpr int kRawStages = 4, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
+constexpr int kTabCap = 12288;    // 1/sqrt(deg) entries in shared memory (larger degrees: SIMT kernel)
 constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 7;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
@@ -60,19 +61,20 @@ struct TcCfg {
   // raw stage (bulk copies): records | P rows | isd rows (2 tiles) | mask blocks (2 tiles)
   static constexpr int RAW_P = 0;
   static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
-  static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
+  static constexpr int RAW_W = RAW_ISD + kKC * kM * 2;  // u16 degrees
   static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
   static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
   static constexpr int OFF_BIAS = OFF_KFL + kMaxKsteps;      // b0 (D floats)
   static constexpr int OFF_BARS = OFF_BIAS + D * 4;
-  static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
+  static constexpr int OFF_TAB = ((OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16 + 15) / 16) * 16;
+  static constexpr int SMEM = OFF_TAB;  // + the 1/sqrt(deg) table, sized at launch
   // TMEM columns: H buffers [0, 2D), accumulator [2D, 3D), A stages (hi 32 | lo 32) from 3D
   static constexpr uint32_t A_COL = 3 * D;
   static constexpr uint32_t TMEM_COLS = 3 * D + kCanStages * 2 * kKC <= 256 ? 256 : 512;
   static_assert(3 * D + kCanStages * 2 * kKC <= 512, "TMEM columns");
   static_assert(D % 32 == 0 && D <= 256, "width");
-  static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(SMEM + kTabCap * 4 <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -218,6 +220,8 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
 
+__device__ __noinline__ float inv_sqrt_deg_slow(uint32_t d) { return inv_sqrt_deg(d); }
+
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -244,7 +248,8 @@ constexpr int kProfSites = 16;
 template <int D, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
-                    uint32_t V, const float* __restrict__ P, const float* __restrict__ bias,
+                    uint32_t V, const uint16_t* __restrict__ deg16, const float* __restrict__ tab, uint32_t tab_n,
+                    const float* __restrict__ P, const float* __restrict__ bias,
                     const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
                     const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
@@ -292,6 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < D; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_BIAS)[j] = bias[j];
+  const uint32_t tab_s = tab_n;  // the launch sizes shared memory for the whole table
+  for (uint32_t j = tid; j < tab_s; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_TAB)[j] = tab[j];
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "r"(Cfg::TMEM_COLS));
@@ -329,12 +336,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (J < cnt * (D / 4)) cp_async16(rw + Cfg::RAW_P + (k * D + ng * 4) * 4, P + uint64_t(x) * D + ng * 4);
         }
       if (!PROF || !(exp & 1))
-        for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
-          const int J = J0 + lane, k = min(J >> 5, 31), q = (J >> 4) & 1, ug = J & 15;
+        for (int J0 = pw_base; J0 < cnt * 2 * 8; J0 += kProdWarps * 32) {  // u16 degree rows, 2 tiles
+          const int J = J0 + lane, k = min(J >> 4, 31), q = (J >> 3) & 1, ug = J & 7;
           const uint32_t x = __shfl_sync(kFull, rec.x, k);
-          if (J < cnt * 2 * 16)
-            cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
-                       isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
+          if (J < cnt * 2 * 8)
+            cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 8) * 2,
+                       deg16 + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 8);
         }
       {  // mask words, one u64 per (entry, tile); self -> all ones, pad -> zero
         const int k = pt >> 1, q = pt & 1;
@@ -357,7 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();  // the A stage in TMEM is rewritten after the MMAs that read it
       const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       const float* Ps = reinterpret_cast<const float*>(rw + Cfg::RAW_P);
-      const float* isds = reinterpret_cast<const float*>(rw + Cfg::RAW_ISD);
+      const uint16_t* degs = reinterpret_cast<const uint16_t*>(rw + Cfg::RAW_ISD);
+      const float* stab = reinterpret_cast<const float*>(smem + Cfg::OFF_TAB);
       const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
       unsigned char* st = smem + s * Cfg::STAGE;
       const int cnt = int(min(uint32_t(kKC), e1 - (e0 + c * kKC)));  // multiple of 8
@@ -372,7 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int w = 0; w < 16; ++w) {
             const int k = k0 + w;
-            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? isds[k * kM + m] : 0.f;
+            const uint32_t dg = degs[k * kM + m];
+            const float iv = stab[min(dg, tab_s - 1)];  // the table covers every degree (host check)
+            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? iv : 0.f;
             const float h = tf32_hi(cf);
             hv[w] = __float_as_uint(h);
             lv[w] = __float_as_uint(cf - h);
@@ -590,17 +600,19 @@ int exp_flags() {
 
 template <int D, bool PROF>
 void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
-                    uint64_t ntp, float* apart, unsigned long long* prof) {
+                    const uint16_t* deg16, uint64_t ntp, float* apart, unsigned long long* prof) {
   using Cfg = TcCfg<D>;
   static bool configured = false;
   if (!configured) {
     SF_CUDA(cudaFuncSetAttribute(fused_tc_kernel<D, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM));
+                                 Cfg::SMEM + kTabCap * 4));
     configured = true;
   }
+  const size_t smem = Cfg::SMEM + size_t(e.isd_tab_n) * 4;
   dim3 grid(e.tc_items, unsigned(ntp / 2));
-  fused_tc_kernel<D, PROF><<<grid, kThreads, Cfg::SMEM, ctx.stream>>>(
-      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
+  fused_tc_kernel<D, PROF><<<grid, kThreads, smem, ctx.stream>>>(
+      maskt, Wp, isd, e.V, deg16, e.isd_tab.p, e.isd_tab_n, e.p0.p, e.b[0]->p,
+      reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
       e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof,
       PROF ? exp_flags() : 0);
@@ -611,10 +623,10 @@ void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t W
 // breakdown (cycles per warp per CTA) every 100 launches to stderr.
 template <int D>
 void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
-               uint64_t ntp, float* apart) {
+               const uint16_t* deg16, uint64_t ntp, float* apart) {
   static const bool prof_on = std::getenv("SF_TC_PROF") != nullptr;
   if (!prof_on) {
-    launch_tc_impl<D, false>(ctx, e, maskt, Wp, isd, ntp, apart, nullptr);
+    launch_tc_impl<D, false>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, nullptr);
     return;
   }
   static unsigned long long* dprof = nullptr;
@@ -623,7 +635,7 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
     SF_CUDA(cudaMalloc(&dprof, kProfSites * sizeof(unsigned long long)));
     SF_CUDA(cudaMemset(dprof, 0, kProfSites * sizeof(unsigned long long)));
   }
-  launch_tc_impl<D, true>(ctx, e, maskt, Wp, isd, ntp, apart, dprof);
+  launch_tc_impl<D, true>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, dprof);
   if (++nlaunch % 100 == 0) {
     unsigned long long h[kProfSites];
     SF_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
@@ -642,6 +654,7 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
 }  // namespace
 
 bool tc_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
+uint32_t tc_max_table() { return uint32_t(kTabCap); }
 
 // Padded entries / k-step flags / segments / items for the tensor-core path.
 void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
@@ -707,11 +720,11 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
 }
 
 bool launch_fused_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
-                     uint64_t ntp, float* apart) {
+                     const uint16_t* deg16, uint64_t ntp, float* apart) {
   switch (e.dims[1]) {
-    case 128: launch_tc<128>(ctx, e, maskt, Wp, isd, ntp, apart); return true;
-    case 64: launch_tc<64>(ctx, e, maskt, Wp, isd, ntp, apart); return true;
-    case 32: launch_tc<32>(ctx, e, maskt, Wp, isd, ntp, apart); return true;
+    case 128: launch_tc<128>(ctx, e, maskt, Wp, isd, deg16, ntp, apart); return true;
+    case 64: launch_tc<64>(ctx, e, maskt, Wp, isd, deg16, ntp, apart); return true;
+    case 32: launch_tc<32>(ctx, e, maskt, Wp, isd, deg16, ntp, apart); return true;
     default: return false;
   }
 }

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256)
                const uint32_t* __restrict__ row_ptr,
                const uint32_t* __restrict__ ep, const uint32_t* __restrict__ order,
                uint32_t nbig, const float* __restrict__ tab, uint32_t V,
-               float* __restrict__ isd) {
+               float* __restrict__ isd, uint16_t* __restrict__ deg16) {
   const int lane = threadIdx.x & 31;
   const Bfly bfly32(lane);
   const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -91,6 +91,11 @@ __global__ void __launch_bounds__(256)
     float* out = isd + (t * V + u) * kTile;
     out[lane] = __ldg(&tab[clo]);
     out[lane + 32] = __ldg(&tab[chi]);
+    if (deg16) {
+      uint16_t* o16 = deg16 + (t * V + u) * kTile;
+      o16[lane] = uint16_t(min(clo, 0xFFFFu));
+      o16[lane + 32] = uint16_t(min(chi, 0xFFFFu));
+    }
     return;
   }
   const uint32_t j = nbig + (w - big_warps);
@@ -103,6 +108,10 @@ __global__ void __launch_bounds__(256)
       float* out = isd + (uint64_t(t) * V + u) * kTile;
       out[lane] = one;
       out[lane + 32] = one;
+      if (deg16) {
+        deg16[(uint64_t(t) * V + u) * kTile + lane] = 1;
+        deg16[(uint64_t(t) * V + u) * kTile + lane + 32] = 1;
+      }
     }
     return;
   }
@@ -118,8 +127,14 @@ __global__ void __launch_bounds__(256)
     for (uint32_t q = 0; q < per && t0 + q < ntiles; ++q) {
       const uint32_t sh = q << lg;
       float* out = isd + (uint64_t(t0 + q) * V + u) * kTile;
-      out[lane] = __ldg(&tab[1 + __popc((lo >> sh) & fmask)]);
-      out[lane + 32] = __ldg(&tab[1 + __popc((hi >> sh) & fmask)]);
+      const uint32_t dlo = 1 + __popc((lo >> sh) & fmask), dhi = 1 + __popc((hi >> sh) & fmask);
+      out[lane] = __ldg(&tab[dlo]);
+      out[lane + 32] = __ldg(&tab[dhi]);
+      if (deg16) {
+        uint16_t* o16 = deg16 + (uint64_t(t0 + q) * V + u) * kTile;
+        o16[lane] = uint16_t(dlo);
+        o16[lane + 32] = uint16_t(dhi);
+      }
     }
   }
 }
@@ -1109,6 +1124,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     e.isd_nbig = 0;
     while (e.isd_nbig < e.V && rp[order[e.isd_nbig] + 1] - rp[order[e.isd_nbig]] > 32) ++e.isd_nbig;
     e.isd_tab.reserve(maxdeg + 2);
+    e.isd_tab_n = maxdeg + 2;
     isd_table_kernel<<<(maxdeg + 2 + 255) / 256, 256, 0, ctx.stream>>>(e.isd_tab.p, maxdeg + 2);
     SF_LAUNCHED(ctx);
   }
@@ -1139,7 +1155,9 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     return v == nullptr || std::strcmp(v, "0") != 0;
   }();
   const bool want_tc = ctx.fused_kind == 2 || (ctx.fused_kind == 0 && use_tc);
-  e.tc = e.fused && want_tc && tc_width(e.dims[1]);
+  // u16 degree rows + a shared-memory 1/sqrt table feed the tcgen05 kernel:
+  // every degree (+ self loop) must be in the table
+  e.tc = e.fused && want_tc && tc_width(e.dims[1]) && e.isd_tab_n <= tc_max_table();
   if (e.tc) build_tc_plan(ctx, e, sg);
   dt.lap("tc plan");
   e.sg_id = sg.id;
@@ -1172,7 +1190,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   }
   for (int l = first_generic; l + 1 < L; ++l) hmax = std::max(hmax, R[l] * kTile * e.dims[l + 1]);
   for (int l = std::max(1, first_generic); l + 1 < L; ++l) amax = std::max(amax, R[l] * kTile * e.dims[l]);
-  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * 4 + (2 * hmax + amax + apart + afused) * 4;
+  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * (e.tc ? 6 : 4) + (2 * hmax + amax + apart + afused) * 4;
   const uint64_t budget = 96ull << 20;  // keep a batch's intermediates L2-sized
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
@@ -1188,7 +1206,9 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   const uint64_t off_a = off_h1 + T * hmax * 4;
   const uint64_t off_p = off_a + T * amax * 4;
   const uint64_t off_af = off_p + T * apart * 4;
-  ctx.work.reserve(off_af + T * afused * 4 + 256);
+  const uint64_t off_d16 = (off_af + T * afused * 4 + 255) & ~uint64_t(255);
+  const uint64_t d16_bytes = e.tc ? T * uint64_t(e.V) * kTile * 2 : 0;  // u16 degrees (tcgen05 path)
+  ctx.work.reserve(off_d16 + d16_bytes + 256);
   unsigned char* base = ctx.work.p;
   uint64_t* maskt = reinterpret_cast<uint64_t*>(base);
   float* isd = reinterpret_cast<float*>(base + off_isd);
@@ -1196,6 +1216,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   float* abuf = reinterpret_cast<float*>(base + off_a);
   float* pbuf = reinterpret_cast<float*>(base + off_p);
   float* afbuf = reinterpret_cast<float*>(base + off_af);
+  uint16_t* deg16 = e.tc ? reinterpret_cast<uint16_t*>(base + off_d16) : nullptr;
 
   for (uint64_t t0 = 0; t0 < tiles; t0 += T) {
     const uint64_t nt = std::min(T, tiles - t0);
@@ -1207,7 +1228,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       const uint64_t warps = uint64_t(e.isd_nbig) * ntp + (e.V - e.isd_nbig);
       isd_kernel<<<unsigned((warps + 7) / 8), 256, 0, ctx.stream>>>(
           maskt, Wp, uint32_t(ntp), e.row_ptr.p, e.edge_player.p, e.isd_order.p, e.isd_nbig,
-          e.isd_tab.p, e.V, isd);
+          e.isd_tab.p, e.V, isd, deg16);
       SF_LAUNCHED(ctx);
     }
     const float* X = e.p0.p;  // current layer input: P0 (shared) or per-coalition H
@@ -1228,7 +1249,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         ctx.dom_pairs += nrows / 2;
         SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
       }
-      const bool ok = (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, ntp, pbuf)) ||
+      const bool ok = (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
                       (wide && (try_fused_wide<128>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
                                 try_fused_wide<64>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
                                 try_fused_wide<32>(ctx, e, maskt, Wp, isd, ntp, pbuf))) ||

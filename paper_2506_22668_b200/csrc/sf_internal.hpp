@@ -155,6 +155,7 @@ struct Engine {
   DevBuf<uint32_t> isd_order;  // nodes by descending degree (isd_kernel)
   uint32_t isd_nbig = 0;       // nodes with more than 32 incidences
   DevBuf<float> isd_tab;       // inv_sqrt_deg(d), d = 0..maxdeg+1
+  uint32_t isd_tab_n = 0;      // entries in isd_tab
   DevBuf<float> p0;                 // X W_0, V x d_1 (layer-0 transform-first)
   std::vector<std::unique_ptr<DevBuf<float>>> w, b;  // per layer (w[0] unused)
   // Fused layer-0 + layer-1 aggregation plan:
@@ -290,9 +291,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
 
 // sf_fused_tc.cu
 bool tc_width(uint64_t d);
+uint32_t tc_max_table();  // largest 1/sqrt(deg) table the tcgen05 kernel stages
 void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg);
 bool launch_fused_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp,
-                     const float* isd, uint64_t ntp, float* apart);
+                     const float* isd, const uint16_t* deg16, uint64_t ntp, float* apart);
 
 // sf_cgls.cu
 struct CglsResult {
