@@ -69,9 +69,10 @@ int sf_ctx_synchronize(sf_ctx* ctx);
  * SF_KERNEL_AUTO = tcgen05 3xTF32 where the hidden width allows (env
  * SF_FUSED_TC=0 forces SIMT), SF_KERNEL_SIMT = FP32 SIMT kernel,
  * SF_KERNEL_TC = tcgen05 where possible. Takes effect on the next call. */
-enum { SF_KERNEL_AUTO = 0, SF_KERNEL_SIMT = 1, SF_KERNEL_TC = 2 };
+enum { SF_KERNEL_AUTO = 0, SF_KERNEL_SIMT = 1, SF_KERNEL_TC = 2, SF_KERNEL_TC16 = 3 };
 int sf_ctx_set_fused_kernel(sf_ctx* ctx, int kind);
-/* which fused kernel the last prediction used: 0 none, 1 SIMT, 2 tcgen05 */
+/* which fused kernel the last prediction used: 0 none, 1 SIMT, 2 tcgen05
+ * 3xTF32, 3 tcgen05 fp16x2 (SF_KERNEL_TC16: opt-in variant, widths 64/128) */
 int sf_ctx_fused_kernel_used(const sf_ctx* ctx);
 /* Plan of the fused kernel prepared by the last prediction: layer-0 entries
  * gathered per coalition (with the fused recompute), the same padded to the

@@ -462,16 +462,17 @@ class Context:
     def synchronize(self):
         _chk(lib.sf_ctx_synchronize(self.h))
 
-    FUSED_KERNELS = {"auto": 0, "simt": 1, "tc": 2}
+    FUSED_KERNELS = {"auto": 0, "simt": 1, "tc": 2, "tc16": 3}
 
     def set_fused_kernel(self, kind):
         """Select the fused layer-0/1 kernel: "auto" (tcgen05 3xTF32 where
-        the hidden width allows), "simt" (FP32 SIMT) or "tc"."""
+        the hidden width allows), "simt" (FP32 SIMT), "tc" (3xTF32) or "tc16"
+        (tcgen05 fp16x2 variant, widths 64 and 128)."""
         _chk(lib.sf_ctx_set_fused_kernel(self.h, self.FUSED_KERNELS[kind]))
 
     def fused_kernel_used(self):
         """Kernel of the last prediction: None, "simt" or "tc"."""
-        return {0: None, 1: "simt", 2: "tc"}.get(lib.sf_ctx_fused_kernel_used(self.h))
+        return {0: None, 1: "simt", 2: "tc", 3: "tc16"}.get(lib.sf_ctx_fused_kernel_used(self.h))
 
     # ---- sampler
     def philox(self, seed, stream, count):

@@ -32,10 +32,13 @@
 
 #include "sf_device.cuh"
 #include "sf_internal.hpp"
+#include "sf_tcgen05.cuh"
 
 namespace sfb {
 
 namespace {
+
+using namespace tc;
 
 constexpr int kTile = 64;
 constexpr unsigned kFull = 0xffffffffu;
@@ -43,9 +46,8 @@ constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
 constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
-constexpr int kRawStages = 4, kCanStages = 2;
+constexpr int kRawStages = 3, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kTabCap = 12288;    // 1/sqrt(deg) entries in shared memory (larger degrees: SIMT kernel)
 constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 7;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
@@ -61,166 +63,20 @@ struct TcCfg {
   // raw stage (bulk copies): records | P rows | isd rows (2 tiles) | mask blocks (2 tiles)
   static constexpr int RAW_P = 0;
   static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
-  static constexpr int RAW_W = RAW_ISD + kKC * kM * 2;  // u16 degrees
+  static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
   static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
   static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
   static constexpr int OFF_BIAS = OFF_KFL + kMaxKsteps;      // b0 (D floats)
   static constexpr int OFF_BARS = OFF_BIAS + D * 4;
-  static constexpr int OFF_TAB = ((OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16 + 15) / 16) * 16;
-  static constexpr int SMEM = OFF_TAB;  // + the 1/sqrt(deg) table, sized at launch
+  static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
   // TMEM columns: H buffers [0, 2D), accumulator [2D, 3D), A stages (hi 32 | lo 32) from 3D
   static constexpr uint32_t A_COL = 3 * D;
   static constexpr uint32_t TMEM_COLS = 3 * D + kCanStages * 2 * kKC <= 256 ? 256 : 512;
   static_assert(3 * D + kCanStages * 2 * kKC <= 512, "TMEM columns");
   static_assert(D % 32 == 0 && D <= 256, "width");
-  static_assert(SMEM + kTabCap * 4 <= 227 * 1024, "shared memory");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
-
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W_%=;\n\t}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
-}
-// arrives on the barrier once all of this thread's prior cp.async copies land
-__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
-               : "memory");
-}
-// D[tmem] (+)= A[smem] * B[smem], kind::tf32, cta_group::1
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// D[tmem] (+)= A[tmem] * B[smem] (A: lane = row m, column = k; see
-// csrc/tools/tc_ts_probe.cu)
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Warp-converged variants: every lane of the warp executes them, one
-// elected lane issues (keeps the operands warp-uniform, no per-MMA elect loop)
-__device__ __forceinline__ void tc_mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                                uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_elect(uint64_t* b) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(b))
-      : "memory");
-}
-// Shared-memory matrix descriptor, no swizzle (SmemDescriptor, version 1)
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= uint64_t((addr >> 4) & 0x3FFF);
-  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
-  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
-  d |= uint64_t(1) << 46;  // version (Blackwell)
-  return d;                // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
-}
-
-#define TC_LD32(taddr, r)                                                                          \
-  asm volatile(                                                                                    \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
-        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
-        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                         \
-      : "r"(taddr))
-#define TC_ST32(taddr, r)                                                                          \
-  asm volatile(                                                                                    \
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr), \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),      \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), \
-      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),           \
-      "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),           \
-      "r"(r[30]), "r"(r[31])                                                                       \
-      : "memory")
-
-#define TC_LD16(taddr, r)                                                                          \
-  asm volatile(                                                                                    \
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
-      "%15}, [%16];"                                                                               \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
-        "=r"(r[14]), "=r"(r[15])                                                                   \
-      : "r"(taddr))
-#define TC_ST16(taddr, r)                                                                          \
-  asm volatile(                                                                                    \
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
-      "%14,%15,%16};" ::"r"(taddr),                                                                \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),      \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) \
-      : "memory")
-
-// (d0, d1) = (a0 b0 + c0, a1 b1 + c1), one packed FFMA2 (each lane fma.rn)
-__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
-                                      float c0, float c1) {
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-
-__device__ __noinline__ float inv_sqrt_deg_slow(uint32_t d) { return inv_sqrt_deg(d); }
 
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
@@ -248,8 +104,7 @@ constexpr int kProfSites = 16;
 template <int D, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
-                    uint32_t V, const uint16_t* __restrict__ deg16, const float* __restrict__ tab, uint32_t tab_n,
-                    const float* __restrict__ P, const float* __restrict__ bias,
+                    uint32_t V, const float* __restrict__ P, const float* __restrict__ bias,
                     const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
                     const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
@@ -297,8 +152,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < D; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_BIAS)[j] = bias[j];
-  const uint32_t tab_s = tab_n;  // the launch sizes shared memory for the whole table
-  for (uint32_t j = tid; j < tab_s; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_TAB)[j] = tab[j];
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "r"(Cfg::TMEM_COLS));
@@ -336,12 +189,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (J < cnt * (D / 4)) cp_async16(rw + Cfg::RAW_P + (k * D + ng * 4) * 4, P + uint64_t(x) * D + ng * 4);
         }
       if (!PROF || !(exp & 1))
-        for (int J0 = pw_base; J0 < cnt * 2 * 8; J0 += kProdWarps * 32) {  // u16 degree rows, 2 tiles
-          const int J = J0 + lane, k = min(J >> 4, 31), q = (J >> 3) & 1, ug = J & 7;
+        for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
+          const int J = J0 + lane, k = min(J >> 5, 31), q = (J >> 4) & 1, ug = J & 15;
           const uint32_t x = __shfl_sync(kFull, rec.x, k);
-          if (J < cnt * 2 * 8)
-            cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 8) * 2,
-                       deg16 + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 8);
+          if (J < cnt * 2 * 16)
+            cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
+                       isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
         }
       {  // mask words, one u64 per (entry, tile); self -> all ones, pad -> zero
         const int k = pt >> 1, q = pt & 1;
@@ -364,8 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();  // the A stage in TMEM is rewritten after the MMAs that read it
       const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       const float* Ps = reinterpret_cast<const float*>(rw + Cfg::RAW_P);
-      const uint16_t* degs = reinterpret_cast<const uint16_t*>(rw + Cfg::RAW_ISD);
-      const float* stab = reinterpret_cast<const float*>(smem + Cfg::OFF_TAB);
+      const float* isds = reinterpret_cast<const float*>(rw + Cfg::RAW_ISD);
       const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
       unsigned char* st = smem + s * Cfg::STAGE;
       const int cnt = int(min(uint32_t(kKC), e1 - (e0 + c * kKC)));  // multiple of 8
@@ -380,9 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int w = 0; w < 16; ++w) {
             const int k = k0 + w;
-            const uint32_t dg = degs[k * kM + m];
-            const float iv = stab[min(dg, tab_s - 1)];  // the table covers every degree (host check)
-            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? iv : 0.f;
+            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? isds[k * kM + m] : 0.f;
             const float h = tf32_hi(cf);
             hv[w] = __float_as_uint(h);
             lv[w] = __float_as_uint(cf - h);
@@ -605,14 +455,13 @@ void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t W
   static bool configured = false;
   if (!configured) {
     SF_CUDA(cudaFuncSetAttribute(fused_tc_kernel<D, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM + kTabCap * 4));
+                                 Cfg::SMEM));
     configured = true;
   }
-  const size_t smem = Cfg::SMEM + size_t(e.isd_tab_n) * 4;
+  const size_t smem = Cfg::SMEM;
   dim3 grid(e.tc_items, unsigned(ntp / 2));
   fused_tc_kernel<D, PROF><<<grid, kThreads, smem, ctx.stream>>>(
-      maskt, Wp, isd, e.V, deg16, e.isd_tab.p, e.isd_tab_n, e.p0.p, e.b[0]->p,
-      reinterpret_cast<const uint2*>(e.tc_ent.p),
+      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
       e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof,
       PROF ? exp_flags() : 0);
@@ -654,9 +503,9 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
 }  // namespace
 
 bool tc_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
-uint32_t tc_max_table() { return uint32_t(kTabCap); }
 
-// Padded entries / k-step flags / segments / items for the tensor-core path.
+// Padded entries / k-step flags / segments / items for the tensor-core path
+// (segments padded to multiples of e.tc_kstep entries).
 void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   const uint32_t U = uint32_t(e.ball[e.L - 2]);
   constexpr uint64_t kItem = 512;
@@ -675,16 +524,17 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
         open = 0;
       }
     };
+    const uint64_t ks = e.tc_kstep;  // entries per MMA k-step (8 tf32, 16 fp16)
     auto segment = [&](uint32_t v, uint32_t euv) {
       const uint64_t w = sg.row_ptr[v + 1] - sg.row_ptr[v] + 1;
-      const uint64_t padded = (w + 7) / 8 * 8;
+      const uint64_t padded = (w + ks - 1) / ks * ks;
       if (open && open + padded > kItem) close();
       const size_t k0 = ent.size() / 2;
       ent.insert(ent.end(), {v, kSelf});
       for (uint64_t k = sg.row_ptr[v]; k < sg.row_ptr[v + 1]; ++k)
         ent.insert(ent.end(), {sg.col[k], sg.edge_player[k]});
       for (uint64_t k = w; k < padded; ++k) ent.insert(ent.end(), {v, kPad});
-      const size_t nk = padded / 8;
+      const size_t nk = padded / ks;
       for (size_t j = 0; j < nk; ++j) kfl.push_back(uint8_t((j == 0 ? 1 : 0) | (j + 1 == nk ? 2 : 0)));
       (void)k0;
       segs.insert(segs.end(), {v, euv});
@@ -696,7 +546,7 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
     u_items.push_back(uint32_t(item_ent.size() - 1));
   }
   for (size_t it = 0; it + 1 < item_ent.size(); ++it)
-    if ((item_ent[it + 1] - item_ent[it]) / 8 > uint32_t(kMaxKsteps)) {
+    if ((item_ent[it + 1] - item_ent[it]) / e.tc_kstep > uint32_t(kMaxKsteps)) {
       e.tc = false;  // a segment too long for the kernel's flag buffer: SIMT kernel
       return;
     }

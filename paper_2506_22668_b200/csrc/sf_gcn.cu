@@ -1154,11 +1154,22 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     const char* v = std::getenv("SF_FUSED_TC");
     return v == nullptr || std::strcmp(v, "0") != 0;
   }();
-  const bool want_tc = ctx.fused_kind == 2 || (ctx.fused_kind == 0 && use_tc);
-  // u16 degree rows + a shared-memory 1/sqrt table feed the tcgen05 kernel:
-  // every degree (+ self loop) must be in the table
-  e.tc = e.fused && want_tc && tc_width(e.dims[1]) && e.isd_tab_n <= tc_max_table();
+  const bool want_tc = ctx.fused_kind >= 2 || (ctx.fused_kind == 0 && use_tc);
+  e.tc = e.fused && want_tc && tc_width(e.dims[1]);
+  // fp16x2 variant (sf_fused_f16.cu: MN-major B gathered directly, K = 16,
+  // u16 degree rows + a shared 1/sqrt table). Opt-in with SF_FUSED_TC16=1:
+  // on C2 it measured level with 3xTF32 (its 16-entry segment padding adds
+  // ~20% work items and its degree buffer shrinks the batch).
+  static const bool use_tc16 = [] {
+    const char* v = std::getenv("SF_FUSED_TC16");
+    return v != nullptr && std::strcmp(v, "0") != 0;
+  }();
+  const bool want_tc16 = ctx.fused_kind == 3 || (ctx.fused_kind == 0 && use_tc16);
+  e.tc16 = e.tc && want_tc16 && tc16_width(e.dims[1]) && e.isd_tab_n <= tc16_max_table();
+  e.tc_kstep = e.tc16 ? 16 : 8;
   if (e.tc) build_tc_plan(ctx, e, sg);
+  if (e.tc16 && !e.tc) e.tc16 = false;  // the plan may have rejected the tensor-core path
+  if (e.tc16) prepare_tc16(ctx, e);
   dt.lap("tc plan");
   e.sg_id = sg.id;
   e.model_id = m.id;
@@ -1190,7 +1201,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   }
   for (int l = first_generic; l + 1 < L; ++l) hmax = std::max(hmax, R[l] * kTile * e.dims[l + 1]);
   for (int l = std::max(1, first_generic); l + 1 < L; ++l) amax = std::max(amax, R[l] * kTile * e.dims[l]);
-  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * (e.tc ? 6 : 4) + (2 * hmax + amax + apart + afused) * 4;
+  const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * (e.tc16 ? 6 : 4) + (2 * hmax + amax + apart + afused) * 4;
   const uint64_t budget = 96ull << 20;  // keep a batch's intermediates L2-sized
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
@@ -1207,7 +1218,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   const uint64_t off_p = off_a + T * amax * 4;
   const uint64_t off_af = off_p + T * apart * 4;
   const uint64_t off_d16 = (off_af + T * afused * 4 + 255) & ~uint64_t(255);
-  const uint64_t d16_bytes = e.tc ? T * uint64_t(e.V) * kTile * 2 : 0;  // u16 degrees (tcgen05 path)
+  const uint64_t d16_bytes = e.tc16 ? T * uint64_t(e.V) * kTile * 2 : 0;  // u16 degrees (fp16 kernel)
   ctx.work.reserve(off_d16 + d16_bytes + 256);
   unsigned char* base = ctx.work.p;
   uint64_t* maskt = reinterpret_cast<uint64_t*>(base);
@@ -1216,7 +1227,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   float* abuf = reinterpret_cast<float*>(base + off_a);
   float* pbuf = reinterpret_cast<float*>(base + off_p);
   float* afbuf = reinterpret_cast<float*>(base + off_af);
-  uint16_t* deg16 = e.tc ? reinterpret_cast<uint16_t*>(base + off_d16) : nullptr;
+  uint16_t* deg16 = e.tc16 ? reinterpret_cast<uint16_t*>(base + off_d16) : nullptr;
 
   for (uint64_t t0 = 0; t0 < tiles; t0 += T) {
     const uint64_t nt = std::min(T, tiles - t0);
@@ -1249,7 +1260,8 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         ctx.dom_pairs += nrows / 2;
         SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
       }
-      const bool ok = (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
+      const bool ok = (e.tc16 && launch_fused_tc16(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
+                      (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
                       (wide && (try_fused_wide<128>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
                                 try_fused_wide<64>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
                                 try_fused_wide<32>(ctx, e, maskt, Wp, isd, ntp, pbuf))) ||

@@ -799,7 +799,8 @@ uint64_t sf_ctx_launches(const sf_ctx* ctx) { return ctx ? ctx->c.launches : 0; 
 int sf_ctx_set_fused_kernel(sf_ctx* ctx, int kind) {
   return guard([&] {
     need(ctx, "context");
-    if (kind < 0 || kind > 2) throw DataError("fused kernel kind must be 0 (auto), 1 (simt) or 2 (tc)");
+    if (kind < 0 || kind > 3)
+      throw DataError("fused kernel kind must be 0 (auto), 1 (simt), 2 (tc) or 3 (tc16)");
     ctx->c.fused_kind = kind;
   });
 }
@@ -819,7 +820,7 @@ int sf_ctx_fused_plan(const sf_ctx* ctx, uint64_t* entries, uint64_t* padded_ent
 int sf_ctx_fused_kernel_used(const sf_ctx* ctx) {
   if (!ctx) return -1;
   const Engine& e = ctx->c.engine;
-  return e.fused ? (e.tc ? 2 : 1) : 0;
+  return e.fused ? (e.tc16 ? 3 : e.tc ? 2 : 1) : 0;
 }
 
 int sf_ctx_io_bytes(const sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {

@@ -172,6 +172,10 @@ struct Engine {
   bool tc = false;
   uint32_t tc_items = 0;
   uint64_t tc_entries = 0;  // padded entries (K of the per-tile MMA chain)
+  uint32_t tc_kstep = 8;    // entries per MMA k-step: 8 (tf32 kernel), 16 (fp16 kernel)
+  bool tc16 = false;        // fp16x2 kernel (sf_fused_f16.cu) instead of 3xTF32
+  DevBuf<uint16_t> p16;     // P0 split into fp16 hi | lo planes per row, scaled (fp16 kernel)
+  DevBuf<float> p16_scale;  // [0] P0 scale (power of two), [1] its inverse
   DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items, tc_const;
   DevBuf<uint8_t> tc_kflags;
 };
@@ -291,7 +295,13 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
 
 // sf_fused_tc.cu
 bool tc_width(uint64_t d);
-uint32_t tc_max_table();  // largest 1/sqrt(deg) table the tcgen05 kernel stages
+
+// sf_fused_f16.cu
+bool tc16_width(uint64_t d);
+uint32_t tc16_max_table();  // largest 1/sqrt(deg) table the fp16 kernel stages
+void prepare_tc16(Ctx& ctx, Engine& e);  // P0 -> scaled fp16 hi/lo planes
+bool launch_fused_tc16(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp,
+                       const float* isd, const uint16_t* deg16, uint64_t ntp, float* apart);
 void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg);
 bool launch_fused_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp,
                      const float* isd, const uint16_t* deg16, uint64_t ntp, float* apart);

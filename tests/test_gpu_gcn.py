@@ -12,18 +12,20 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-5  # BASELINE north_star: predictions within 1e-5 relative
 
 
-@pytest.fixture(params=["simt", "tc"])
+@pytest.fixture(params=["simt", "tc", "tc16"])
 def kernel(request, ctx):
-    """Run a parity case on both fused layer-0/1 kernels (FP32 SIMT and
-    tcgen05 3xTF32); the context goes back to "auto" afterwards."""
+    """Run a parity case on every fused layer-0/1 kernel (FP32 SIMT, tcgen05
+    3xTF32, tcgen05 fp16x2); the context goes back to "auto" afterwards."""
     ctx.set_fused_kernel(request.param)
     yield request.param
     ctx.set_fused_kernel("auto")
 
 
 def _check_kernel(ctx, kernel, hidden):
-    if len(hidden) >= 1 and hidden[0] in (32, 64, 128):
+    if len(hidden) >= 1 and hidden[0] in (64, 128):
         assert ctx.fused_kernel_used() == kernel
+    elif len(hidden) >= 1 and hidden[0] == 32:
+        assert ctx.fused_kernel_used() == ("tc" if kernel == "tc16" else kernel)
     elif len(hidden) >= 1 and hidden[0] in (16, 256):
         assert ctx.fused_kernel_used() == "simt"
 
