@@ -815,6 +815,21 @@ __global__ void last_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
 
 constexpr int kTailThreads = 512;
 
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+// d += a (16x8, row) * b (8x8, col), tf32 in, f32 accumulate
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 // ---------------------------------------------------------------- fused tail
 // Everything after the fused layer-0/1 kernel, for one tile t and cpb
 // coalitions per CTA, in shared memory (replaces reduce_partials + sgemm +
@@ -838,9 +853,11 @@ __global__ void __launch_bounds__(kTailThreads, 2)
                 float* __restrict__ out, float* __restrict__ allprobs) {
   extern __shared__ float4 sm4[];
   const uint32_t R = U * cpb, K4 = K / 4;
-  float4* sA = sm4;                                    // [R][K4]
-  float* sW1 = reinterpret_cast<float*>(sA + R * K4);  // [K][N]
-  float* sW2 = sW1 + K * N;                            // [N][C] (three_layer)
+  // padded row strides (floats): conflict-free mma.sync fragment loads
+  const uint32_t SA = K + 4, SA4 = SA / 4, SW = (N % 4 == 0) ? N + 8 : N;
+  float4* sA = sm4;                                    // [R][SA]
+  float* sW1 = reinterpret_cast<float*>(sA + R * SA4); // [K][SW]
+  float* sW2 = sW1 + K * SW;                           // [N][C] (three_layer)
   float* sH = sW2 + (three_layer ? N * C : 0);         // [R][N]
   float* sa = sH + R * N;                              // [cpb][N]
   float* sz = sa + cpb * N;                            // [cpb][C]
@@ -850,10 +867,18 @@ __global__ void __launch_bounds__(kTailThreads, 2)
   const int tid = threadIdx.x;
   {  // weights -> shared memory with cp.async, overlapped with the partial sums below
     const uint32_t n1 = K * N / 4;
-    for (uint32_t idx = tid; idx < n1; idx += blockDim.x)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(sW1 + 4 * idx))),
-                   "l"(W1 + 4 * idx) : "memory");
+    if (SW != N) {  // padded rows
+      const uint32_t rq = N / 4;
+      for (uint32_t idx = tid; idx < n1; idx += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(sW1 + (idx / rq) * SW + 4 * (idx % rq)))),
+                     "l"(W1 + 4 * idx) : "memory");
+    } else {  // K * N is a multiple of 4 (K is)
+      for (uint32_t idx = tid; idx < n1; idx += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(sW1 + 4 * idx))),
+                     "l"(W1 + 4 * idx) : "memory");
+    }
     if (three_layer) {
       const uint32_t n2 = N * C / 4;
       for (uint32_t idx = tid; idx < n2; idx += blockDim.x)
@@ -892,11 +917,56 @@ __global__ void __launch_bounds__(kTailThreads, 2)
       s.w += p.w;
     }
     const float sc = isd_t[uint64_t(u) * kTile + i];
-    sA[idx] = make_float4(sc * s.x, sc * s.y, sc * s.z, sc * s.w);
+    sA[r * SA4 + k4] = make_float4(sc * s.x, sc * s.y, sc * s.z, sc * s.w);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // H = act(A W1 + b1): thread = (column n, row group of up to kRB rows),
+  // H = act(A W1 + b1)
+  if (N % 16 == 0 && K % 8 == 0) {
+    // warp tensor-core MMAs (mma.sync m16n8k8 tf32, 3xTF32 split in
+    // registers: FP32-level products); warp job = 16 rows x 16 columns
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+    const float* Af = reinterpret_cast<const float*>(sA);
+    const uint32_t mtiles = (R + 15) / 16, npairs = N / 16;
+    for (uint32_t job = warp; job < mtiles * npairs; job += blockDim.x / 32) {
+      const uint32_t m0 = (job / npairs) * 16, n0 = (job % npairs) * 16;
+      const uint32_t r0 = m0 + g, r1 = m0 + g + 8;
+      float d[2][4] = {};
+      for (uint32_t k0 = 0; k0 < K; k0 += 8) {
+        const float af[4] = {r0 < R ? Af[r0 * SA + k0 + tq] : 0.f, r1 < R ? Af[r1 * SA + k0 + tq] : 0.f,
+                             r0 < R ? Af[r0 * SA + k0 + tq + 4] : 0.f, r1 < R ? Af[r1 * SA + k0 + tq + 4] : 0.f};
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tf32_split(af[q], ah[q], al[q]);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const uint32_t n = n0 + nt * 8 + g;
+          uint32_t bh[2], bl[2];
+          tf32_split(sW1[(k0 + tq) * SW + n], bh[0], bl[0]);
+          tf32_split(sW1[(k0 + tq + 4) * SW + n], bh[1], bl[1]);
+          mma_tf32(d[nt], ah, bh);
+          mma_tf32(d[nt], ah, bl);
+          mma_tf32(d[nt], al, bh);
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const uint32_t c0 = n0 + nt * 8 + 2 * tq;
+        const float bb0 = b1[c0], bb1 = b1[c0 + 1];
+        if (r0 < R) {
+          const float v0 = d[nt][0] + bb0, v1 = d[nt][1] + bb1;
+          sH[r0 * N + c0] = three_layer ? fmaxf(v0, 0.f) : v0;
+          sH[r0 * N + c0 + 1] = three_layer ? fmaxf(v1, 0.f) : v1;
+        }
+        if (r1 < R) {
+          const float v2 = d[nt][2] + bb0, v3 = d[nt][3] + bb1;
+          sH[r1 * N + c0] = three_layer ? fmaxf(v2, 0.f) : v2;
+          sH[r1 * N + c0 + 1] = three_layer ? fmaxf(v3, 0.f) : v3;
+        }
+      }
+    }
+  } else {
+  // SIMT: thread = (column n, row group of up to kRB rows)
   // one job per thread when N * ceil(R / kRB) <= blockDim.x
   constexpr uint32_t kRB = 8;
   const uint32_t rgroups = max(1u, min(R, blockDim.x / N));
@@ -909,12 +979,12 @@ __global__ void __launch_bounds__(kTailThreads, 2)
 #pragma unroll
       for (uint32_t j = 0; j < kRB; ++j) acc[j] = 0.f;
       for (uint32_t k4 = 0; k4 < K4; ++k4) {
-        const float w0 = sW1[(4 * k4) * N + n], w1 = sW1[(4 * k4 + 1) * N + n];
-        const float w2 = sW1[(4 * k4 + 2) * N + n], w3 = sW1[(4 * k4 + 3) * N + n];
+        const float w0 = sW1[(4 * k4) * SW + n], w1 = sW1[(4 * k4 + 1) * SW + n];
+        const float w2 = sW1[(4 * k4 + 2) * SW + n], w3 = sW1[(4 * k4 + 3) * SW + n];
 #pragma unroll
         for (uint32_t j = 0; j < kRB; ++j) {
           if (j < nr) {
-            const float4 a = sA[(rb0 + j) * K4 + k4];
+            const float4 a = sA[(rb0 + j) * SA4 + k4];
             acc[j] = fmaf(a.x, w0, acc[j]);
             acc[j] = fmaf(a.y, w1, acc[j]);
             acc[j] = fmaf(a.z, w2, acc[j]);
@@ -931,6 +1001,7 @@ __global__ void __launch_bounds__(kTailThreads, 2)
         }
       }
     }
+  }
   }
   __syncthreads();
   if (three_layer) {
@@ -976,7 +1047,7 @@ __global__ void __launch_bounds__(kTailThreads, 2)
 }
 
 size_t tail_smem(uint32_t U, uint32_t K, uint32_t N, uint32_t C, uint32_t cpb, bool three_layer) {
-  return (size_t(U) * cpb * (K + N) + size_t(cpb) * (N + C) + size_t(K) * N +
+  return (size_t(U) * cpb * (K + 4 + N) + size_t(cpb) * (N + C) + size_t(K) * (N + 8) +
           (three_layer ? size_t(N) * C : 0)) * 4;
 }
 
