@@ -92,7 +92,8 @@ __device__ void floyd_warp(const Set& set, uint32_t n, uint32_t s,
     const uint32_t mm0 = m0 + i0, mm1 = m0 + i1;
     const uint32_t t0 = v0 ? mod_u64_u32(x0, mm0 + 1) : 0xffffffffu;
     const uint32_t t1 = v1 ? mod_u64_u32(x1, mm1 + 1) : 0xffffffffu;
-    __syncwarp();
+    // (the set is ordered for this chunk by the previous chunk's trailing
+    // __syncwarp, or by the caller's before the first chunk)
     bool hit0 = v0 && set.test(t0);
     bool hit1 = v1 && set.test(t1);
     __syncwarp();
