@@ -465,18 +465,14 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     reduce_stage2<<<1, kRedBlocks, 0, st>>>(red, kRedBlocks, out);
     SF_LAUNCHED(ctx);
   };
-  double* host = nullptr;
-  SF_CUDA(cudaMallocHost(&host, 16 * sizeof(double)));
+  ctx.solver_host.reserve(16);
+  double* host = ctx.solver_host.p;
   auto fetch = [&](int idx, int count) {
     ctx.d2h_bytes += uint64_t(count) * sizeof(double);
     SF_CUDA(cudaMemcpyAsync(host + idx, scal + idx, count * sizeof(double),
                             cudaMemcpyDeviceToHost, st));
     SF_CUDA(cudaStreamSynchronize(st));
   };
-  struct HostFree {
-    double* p;
-    ~HostFree() { cudaFreeHost(p); }
-  } host_guard{host};
 
   launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, 2ull * W);
   if (pairs) {

@@ -1200,22 +1200,23 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     SF_LAUNCHED(ctx);
   }
   // P0 = X W0 on the device
-  DevBuf<float> x, w0;
+  DevBuf<float>& x = ctx.feat_dev;
+  DevBuf<float>& w0 = ctx.w0_dev;
   x.upload(sg.features.data(), sg.features.size(), ctx.stream);
   w0.upload(m.layers[0].weight.data(), m.layers[0].weight.size(), ctx.stream);
   e.p0.reserve(uint64_t(e.V) * e.dims[1]);
   gemm(ctx, x.p, w0.p, nullptr, e.p0.p, e.V, uint32_t(e.dims[1]), uint32_t(e.dims[0]), false);
-  e.w.clear();
-  e.b.clear();
-  for (int l = 0; l < e.L; ++l) {
+  while (int(e.w.size()) < e.L) {  // buffers are kept (and grown) across targets
     e.w.emplace_back(new DevBuf<float>);
     e.b.emplace_back(new DevBuf<float>);
+  }
+  for (int l = 0; l < e.L; ++l) {
     if (l > 0) e.w[l]->upload(m.layers[l].weight.data(), m.layers[l].weight.size(), ctx.stream);
     e.b[l]->upload(m.layers[l].bias.data(), m.layers[l].bias.size(), ctx.stream);
   }
   ctx.h2d_bytes += (rp.size() + sg.col.size() + sg.edge_player.size()) * 4 + sg.features.size() * 4;
   for (const Layer& l : m.layers) ctx.h2d_bytes += (l.weight.size() + l.bias.size()) * 4;
-  SF_CUDA(cudaStreamSynchronize(ctx.stream));  // temporaries x, w0 die here
+  SF_CUDA(cudaStreamSynchronize(ctx.stream));  // host sources of the uploads may go now
   dt.lap("p0 gemm + weights");
   e.fused = e.L >= 2 && fused_width(e.dims[1]) && e.n > 0;
   if (e.fused) build_fused_plan(ctx, e, sg);

@@ -482,9 +482,10 @@ static FidelityOut fidelity(Ctx& ctx, const Subgraph& sg, const Model& m, uint32
   ctx.h2d_bytes += rows * W * 8;
   const uint64_t jobs = streams.size();
   if (jobs) {
-    DevBuf<uint64_t> d_streams, d_rows;
-    DevBuf<uint32_t> d_sizes;
-    DevBuf<uint8_t> d_inv;
+    DevBuf<uint64_t>& d_streams = ctx.fid_streams;
+    DevBuf<uint64_t>& d_rows = ctx.fid_rows;
+    DevBuf<uint32_t>& d_sizes = ctx.fid_sizes;
+    DevBuf<uint8_t>& d_inv = ctx.fid_inv;
     d_streams.upload(streams.data(), jobs, ctx.stream);
     d_sizes.upload(sizes.data(), jobs, ctx.stream);
     d_inv.upload(invert.data(), jobs, ctx.stream);
@@ -617,8 +618,10 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
 
     t_stage = Clock::now();
     const std::vector<double> wsize = weight_of_size(n, global_rows_of_size(plan));
-    DevBuf<double> d_wsize, d_sw, d_tgt;
-    DevBuf<int> d_bad;
+    DevBuf<double>& d_wsize = ctx.wsize_dev;
+    DevBuf<double>& d_sw = ctx.sw_dev;
+    DevBuf<double>& d_tgt = ctx.tgt_dev;
+    DevBuf<int>& d_bad = ctx.bad_dev;
     d_wsize.upload(wsize.data(), wsize.size(), ctx.stream);
     d_sw.reserve(std::max<uint64_t>(rows, 1));
     d_tgt.reserve(std::max<uint64_t>(rows, 1));

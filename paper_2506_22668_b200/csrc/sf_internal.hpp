@@ -234,6 +234,14 @@ struct Ctx {
   DevBuf<uint32_t> plan_dev32;
   cudaEvent_t plan_ready = nullptr;
   DevBuf<double> barrier_buf;
+  // per-call scratch kept across calls (no allocation on the explain path)
+  DevBuf<double> wsize_dev, sw_dev, tgt_dev;
+  DevBuf<int> bad_dev;
+  PinnedBuf<double> solver_host;  // CGLS scalars fetched by the host loop
+  DevBuf<float> feat_dev, w0_dev; // engine_prepare temporaries (X, W0 for P0 = X W0)
+  DevBuf<uint64_t> fid_streams, fid_rows;  // fidelity random-baseline jobs
+  DevBuf<uint32_t> fid_sizes;
+  DevBuf<uint8_t> fid_inv;
   Ctx();
   ~Ctx();
 };
