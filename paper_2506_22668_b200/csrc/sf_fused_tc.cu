@@ -46,11 +46,12 @@ constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
 constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
-constexpr int kRawStages = 3, kCanStages = 2;
+constexpr int kRawStages = 4, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 7;
+constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 6;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
-constexpr int kThreads = (kMmaWarp + 1) * 32;
+constexpr int kBLoadWarp = kMmaWarp + 1;  // one warp, one lane: B tiles from the B bank
+constexpr int kThreads = (kBLoadWarp + 1) * 32;
 
 template <int D>
 struct TcCfg {
@@ -60,16 +61,16 @@ struct TcCfg {
   static constexpr int OFF_BHI = 0;
   static constexpr int OFF_BLO = B_BYTES;
   static constexpr int STAGE = ((2 * B_BYTES + 1023) / 1024) * 1024;
-  // raw stage (bulk copies): records | P rows | isd rows (2 tiles) | mask blocks (2 tiles)
-  static constexpr int RAW_P = 0;
-  static constexpr int RAW_ISD = RAW_P + kKC * D * 4;
+  // raw stage: isd rows (2 tiles) | mask words (2 tiles); B tiles come
+  // pre-transposed from the B bank straight into the stage
+  static constexpr int RAW_ISD = 0;
   static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
   static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
   static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
   static constexpr int OFF_BIAS = OFF_KFL + kMaxKsteps;      // b0 (D floats)
   static constexpr int OFF_BARS = OFF_BIAS + D * 4;
-  static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 2 * kCanStages + 4) + 16;
+  static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 3 * kCanStages + 4) + 16;
   // TMEM columns: H buffers [0, 2D), accumulator [2D, 3D), A stages (hi 32 | lo 32) from 3D
   static constexpr uint32_t A_COL = 3 * D;
   static constexpr uint32_t TMEM_COLS = 3 * D + kCanStages * 2 * kKC <= 256 ? 256 : 512;
@@ -104,7 +105,8 @@ constexpr int kProfSites = 16;
 template <int D, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
-                    uint32_t V, const float* __restrict__ P, const float* __restrict__ bias,
+                    uint32_t V, const float* __restrict__ bbank, const uint32_t* __restrict__ item_chunk,
+                    const float* __restrict__ bias,
                     const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
                     const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
@@ -129,7 +131,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* can_empty = can_full + kCanStages;  // MMA commit -> staging
   uint64_t* hfull = can_empty + kCanStages;     // MMA commit -> epilogue
   uint64_t* hfree = hfull + 2;                  // epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
+  uint64_t* b_full = hfree + 2;                 // B loader (bulk copy, expect_tx) -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + kCanStages);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t item = item_order[blockIdx.x];
   const uint64_t t0 = uint64_t(blockIdx.y) * 2;  // tiles t0, t0+1
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kCanStages; ++s) {
       mbar_init(&can_full[s], kStgWarps);
       mbar_init(&can_empty[s], 1);
+      mbar_init(&b_full[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
@@ -182,12 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       // trip counts are warp-uniform (J0 steps by whole warps), so every lane
       // takes part in the shuffles
-      if (!PROF || !(exp & 2))
-        for (int J0 = pw_base; J0 < cnt * (D / 4); J0 += kProdWarps * 32) {  // P rows
-          const int J = J0 + lane, k = min(J / (D / 4), 31), ng = J % (D / 4);
-          const uint32_t x = __shfl_sync(kFull, rec.x, k);
-          if (J < cnt * (D / 4)) cp_async16(rw + Cfg::RAW_P + (k * D + ng * 4) * 4, P + uint64_t(x) * D + ng * 4);
-        }
       if (!PROF || !(exp & 1))
         for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
           const int J = J0 + lane, k = min(J >> 5, 31), q = (J >> 4) & 1, ug = J & 15;
@@ -216,7 +214,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (c >= uint32_t(kCanStages)) TC_WAIT(1, &can_empty[s], ((c / kCanStages) - 1) & 1);
       tc_fence_after();  // the A stage in TMEM is rewritten after the MMAs that read it
       const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
-      const float* Ps = reinterpret_cast<const float*>(rw + Cfg::RAW_P);
       const float* isds = reinterpret_cast<const float*>(rw + Cfg::RAW_ISD);
       const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
       unsigned char* st = smem + s * Cfg::STAGE;
@@ -242,21 +239,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           TC_ST16(ta + kKC, lv);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-      }
-      // B: gathered P rows transposed to K-major, unit (feature n, 4 entries), hi/lo split
-      for (int J = st_tid; J < ((PROF && (exp & 4)) ? 0 : D * (cnt / 4)); J += kStgWarps * 32) {
-        const int n = J % D, u = J / D;
-        const float p0 = Ps[(4 * u) * D + n], p1 = Ps[(4 * u + 1) * D + n];
-        const float p2 = Ps[(4 * u + 2) * D + n], p3 = Ps[(4 * u + 3) * D + n];
-        float4 hi;
-        hi.x = tf32_hi(p0);
-        hi.y = tf32_hi(p1);
-        hi.z = tf32_hi(p2);
-        hi.w = tf32_hi(p3);
-        const float4 lo = make_float4(p0 - hi.x, p1 - hi.y, p2 - hi.z, p3 - hi.w);
-        const uint32_t off = u * Cfg::B_LBO + (n >> 3) * 128 + (n & 7) * 16;
-        *reinterpret_cast<float4*>(st + Cfg::OFF_BHI + off) = hi;
-        *reinterpret_cast<float4*>(st + Cfg::OFF_BLO + off) = lo;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
@@ -294,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t c = 0; c < nchunks; ++c) {
         const int s = c % kCanStages;
         TC_WAIT(0, &can_full[s], (c / kCanStages) & 1);
+        mbar_wait(&b_full[s], (c / kCanStages) & 1);
         tc_fence_after();
         const int nk = int(min(uint32_t(kKC), e1 - (e0 + c * kKC))) / 8;
         const uint32_t fw = sfl32[c];
@@ -327,6 +310,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit_elect(&can_empty[s]);
       }
       prof_flush(6, 2);  // 6 wait can_full, 7 wait hfree, 8 total
+    }
+  } else if (warp == kBLoadWarp) {
+    // ------------------------------------------------------------ B loader
+    // The chunk's B operand (P0 rows of its entries, K-major, tf32 hi | lo)
+    // is the same for every tile pair: one bulk copy from the B bank.
+    if (lane == 0) {
+      const float* src = bbank + uint64_t(item_chunk[item]) * (2 * Cfg::B_BYTES / 4);
+      for (uint32_t c = 0; c < nchunks; ++c) {
+        const int s = c % kCanStages;
+        if (c >= uint32_t(kCanStages)) mbar_wait(&can_empty[s], ((c / kCanStages) - 1) & 1);
+        mbar_arrive_expect_tx(&b_full[s], 2 * Cfg::B_BYTES);
+        bulk_g2s(smem + s * Cfg::STAGE, src + uint64_t(c) * (2 * Cfg::B_BYTES / 4), 2 * Cfg::B_BYTES, &b_full[s]);
+      }
     }
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
@@ -448,6 +444,37 @@ int exp_flags() {
   return f;
 }
 
+// B bank: for every chunk of every item, the K-major tf32 hi | lo B tile of
+// the chunk's P0 rows (entries past the chunk end are zero). One CTA per
+// chunk; thread = (feature n, 4 entries), the same layout the staging warps
+// used to build per tile pair.
+template <int D>
+__global__ void __launch_bounds__(256)
+    build_bbank_kernel(const float* __restrict__ P, const uint2* __restrict__ ent,
+                       const uint32_t* __restrict__ chunk_ent, float* __restrict__ bank) {
+  using Cfg = TcCfg<D>;
+  const uint32_t ci = blockIdx.x, base = chunk_ent[2 * ci], cnt = chunk_ent[2 * ci + 1];
+  unsigned char* out = reinterpret_cast<unsigned char*>(bank + uint64_t(ci) * (2 * Cfg::B_BYTES / 4));
+  for (int J = threadIdx.x; J < D * (kKC / 4); J += blockDim.x) {
+    const int n = J % D, u = J / D;
+    float pv[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t k = 4 * u + w;
+      pv[w] = k < cnt ? __ldg(&P[uint64_t(ent[base + k].x) * D + n]) : 0.f;
+    }
+    float4 hi;
+    hi.x = tf32_hi(pv[0]);
+    hi.y = tf32_hi(pv[1]);
+    hi.z = tf32_hi(pv[2]);
+    hi.w = tf32_hi(pv[3]);
+    const float4 lo = make_float4(pv[0] - hi.x, pv[1] - hi.y, pv[2] - hi.z, pv[3] - hi.w);
+    const uint32_t off = u * Cfg::B_LBO + (n >> 3) * 128 + (n & 7) * 16;
+    *reinterpret_cast<float4*>(out + Cfg::OFF_BHI + off) = hi;
+    *reinterpret_cast<float4*>(out + Cfg::OFF_BLO + off) = lo;
+  }
+}
+
 template <int D, bool PROF>
 void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
                     const uint16_t* deg16, uint64_t ntp, float* apart, unsigned long long* prof) {
@@ -461,7 +488,7 @@ void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t W
   const size_t smem = Cfg::SMEM;
   dim3 grid(e.tc_items, unsigned(ntp / 2));
   fused_tc_kernel<D, PROF><<<grid, kThreads, smem, ctx.stream>>>(
-      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
+      maskt, Wp, isd, e.V, e.tc_bbank.p, e.tc_item_chunk.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
       e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof,
       PROF ? exp_flags() : 0);
@@ -570,6 +597,32 @@ void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   e.tc_u_items.upload(u_items.data(), u_items.size(), ctx.stream);
   ctx.h2d_bytes += ent.size() * 4 + kfl.size() + segs.size() * 4 +
                    (item_ent.size() + item_seg.size() + order.size() + u_items.size()) * 4;
+  if (!e.tc16) {  // B bank for the 3xTF32 kernel: one pre-transposed B tile per chunk
+    std::vector<uint32_t> item_chunk(work.size()), chunk_ent;
+    uint32_t nch = 0;
+    for (size_t it = 0; it + 1 < item_ent.size(); ++it) {
+      item_chunk[it] = nch;
+      for (uint32_t b0 = item_ent[it]; b0 < item_ent[it + 1]; b0 += kKC) {
+        chunk_ent.push_back(b0);
+        chunk_ent.push_back(std::min<uint32_t>(kKC, item_ent[it + 1] - b0));
+        ++nch;
+      }
+    }
+    e.tc_item_chunk.upload(item_chunk.data(), item_chunk.size(), ctx.stream);
+    e.tc_chunk_ent.upload(chunk_ent.data(), chunk_ent.size(), ctx.stream);
+    ctx.h2d_bytes += (item_chunk.size() + chunk_ent.size()) * 4;
+    const uint32_t D = uint32_t(e.dims[1]);
+    e.tc_bbank.reserve(uint64_t(nch) * 2 * D * kKC);
+    if (nch) {
+      switch (D) {
+        case 128: build_bbank_kernel<128><<<nch, 256, 0, ctx.stream>>>(e.p0.p, reinterpret_cast<const uint2*>(e.tc_ent.p), e.tc_chunk_ent.p, e.tc_bbank.p); break;
+        case 64: build_bbank_kernel<64><<<nch, 256, 0, ctx.stream>>>(e.p0.p, reinterpret_cast<const uint2*>(e.tc_ent.p), e.tc_chunk_ent.p, e.tc_bbank.p); break;
+        case 32: build_bbank_kernel<32><<<nch, 256, 0, ctx.stream>>>(e.p0.p, reinterpret_cast<const uint2*>(e.tc_ent.p), e.tc_chunk_ent.p, e.tc_bbank.p); break;
+        default: throw std::logic_error("B bank width");
+      }
+      SF_LAUNCHED(ctx);
+    }
+  }
   SF_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 

@@ -173,6 +173,9 @@ struct Engine {
   uint32_t tc_items = 0;
   uint64_t tc_entries = 0;  // padded entries (K of the per-tile MMA chain)
   uint32_t tc_kstep = 8;    // entries per MMA k-step: 8 (tf32 kernel), 16 (fp16 kernel)
+  DevBuf<float> tc_bbank;          // per chunk: K-major tf32 hi | lo B tile (3xTF32 kernel)
+  DevBuf<uint32_t> tc_item_chunk;  // first B-bank chunk of each item
+  DevBuf<uint32_t> tc_chunk_ent;   // per chunk: first entry, entry count
   bool tc16 = false;        // fp16x2 kernel (sf_fused_f16.cu) instead of 3xTF32
   DevBuf<uint16_t> p16;     // P0 split into fp16 hi | lo planes per row, scaled (fp16 kernel)
   DevBuf<float> p16_scale;  // [0] P0 scale (power of two), [1] its inverse
