@@ -373,210 +373,6 @@ __global__ void __launch_bounds__(kConsumers + 32) __maxnreg__(D >= 256 ? 224 : 
     reinterpret_cast<float4*>(out + uint64_t(cg * Cfg::CB + j) * D)[fg] = acc[j];
 }
 
-// Wide variant for D in {32, 64, 128}: two tiles (128 coalitions) per CTA,
-// each consumer thread owns 8 features of CB coalitions (64 FFMA per entry
-// for D = 128), so every staged P row serves 128 coalitions and the FMA
-// density per issued instruction doubles. The per-u accumulators live in
-// shared memory (thread-strided, conflict-free) and are touched only at
-// segment ends; the open segment's partial sums stay in registers.
-template <int D>
-struct WideCfg {
-  static constexpr int TPC = 2;                  // tiles per CTA
-  static constexpr int CO = kTile * TPC;          // coalitions per CTA
-  static constexpr int FG = D / 8;                // threads per feature row
-  static constexpr int CGS = kConsumers / FG;     // coalition groups
-  static constexpr int CB = CO / CGS;             // coalitions per thread
-  static constexpr int STAGES = 3;
-  static constexpr int OFF_P = kChunkEntries * 16;
-  static constexpr int OFF_ISD = OFF_P + kChunkEntries * D * 4;
-  static constexpr int OFF_W = OFF_ISD + kChunkEntries * CO * 4;
-  static constexpr int OFF_COEF = OFF_W + kChunkEntries * TPC * 32;
-  static constexpr int OFF_FLAGS = OFF_COEF + kChunkEntries * CO * 4;
-  static constexpr int STAGE_BYTES = OFF_FLAGS + 16;
-  static constexpr int ACC_BYTES = kConsumers * CB * 8 * 4;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + ACC_BYTES + 2 * STAGES * 8;
-  static_assert(D % 8 == 0 && FG <= 32 && CO % CGS == 0 && CB >= 1, "shape");
-  static_assert(SMEM <= 227 * 1024, "shared memory");
-};
-
-template <int D>
-__global__ void __launch_bounds__(kConsumers + 32, 1)
-    fused_wide_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
-                      const float* __restrict__ isd, uint32_t V,
-                      const float* __restrict__ P, const float* __restrict__ bias,
-                      const uint4* __restrict__ ent, const uint32_t* __restrict__ item_ent,
-                      const uint32_t* __restrict__ item_order, uint32_t items,
-                      float* __restrict__ Apart) {
-  using Cfg = WideCfg<D>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  float* accs = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::ACC_BYTES);
-  uint64_t* empty = full + Cfg::STAGES;
-  const uint32_t item = item_order[blockIdx.x];
-  const uint64_t t = uint64_t(blockIdx.y) * Cfg::TPC;  // first tile of the pair
-  const int tid = threadIdx.x;
-  const uint32_t e0 = item_ent[item], e1 = item_ent[item + 1];
-  const uint32_t nchunks = (e1 - e0 + kChunkEntries - 1) / kChunkEntries;
-  if (tid == 0) {
-    for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = tid; i < kConsumers * Cfg::CB * 8; i += blockDim.x) accs[i] = 0.f;
-  __syncthreads();
-
-  if (tid >= kConsumers) {
-    // ------------------------------------------------------------ producer
-    const int lane = tid - kConsumers;
-    uint4 rec_next = make_uint4(0, kSelf, kSelf, 0);
-    if (e0 + lane < e1) rec_next = ent[e0 + lane];
-    for (uint32_t c = 0; c < nchunks; ++c) {
-      const int s = c % Cfg::STAGES;
-      unsigned char* st = smem + s * Cfg::STAGE_BYTES;
-      const uint32_t base = e0 + c * kChunkEntries;
-      const bool on = base + lane < e1;
-      const uint4 rec = on ? rec_next : make_uint4(0, kSelf, kSelf, 0);
-      // prefetch the next chunk's records before waiting for a free stage
-      if (base + kChunkEntries + lane < e1) rec_next = ent[base + kChunkEntries + lane];
-      if (c >= uint32_t(Cfg::STAGES)) mbar_wait(&empty[s], ((c / Cfg::STAGES) - 1) & 1);
-      uint32_t bytes = 0;
-      if (on) {
-        bytes = D * 4 + Cfg::TPC * (kTile * 4 + (rec.y != kSelf ? 16 : 0) + (rec.z != kSelf ? 16 : 0));
-        reinterpret_cast<uint4*>(st)[lane] = rec;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
-      const uint32_t startm = __ballot_sync(kFull, on && (rec.w & 1u));
-      const uint32_t endm = __ballot_sync(kFull, on && (rec.w & 2u));
-      if (lane == 0) {
-        reinterpret_cast<uint32_t*>(st + Cfg::OFF_FLAGS)[0] = startm;
-        reinterpret_cast<uint32_t*>(st + Cfg::OFF_FLAGS)[1] = endm;
-        mbar_arrive_expect_tx(&full[s], bytes);
-      }
-      __syncwarp();
-      if (on) {
-        bulk_g2s(st + Cfg::OFF_P + lane * D * 4, P + uint64_t(rec.x) * D, D * 4, &full[s]);
-#pragma unroll
-        for (int q = 0; q < Cfg::TPC; ++q) {
-          const uint64_t* mt = maskt + (t + q) * Wp;
-          const float* isd_t = isd + (t + q) * uint64_t(V) * kTile;
-          bulk_g2s(st + Cfg::OFF_ISD + (lane * Cfg::CO + q * kTile) * 4, isd_t + uint64_t(rec.x) * kTile,
-                   kTile * 4, &full[s]);
-          if (rec.y != kSelf)
-            bulk_g2s(st + Cfg::OFF_W + (lane * Cfg::TPC + q) * 32, mt + (rec.y & ~1u), 16, &full[s]);
-          if (rec.z != kSelf)
-            bulk_g2s(st + Cfg::OFF_W + (lane * Cfg::TPC + q) * 32 + 16, mt + (rec.z & ~1u), 16, &full[s]);
-        }
-      }
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumers
-  const int fg = tid % Cfg::FG, cg = tid / Cfg::FG;
-  const int c0i = cg * Cfg::CB;  // first coalition of this thread (0..127)
-  const float4 bv0 = reinterpret_cast<const float4*>(bias)[2 * fg];
-  const float4 bv1 = reinterpret_cast<const float4*>(bias)[2 * fg + 1];
-  float4 h0[Cfg::CB], h1[Cfg::CB];
-  float sv[Cfg::CB];
-  uint32_t dmask = 0;
-#pragma unroll
-  for (int j = 0; j < Cfg::CB; ++j) {
-    h0[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    h1[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    sv[j] = 0.f;
-  }
-  for (uint32_t c = 0; c < nchunks; ++c) {
-    const int s = c % Cfg::STAGES;
-    mbar_wait(&full[s], (c / Cfg::STAGES) & 1);
-    unsigned char* st = smem + s * Cfg::STAGE_BYTES;
-    const uint4* recs = reinterpret_cast<const uint4*>(st);
-    const float* Ps = reinterpret_cast<const float*>(st + Cfg::OFF_P);
-    const float* isds = reinterpret_cast<const float*>(st + Cfg::OFF_ISD);
-    const uint64_t* ws = reinterpret_cast<const uint64_t*>(st + Cfg::OFF_W);
-    float* coef = reinterpret_cast<float*>(st + Cfg::OFF_COEF);
-    const int cnt = int(min(uint32_t(kChunkEntries), e1 - (e0 + c * kChunkEntries)));
-    // coefficients m_i(e) isd_i(x) for the 128 coalitions of the chunk's entries
-    for (int idx = tid; idx < cnt * Cfg::CO; idx += kConsumers) {
-      const int k = idx / Cfg::CO, i = idx % Cfg::CO, q = i / kTile;
-      const uint32_t y = recs[k].y;
-      const bool kept = y == kSelf || ((ws[(k * Cfg::TPC + q) * 4 + (y & 1u)] >> (i % kTile)) & 1ull);
-      coef[idx] = kept ? isds[idx] : 0.f;
-    }
-    consumer_sync();
-    const uint32_t startm = reinterpret_cast<const uint32_t*>(st + Cfg::OFF_FLAGS)[0];
-    const uint32_t endm = reinterpret_cast<const uint32_t*>(st + Cfg::OFF_FLAGS)[1];
-    int k = 0;
-    while (k < cnt) {
-      if ((startm >> k) & 1u) {  // segment start: keep isd_i(v), m_i(e_uv) for my coalitions
-        const uint32_t z = recs[k].z;
-        dmask = 0;
-#pragma unroll
-        for (int j = 0; j < Cfg::CB; ++j) {
-          const int i = c0i + j;
-          sv[j] = isds[k * Cfg::CO + i];
-          const bool m = z == kSelf || ((ws[(k * Cfg::TPC + i / kTile) * 4 + 2 + (z & 1u)] >> (i % kTile)) & 1ull);
-          dmask |= uint32_t(m) << j;
-        }
-      }
-      const uint32_t rest = endm >> k;
-      const int stop = rest ? k + __ffs(int(rest)) - 1 : cnt - 1;
-#pragma unroll 2
-      for (; k <= stop; ++k) {
-        const float4 xa = reinterpret_cast<const float4*>(Ps + k * D)[2 * fg];
-        const float4 xb = reinterpret_cast<const float4*>(Ps + k * D)[2 * fg + 1];
-        const float* ckp = coef + k * Cfg::CO + c0i;
-#pragma unroll
-        for (int j = 0; j < Cfg::CB; ++j) {
-          const float cc = ckp[j];
-          h0[j].x = fmaf(cc, xa.x, h0[j].x);
-          h0[j].y = fmaf(cc, xa.y, h0[j].y);
-          h0[j].z = fmaf(cc, xa.z, h0[j].z);
-          h0[j].w = fmaf(cc, xa.w, h0[j].w);
-          h1[j].x = fmaf(cc, xb.x, h1[j].x);
-          h1[j].y = fmaf(cc, xb.y, h1[j].y);
-          h1[j].z = fmaf(cc, xb.z, h1[j].z);
-          h1[j].w = fmaf(cc, xb.w, h1[j].w);
-        }
-      }
-      if (rest) {  // segment end: A += m isd_i(v) relu(isd_i(v) h + b0)
-#pragma unroll
-        for (int j = 0; j < Cfg::CB; ++j) {
-          const float sj = sv[j];
-          const float dv = ((dmask >> j) & 1u) ? sj : 0.f;
-          float* a = accs + (j * 8) * kConsumers + tid;
-          a[0 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].x, bv0.x), 0.f), a[0 * kConsumers]);
-          a[1 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].y, bv0.y), 0.f), a[1 * kConsumers]);
-          a[2 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].z, bv0.z), 0.f), a[2 * kConsumers]);
-          a[3 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h0[j].w, bv0.w), 0.f), a[3 * kConsumers]);
-          a[4 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].x, bv1.x), 0.f), a[4 * kConsumers]);
-          a[5 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].y, bv1.y), 0.f), a[5 * kConsumers]);
-          a[6 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].z, bv1.z), 0.f), a[6 * kConsumers]);
-          a[7 * kConsumers] = fmaf(dv, fmaxf(fmaf(sj, h1[j].w, bv1.w), 0.f), a[7 * kConsumers]);
-          h0[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          h1[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-    }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
-  }
-  // Apart[t'][item][i][f] for both tiles of the pair
-#pragma unroll
-  for (int j = 0; j < Cfg::CB; ++j) {
-    const int i = c0i + j;
-    const uint64_t tt = t + i / kTile;
-    float* out = Apart + ((tt * items + item) * kTile + (i % kTile)) * uint64_t(D);
-    const float* a = accs + (j * 8) * kConsumers + tid;
-    reinterpret_cast<float4*>(out)[2 * fg] =
-        make_float4(a[0 * kConsumers], a[1 * kConsumers], a[2 * kConsumers], a[3 * kConsumers]);
-    reinterpret_cast<float4*>(out)[2 * fg + 1] =
-        make_float4(a[4 * kConsumers], a[5 * kConsumers], a[6 * kConsumers], a[7 * kConsumers]);
-  }
-}
-
 // Softmax of z (float, max subtraction, sequential sum) as gcn.cpp:143-152.
 __device__ __forceinline__ void softmax_row(float* zi, uint32_t C) {
   float mx = zi[0];
@@ -696,7 +492,7 @@ __global__ void agg_generic_kernel(const uint64_t* __restrict__ maskt,
 __global__ void __launch_bounds__(256)
     sgemm_kernel(const float* __restrict__ A, const float* __restrict__ B,
                  const float* __restrict__ bias, float* __restrict__ Cm,
-                 uint64_t M, uint32_t N, uint32_t K, int relu) {
+                 uint64_t M, uint32_t N, uint32_t K, int relu, const uint32_t* __restrict__ arow) {
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -708,7 +504,7 @@ __global__ void __launch_bounds__(256)
       const int mm = idx / 16, kk = idx % 16;
       const uint64_t gm = m0 + mm;
       const uint32_t gk = k0 + kk;
-      As[kk][mm] = (gm < M && gk < K) ? A[gm * K + gk] : 0.f;
+      As[kk][mm] = (gm < M && gk < K) ? A[(arow ? uint64_t(arow[gm]) : gm) * K + gk] : 0.f;
       const int kb = idx / 64, nb = idx % 64;
       const uint32_t gkb = k0 + kb, gn = n0 + nb;
       Bs[kb][nb] = (gkb < K && gn < N) ? B[uint64_t(gkb) * N + gn] : 0.f;
@@ -1052,11 +848,13 @@ size_t tail_smem(uint32_t U, uint32_t K, uint32_t N, uint32_t C, uint32_t cpb, b
 }
 
 // X W0 for the whole subgraph (once per target)
+// (arow: row r of A is row arow[r] of the given matrix — the ball's rows
+// of the graph's features)
 void gemm(Ctx& ctx, const float* A, const float* B, const float* bias, float* Cm,
-          uint64_t M, uint32_t N, uint32_t K, bool relu) {
+          uint64_t M, uint32_t N, uint32_t K, bool relu, const uint32_t* arow = nullptr) {
   if (M == 0 || N == 0) return;
   dim3 grid((N + 63) / 64, unsigned((M + 63) / 64));
-  sgemm_kernel<<<grid, 256, 0, ctx.stream>>>(A, B, bias, Cm, M, N, K, relu ? 1 : 0);
+  sgemm_kernel<<<grid, 256, 0, ctx.stream>>>(A, B, bias, Cm, M, N, K, relu ? 1 : 0, arow);
   SF_LAUNCHED(ctx);
 }
 
@@ -1088,27 +886,6 @@ bool try_fused(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
   SF_LAUNCHED(ctx);
   return true;
 }
-
-template <int D>
-bool try_fused_wide(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
-                    uint64_t ntp, float* apart) {
-  if (e.dims[1] != uint64_t(D)) return false;
-  using Cfg = WideCfg<D>;
-  static bool configured = false;
-  if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_wide_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM));
-    configured = true;
-  }
-  dim3 grid(e.items, unsigned(ntp / Cfg::TPC));
-  fused_wide_kernel<D><<<grid, kConsumers + 32, Cfg::SMEM, ctx.stream>>>(
-      maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint4*>(e.ent.p), e.item_ent.p,
-      e.item_order.p, e.items, apart);
-  SF_LAUNCHED(ctx);
-  return true;
-}
-
-bool wide_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
 
 // Entry records and work items of the fused plan (see Engine / fused_kernel).
 void build_fused_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
@@ -1200,12 +977,26 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     SF_LAUNCHED(ctx);
   }
   // P0 = X W0 on the device
-  DevBuf<float>& x = ctx.feat_dev;
   DevBuf<float>& w0 = ctx.w0_dev;
-  x.upload(sg.features.data(), sg.features.size(), ctx.stream);
   w0.upload(m.layers[0].weight.data(), m.layers[0].weight.size(), ctx.stream);
   e.p0.reserve(uint64_t(e.V) * e.dims[1]);
-  gemm(ctx, x.p, w0.p, nullptr, e.p0.p, e.V, uint32_t(e.dims[1]), uint32_t(e.dims[0]), false);
+  if (sg.source) {  // X rows gathered from the graph's device-resident features
+    const Graph& g = *sg.source;
+    if (ctx.graph_feat_id != g.id) {
+      ctx.graph_feat.upload(g.features.data(), g.features.size(), ctx.stream);
+      ctx.graph_feat_id = g.id;
+      ctx.h2d_bytes += g.features.size() * 4;
+    }
+    ctx.ball_rows.upload(sg.local_to_global.data(), sg.local_to_global.size(), ctx.stream);
+    ctx.h2d_bytes += sg.local_to_global.size() * 4;
+    gemm(ctx, ctx.graph_feat.p, w0.p, nullptr, e.p0.p, e.V, uint32_t(e.dims[1]), uint32_t(e.dims[0]), false,
+         ctx.ball_rows.p);
+  } else {
+    DevBuf<float>& x = ctx.feat_dev;
+    x.upload(sg.features.data(), sg.features.size(), ctx.stream);
+    ctx.h2d_bytes += sg.features.size() * 4;
+    gemm(ctx, x.p, w0.p, nullptr, e.p0.p, e.V, uint32_t(e.dims[1]), uint32_t(e.dims[0]), false);
+  }
   while (int(e.w.size()) < e.L) {  // buffers are kept (and grown) across targets
     e.w.emplace_back(new DevBuf<float>);
     e.b.emplace_back(new DevBuf<float>);
@@ -1214,7 +1005,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
     if (l > 0) e.w[l]->upload(m.layers[l].weight.data(), m.layers[l].weight.size(), ctx.stream);
     e.b[l]->upload(m.layers[l].bias.data(), m.layers[l].bias.size(), ctx.stream);
   }
-  ctx.h2d_bytes += (rp.size() + sg.col.size() + sg.edge_player.size()) * 4 + sg.features.size() * 4;
+  ctx.h2d_bytes += (rp.size() + sg.col.size() + sg.edge_player.size()) * 4;
   for (const Layer& l : m.layers) ctx.h2d_bytes += (l.weight.size() + l.bias.size()) * 4;
   SF_CUDA(cudaStreamSynchronize(ctx.stream));  // host sources of the uploads may go now
   dt.lap("p0 gemm + weights");
@@ -1283,10 +1074,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   uint64_t T = std::max<uint64_t>(1, budget / std::max<uint64_t>(per_tile, 1));
   T = std::min<uint64_t>(T, tiles);
   T = std::min<uint64_t>(T, 65534);
-  // the wide variant (two tiles per CTA) measured slower than the narrow one
-  // on B200 (smem-bandwidth co-limited at 1 CTA/SM); opt in for A/B runs
-  static const bool narrow_only = std::getenv("SF_FUSED_WIDE") == nullptr;
-  const bool wide = (e.fused && wide_width(e.dims[1]) && !narrow_only) || e.tc;
+  const bool wide = e.tc;  // the tensor-core kernels take tile pairs
   if (wide) T = (T + 1) & ~uint64_t(1);  // tile pairs: odd batches get an all-zero tile
   const uint64_t off_isd = T * Wp * 8;
   const uint64_t off_h0 = off_isd + T * uint64_t(e.V) * kTile * 4;
@@ -1339,9 +1127,6 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       }
       const bool ok = (e.tc16 && launch_fused_tc16(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
                       (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
-                      (wide && (try_fused_wide<128>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
-                                try_fused_wide<64>(ctx, e, maskt, Wp, isd, ntp, pbuf) ||
-                                try_fused_wide<32>(ctx, e, maskt, Wp, isd, ntp, pbuf))) ||
                       try_fused<128>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<64>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<32>(ctx, e, maskt, Wp, isd, nt, pbuf) ||

@@ -239,7 +239,7 @@ static void save_sfg(const Graph& g, const std::string& path) {
   if (!out) throw DataError("write failed: " + path);
 }
 
-static Subgraph extract(const Graph& g, uint32_t target, int hops) {
+static Subgraph extract(const Graph& g, uint32_t target, int hops, bool with_features = true) {
   // graph.cpp:195-261: BFS ball (discovery order = local ids, target 0),
   // induced undirected edges sorted lexicographically, symmetric local CSR
   // with edge_player, feature slice.
@@ -293,6 +293,10 @@ static Subgraph extract(const Graph& g, uint32_t target, int hops) {
     sg.edge_player[cursor[u]++] = e;
     sg.col[cursor[v]] = u;
     sg.edge_player[cursor[v]++] = e;
+  }
+  if (!with_features) {  // the engine gathers the rows from a device copy of the graph's features
+    sg.source = &g;
+    return sg;
   }
   sg.features.resize(uint64_t(V) * g.feature_dim);
   for (uint32_t lu = 0; lu < V; ++lu)
@@ -546,7 +550,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     throw DataError("model expects " + std::to_string(m.layers.front().in) +
                     " input features but the graph has " + std::to_string(g.feature_dim));
   DebugTimer("explain").lap("start");
-  const Subgraph sg = extract(g, node, m.depth());
+  const Subgraph sg = extract(g, node, m.depth(), false);
   out->extract_ms = ms_since(t_start);
   const uint64_t n_raw = sg.num_players();
   if (o.player_cap != 0 && n_raw > o.player_cap) {

@@ -84,7 +84,8 @@ struct Subgraph {  // graph.hpp:36-53
   std::vector<uint64_t> row_ptr;
   std::vector<uint32_t> col;
   std::vector<uint32_t> edge_player;
-  std::vector<float> features;
+  std::vector<float> features;  // empty when `source` is set (explain path)
+  const Graph* source = nullptr;  // features gathered on the device from this graph
   uint32_t num_nodes() const {
     return static_cast<uint32_t>(local_to_global.size());
   }
@@ -242,6 +243,9 @@ struct Ctx {
   DevBuf<int> bad_dev;
   PinnedBuf<double> solver_host;  // CGLS scalars fetched by the host loop
   DevBuf<float> feat_dev, w0_dev; // engine_prepare temporaries (X, W0 for P0 = X W0)
+  DevBuf<float> graph_feat;       // device copy of a graph's features (explain path)
+  uint64_t graph_feat_id = 0;     // Graph::id it holds
+  DevBuf<uint32_t> ball_rows;     // local -> global node ids of the prepared subgraph
   DevBuf<uint64_t> fid_streams, fid_rows;  // fidelity random-baseline jobs
   DevBuf<uint32_t> fid_sizes;
   DevBuf<uint8_t> fid_inv;
