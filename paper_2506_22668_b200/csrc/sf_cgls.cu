@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "sf_device.cuh"
 #include "sf_internal.hpp"
@@ -204,6 +205,174 @@ __global__ void __launch_bounds__(kFwdThreads)
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int i = 0; i < kFwdThreads / 32; ++i) t += red[i];
+    dsq_part[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------- nibble tables
+// When every pair is a complement pair (the sampler's layout), both passes
+// run dense over the mask words instead of looping over set bits: each
+// 4-bit nibble of a word indexes a 16-entry table of subset sums (the 16
+// sums of 4 coefficients, 128 bytes = one row of shared-memory banks). All
+// lanes of a warp read the same table row at the same time (lanes own rows
+// in M u and players in M^T r), so every lookup is a conflict-free shared
+// load, there is no per-bit loop and no divergence except skipping all-zero
+// 32-bit half words. 16 lookups per word replace ~4 set bits at ~25
+// issued instructions each.
+
+// the 16 subset sums of (a, b, c, d), nibble bit i <-> element i
+__device__ __forceinline__ void subset_sums(double a, double b, double c, double d,
+                                            double* __restrict__ t) {
+  const double ab = a + b, cd = c + d;
+  const double lo[4] = {0.0, a, b, ab};
+  const double hi[4] = {0.0, c, d, cd};
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+#pragma unroll
+    for (int l = 0; l < 4; ++l) t[h * 4 + l] = (h == 0) ? lo[l] : (l == 0 ? hi[h] : hi[h] + lo[l]);
+}
+
+// acc += sum over the 8 nibbles of x of tab[j][nibble_j] (tab: 8 rows of 16)
+__device__ __forceinline__ void nib8(uint32_t x, const double* __restrict__ tab, double& acc) {
+  if (x == 0u) return;
+  double t[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t[j] = tab[j * 16 + ((x >> (4 * j)) & 15u)];
+  acc += ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+}
+
+// M^T (coef) over the transposed pair tiles: CTA = kNbPlayers players x one
+// split of tiles; per step kNbTT tiles' tables (16 per tile) are built from
+// the coefficients (double-buffered, one barrier per step).
+constexpr int kNbTT = 8;
+constexpr int kNbPer = 2;  // players per thread
+constexpr int kNbPlayers = 256 * kNbPer;
+
+__global__ void __launch_bounds__(256)
+    nib_transpose_kernel(const uint64_t* __restrict__ mt, uint64_t Wp, uint32_t n, uint64_t ptiles,
+                         const uint32_t* __restrict__ split_start, const double* __restrict__ coef,
+                         double* __restrict__ s_part) {
+  __shared__ __align__(16) double tab[2][kNbTT][16][16];  // 32 KB
+  const int tid = threadIdx.x;
+  const uint32_t e0 = blockIdx.x * kNbPlayers + tid;
+  const uint64_t t0 = split_start[blockIdx.y], t1 = split_start[blockIdx.y + 1];
+  double acc[kNbPer];
+#pragma unroll
+  for (int p = 0; p < kNbPer; ++p) acc[p] = 0.0;
+  int buf = 0;
+  for (uint64_t tb = t0; tb < t1; tb += kNbTT, buf ^= 1) {
+    const int nt = (t1 - tb) < uint64_t(kNbTT) ? int(t1 - tb) : kNbTT;
+    uint64_t w[kNbTT][kNbPer];
+#pragma unroll
+    for (int q = 0; q < kNbTT; ++q)
+#pragma unroll
+      for (int p = 0; p < kNbPer; ++p) {
+        const uint32_t e = e0 + p * 256;
+        w[q][p] = (q < nt && e < n) ? __ldcs(mt + (tb + q) * Wp + e) : 0ull;
+      }
+    if (tid < kNbTT * 16) {  // one (tile, nibble group) per thread
+      const int q = tid >> 4, j = tid & 15;
+      double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+      if (q < nt && tb + q < ptiles) {
+        const double2* cp = reinterpret_cast<const double2*>(coef + (tb + q) * 64 + 4 * j);
+        const double2 x = cp[0], y = cp[1];
+        a = x.x, b = x.y, c = y.x, d = y.y;
+      }
+      subset_sums(a, b, c, d, &tab[buf][q][j][0]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kNbTT; ++q)
+#pragma unroll
+      for (int p = 0; p < kNbPer; ++p) {
+        nib8(uint32_t(w[q][p]), &tab[buf][q][0][0], acc[p]);
+        nib8(uint32_t(w[q][p] >> 32), &tab[buf][q][8][0], acc[p]);
+      }
+  }
+  double* out = s_part + uint64_t(blockIdx.y) * n;
+#pragma unroll
+  for (int p = 0; p < kNbPer; ++p) {
+    const uint32_t e = e0 + p * 256;
+    if (e < n) out[e] = acc[p];
+  }
+}
+
+// M u over the even rows, lane per pair: CTA = 256 pairs x one part of the
+// player axis, walked in chunks of kNbChunk players whose tables (built from
+// u) fill 64 KB of shared memory. Writes the even-row dots per part.
+constexpr uint32_t kNbChunk = 2048;  // players per table chunk (a multiple of 64)
+
+__global__ void __launch_bounds__(256)
+    nib_forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t j0, uint64_t pairs,
+                       const double* __restrict__ u, uint32_t n, uint32_t part_players,
+                       double* __restrict__ vpart) {
+  extern __shared__ __align__(16) double ftab[];  // [kNbChunk / 4][16]
+  const int tid = threadIdx.x;
+  const uint64_t j = j0 + blockIdx.x * 256ull + tid;
+  const bool live = j < pairs;
+  const uint32_t p0 = blockIdx.y * part_players, p1 = min(n, p0 + part_players);
+  const uint64_t* rp = rows + 2 * (live ? j : 0) * W;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (uint32_t c0 = p0; c0 < p1; c0 += kNbChunk) {
+    const uint32_t cp = min(kNbChunk, p1 - c0);
+    __syncthreads();  // the previous chunk's lookups are done
+    for (uint32_t g = tid; g < kNbChunk / 4; g += 256) {
+      const uint32_t e = c0 + 4 * g;
+      double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+      if (4 * g < cp) {  // n need not be a multiple of 4
+        a = u[e];
+        if (e + 1 < p1) b = u[e + 1];
+        if (e + 2 < p1) c = u[e + 2];
+        if (e + 3 < p1) d = u[e + 3];
+      }
+      subset_sums(a, b, c, d, ftab + g * 16);
+    }
+    __syncthreads();
+    const uint32_t w0 = c0 / 64, nw = (cp + 63) / 64;
+    for (uint32_t k = 0; k < nw; k += 8) {
+      // 8 words per lane in flight (rows are 16-byte aligned, w0 + k even);
+      // words past the chunk are zeroed (they belong to the next chunk)
+      uint64_t x[8];
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        ulonglong2 y = make_ulonglong2(0ull, 0ull);
+        if (live && k + q < nw) y = __ldcs(reinterpret_cast<const ulonglong2*>(rp + w0 + k + q));
+        x[q] = y.x;
+        x[q + 1] = (k + q + 1 < nw) ? y.y : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double* t = ftab + (k + q) * 256;
+        nib8(uint32_t(x[q]), t, (q & 1) ? acc1 : acc0);
+        nib8(uint32_t(x[q] >> 32), t + 128, (q & 1) ? acc1 : acc0);
+      }
+    }
+  }
+  if (live) vpart[uint64_t(blockIdx.y) * (pairs - j0) + (j - j0)] = acc0 + acc1;
+}
+
+// v (complement shortcut, solver.cpp:261-263) and per-block sums of v^2
+__global__ void __launch_bounds__(256)
+    nib_forward_finish(const double* __restrict__ vpart, uint32_t parts, uint64_t j0, uint64_t pairs,
+                       const double* __restrict__ sw, const double* __restrict__ sum_u,
+                       double* __restrict__ v, double* __restrict__ dsq_part) {
+  __shared__ double red[8];
+  const uint64_t j = j0 + blockIdx.x * 256ull + threadIdx.x;
+  double dsq = 0.0;
+  if (j < pairs) {
+    double de = 0.0;
+    for (uint32_t k = 0; k < parts; ++k) de += vpart[uint64_t(k) * (pairs - j0) + (j - j0)];
+    const double ve = sw[2 * j] * de, vo = sw[2 * j + 1] * (*sum_u - de);
+    v[2 * j] = ve;
+    v[2 * j + 1] = vo;
+    dsq = ve * ve + vo * vo;
+  }
+  dsq = warp_sum(dsq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
     dsq_part[blockIdx.x] = t;
   }
 }
@@ -431,10 +600,15 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
   const uint64_t pblocks = (n + 511) / 512;  // transpose: 512 players per CTA
   const uint64_t max_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
-  const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2;
+  const uint64_t nib_pblocks = (n + kNbPlayers - 1) / kNbPlayers;
+  const uint64_t max_nsplits = (12ull * sms + nib_pblocks - 1) / nib_pblocks;
+  const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2 + (pairs + 255) / 256 + 1;
+  // nibble forward: the player axis in parts so the grid covers the SMs
+  const uint32_t nb_parts_max = uint32_t((n + kNbChunk - 1) / kNbChunk);
   const uint64_t bytes = 2 * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
-                         (fblocks_max + max_splits + 2) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
-                         max_splits * n * 8 + uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
+                         (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
+                         (max_splits + max_nsplits) * n * 8 + std::min<uint64_t>(nb_parts_max, 6ull * sms) * pairs * 8 +
+                         uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
   ctx.solver_work.reserve(bytes);
   Scratch sc{ctx.solver_work.p, 0};
   uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
@@ -446,9 +620,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* coef_o = sc.take<double>(ptiles * 64);
   double* dsq = sc.take<double>(fblocks_max);
   uint32_t* pop = sc.take<uint32_t>(rows);
-  uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + 2);
+  uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + max_nsplits + 4);
   double* kc = sc.take<double>(pairs);
-  double* s_part = sc.take<double>(max_splits * n);
+  double* s_part = sc.take<double>((max_splits + max_nsplits) * n);
+  double* vpart = sc.take<double>(std::min<uint64_t>(nb_parts_max, 6ull * sms) * pairs);
   double* s = sc.take<double>(n);
   double* tv = sc.take<double>(n + 1);  // fused mode: [A^T v ; ||v||^2]
   double* u = sc.take<double>(n);
@@ -483,9 +658,6 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     rowpop_kernel<<<blocks_for(rows * 32), 256, 0, st>>>(in.dev_rows, W, rows, pop);
     SF_LAUNCHED(ctx);
   }
-  // Load balance (rows are ordered by coalition size, so uniform splits put
-  // every dense row in the last blocks): forward row blocks and transpose
-  // tile splits are cut at equal cumulative set-bit cost, once per solve.
   std::vector<uint32_t> h_pop(rows);
   std::vector<uint8_t> h_comp(pairs);
   if (rows) {
@@ -498,14 +670,43 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   bool any_noncomp = false;
   for (uint64_t j = 0; j < pairs; ++j) any_noncomp |= !h_comp[j];
   if (any_noncomp) launch_transpose_tiles(ctx, in.dev_rows + W, pairs, W, ptiles, mto, 2ull * W);
-  std::vector<uint32_t> bounds{0};
+
+  // Dense tiles (pairs from pd on) take the nibble-table passes, sparse
+  // tiles the set-bit loops: with every pair a complement pair, the first
+  // tile whose mean kept-set size reaches n * density (SF_CGLS_NIB_DENSITY,
+  // default 1/32; the sampler orders pairs by size, so that is a suffix).
+  // SF_CGLS_NIBBLE=0 keeps every tile on the set-bit loops.
+  uint64_t pd = pairs;
   {
+    bool nibble = pairs > 0 && !any_noncomp;
+    if (const char* env = std::getenv("SF_CGLS_NIBBLE")) nibble = nibble && std::atoi(env) != 0;
+    double density = 1.0 / 32;
+    if (const char* env = std::getenv("SF_CGLS_NIB_DENSITY")) density = std::atof(env);
+    if (nibble) {
+      const double thr = density * n * 64;
+      for (uint64_t t = 0; t < ptiles; ++t) {
+        uint64_t c = 0;
+        for (uint64_t j = t * 64; j < std::min(pairs, t * 64 + 64); ++j) c += h_pop[2 * j];
+        if (double(c) >= thr) {
+          pd = t * 64;
+          break;
+        }
+      }
+    }
+  }
+  const uint64_t rows_b = 2 * pd, tiles_b = (pd + 63) / 64, pairs_n = pairs - pd;
+  // Load balance (rows are ordered by coalition size, so uniform splits put
+  // every dense row in the last blocks): forward row blocks and transpose
+  // tile splits of the set-bit part are cut at equal cumulative set-bit
+  // cost, once per solve.
+  std::vector<uint32_t> bounds{0};
+  if (rows_b) {
     const uint64_t wcost = (W + 31) / 32 * 4 + 16;  // word loads + row overhead per needed row
     uint64_t total = 0;
-    for (uint64_t i = 0; i < rows; ++i) total += needed(i) ? h_pop[i] + wcost : 1;
+    for (uint64_t i = 0; i < rows_b; ++i) total += needed(i) ? h_pop[i] + wcost : 1;
     const uint64_t target = std::max<uint64_t>(1, total / (4ull * sms));
     uint64_t acc = 0;
-    for (uint64_t i = 0; i < rows; i += 2) {
+    for (uint64_t i = 0; i < rows_b; i += 2) {
       acc += (needed(i) ? h_pop[i] + wcost : 1) + (needed(i + 1) ? h_pop[i + 1] + wcost : 1);
       const uint64_t cur = i + 2 - bounds.back();
       if (acc >= target || cur >= kFwdRows) {
@@ -513,34 +714,54 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
         acc = 0;
       }
     }
-    if (bounds.back() != rows) bounds.push_back(uint32_t(rows));
+    if (bounds.back() != rows_b) bounds.push_back(uint32_t(rows_b));
   }
   const uint64_t fblocks = bounds.size() - 1;
   std::vector<uint32_t> sbounds{0};
-  {
-    std::vector<uint64_t> tcost(ptiles, (any_noncomp ? 2 : 1) * (n / 8 + 64));
-    for (uint64_t i = 0; i < rows; ++i)
+  if (tiles_b) {
+    std::vector<uint64_t> tcost(tiles_b, (any_noncomp ? 2 : 1) * (n / 8 + 64));
+    for (uint64_t i = 0; i < std::min(rows, tiles_b * 128); ++i)
       if (needed(i)) tcost[i / 128] += h_pop[i];
     uint64_t total = 0;
     for (uint64_t c : tcost) total += c;
     const uint64_t target = std::max<uint64_t>(1, (total + max_splits - 1) / max_splits);
     uint64_t acc = 0;
-    for (uint64_t t = 0; t < ptiles; ++t) {
+    for (uint64_t t = 0; t < tiles_b; ++t) {
       acc += tcost[t];
       if (acc >= target && sbounds.size() < max_splits) {
         sbounds.push_back(uint32_t(t + 1));
         acc = 0;
       }
     }
-    if (sbounds.back() != ptiles) sbounds.push_back(uint32_t(ptiles));
+    if (sbounds.back() != tiles_b) sbounds.push_back(uint32_t(tiles_b));
   }
   const uint32_t splits = uint32_t(sbounds.size() - 1);
+  // nibble part: uniform tile splits (every dense tile costs the same)
+  std::vector<uint32_t> nbounds{uint32_t(tiles_b)};
+  if (ptiles > tiles_b) {
+    const uint64_t nt = ptiles - tiles_b;
+    const uint64_t ns = std::max<uint64_t>(1, std::min<uint64_t>(max_nsplits, (nt + kNbTT - 1) / kNbTT));
+    for (uint64_t k = 1; k <= ns; ++k) nbounds.push_back(uint32_t(tiles_b + nt * k / ns));
+  }
+  const uint32_t nsplits = uint32_t(nbounds.size() - 1);
+  const uint64_t nb_rowblocks = (pairs_n + 255) / 256;
+  const uint32_t nb_parts = uint32_t(std::max<uint64_t>(
+      1, std::min<uint64_t>({uint64_t(nb_parts_max), 6ull * sms,
+                             (6ull * sms + nb_rowblocks - 1) / std::max<uint64_t>(nb_rowblocks, 1)})));
+  const uint32_t nb_part_players = uint32_t(((uint64_t(n) + nb_parts - 1) / nb_parts + 63) / 64 * 64);
+  if (pairs_n) {
+    SF_CUDA(cudaFuncSetAttribute(nib_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kNbChunk / 4 * 16 * 8)));
+  }
   const uint32_t* row_start = d_bounds;
   const uint32_t* split_start = d_bounds + bounds.size();
+  const uint32_t* nsplit_start = split_start + sbounds.size();
   SF_CUDA(cudaMemcpyAsync(d_bounds, bounds.data(), bounds.size() * 4, cudaMemcpyHostToDevice, st));
   SF_CUDA(cudaMemcpyAsync(d_bounds + bounds.size(), sbounds.data(), sbounds.size() * 4,
                           cudaMemcpyHostToDevice, st));
-  ctx.h2d_bytes += (bounds.size() + sbounds.size()) * 4;
+  SF_CUDA(cudaMemcpyAsync(d_bounds + bounds.size() + sbounds.size(), nbounds.data(), nbounds.size() * 4,
+                          cudaMemcpyHostToDevice, st));
+  ctx.h2d_bytes += (bounds.size() + sbounds.size() + nbounds.size()) * 4;
   SF_CUDA(cudaStreamSynchronize(st));
   const double scw = std::sqrt(in.constraint_weight);
   double r_c = scw * in.constraint_target;
@@ -555,14 +776,21 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       SF_LAUNCHED(ctx);
     }
     reduce(kc, pairs, 0, 0.0, scal + 4);
-    dim3 grid(unsigned(pblocks), splits);
-    transpose_partial_kernel<<<grid, 256, 0, st>>>(mte, Wp, n, split_start, coef_e, 0, s_part);
-    SF_LAUNCHED(ctx);
-    if (any_noncomp) {
-      transpose_partial_kernel<<<grid, 256, 0, st>>>(mto, Wp, n, split_start, coef_o, 1, s_part);
+    if (splits) {
+      dim3 grid(unsigned(pblocks), splits);
+      transpose_partial_kernel<<<grid, 256, 0, st>>>(mte, Wp, n, split_start, coef_e, 0, s_part);
+      SF_LAUNCHED(ctx);
+      if (any_noncomp) {
+        transpose_partial_kernel<<<grid, 256, 0, st>>>(mto, Wp, n, split_start, coef_o, 1, s_part);
+        SF_LAUNCHED(ctx);
+      }
+    }
+    if (nsplits) {
+      nib_transpose_kernel<<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
+          mte, Wp, n, ptiles, nsplit_start, coef_e, s_part + uint64_t(splits) * n);
       SF_LAUNCHED(ctx);
     }
-    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits, n, scal + 4, out);
+    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits + nsplits, n, scal + 4, out);
     SF_LAUNCHED(ctx);
   };
   // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
@@ -572,18 +800,30 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw * r_c, n);
     SF_LAUNCHED(ctx);
   };
+  // v (set-bit rows [0, rows_b), nibble pairs [pd, pairs)) and the per-block
+  // sums of v^2 in dsq[0, fwd_blocks)
+  const uint64_t fwd_blocks = fblocks + nb_rowblocks;
+  auto forward_v = [&](const double* x) {
+    if (fblocks) {
+      forward_kernel<<<unsigned(fblocks), kFwdThreads, size_t(std::min<uint32_t>(n, kFwdChunk)) * 8, st>>>(
+          in.dev_rows, W, row_start, is_comp, x, n, in.dev_sw, scal + 0, v, dsq);
+      SF_LAUNCHED(ctx);
+    }
+    if (nb_rowblocks) {
+      nib_forward_kernel<<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 4 * 16 * 8, st>>>(
+          in.dev_rows, W, pd, pairs, x, n, nb_part_players, vpart);
+      SF_LAUNCHED(ctx);
+      nib_forward_finish<<<unsigned(nb_rowblocks), 256, 0, st>>>(vpart, nb_parts, pd, pairs, in.dev_sw,
+                                                                   scal + 0, v, dsq + fblocks);
+      SF_LAUNCHED(ctx);
+    }
+  };
+  SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdChunk * 8)));
   // v = sqrt(W) M u; delta = ||v||^2 all-reduced + v_c^2 (solver.cpp:252-287)
   auto forward_product = [&](double& delta, double& v_c) {
     reduce(u, n, 0, 0.0, scal + 0);  // sum_u
-    if (rows) {
-      const size_t smem = size_t(std::min<uint32_t>(n, kFwdChunk)) * 8;
-      SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kFwdChunk * 8)));
-      forward_kernel<<<unsigned(fblocks), kFwdThreads, smem, st>>>(in.dev_rows, W, row_start, is_comp, u,
-                                                                   n, in.dev_sw, scal + 0, v, dsq);
-      SF_LAUNCHED(ctx);
-    }
-    reduce(dsq, fblocks, 0, 0.0, scal + 1);
+    if (rows) forward_v(u);
+    reduce(dsq, rows ? fwd_blocks : 0, 0, 0.0, scal + 1);
     comm_allreduce_sum(ctx, scal + 1, 1);
     fetch(0, 2);
     delta = host[1];
@@ -623,17 +863,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     while (res.iterations < maxit) {
       reduce(u, n, 0, 0.0, scal + 0);  // sum_u (pin row: v_c = scw sum_u)
       if (rows) {
-        const size_t smem = size_t(std::min<uint32_t>(n, kFwdChunk)) * 8;
-        SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kFwdChunk * 8)));
-        forward_kernel<<<unsigned(fblocks), kFwdThreads, smem, st>>>(in.dev_rows, W, row_start, is_comp, u,
-                                                                     n, in.dev_sw, scal + 0, v, dsq);
-        SF_LAUNCHED(ctx);
+        forward_v(u);
         transpose_local(v, tv);
       } else {
         SF_CUDA(cudaMemsetAsync(tv, 0, uint64_t(n) * 8, st));
       }
-      reduce(dsq, rows ? fblocks : 0, 0, 0.0, tv + n);
+      reduce(dsq, rows ? fwd_blocks : 0, 0, 0.0, tv + n);
       comm_allreduce_sum(ctx, tv, uint64_t(n) + 1);
       fetch(0, 1);
       SF_CUDA(cudaMemcpyAsync(host + 1, tv + n, sizeof(double), cudaMemcpyDeviceToHost, st));
