@@ -17,6 +17,8 @@
 // PairwiseFolder; here the parity bar is 1e-3 relative L2).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -73,37 +75,36 @@ __global__ void reduce_stage2(const double* __restrict__ part, int count,
 }
 
 // ---------------------------------------------------------------- setup
-// is_comp[j]: row 2j+1 == ~row 2j (tail cleared)  (solver.cpp:188-198)
-__global__ void comp_flags_kernel(const uint64_t* __restrict__ rows, uint32_t W,
-                                  uint32_t n, uint64_t pairs,
-                                  uint8_t* __restrict__ is_comp) {
+// warp per pair, one read of both rows: set bits per row (load-balancing
+// weights, list sizes) and is_comp[j] = (row 2j+1 == ~row 2j, tail cleared)
+// (solver.cpp:188-198)
+__global__ void pair_scan_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint32_t n, uint64_t pairs,
+                                 uint32_t* __restrict__ pop, uint8_t* __restrict__ is_comp) {
   const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= pairs) return;
   const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
   const uint64_t* e = rows + 2 * j * W;
   const uint64_t* o = e + W;
+  uint32_t pe = 0, po = 0;
   bool ok = true;
   for (uint32_t w = lane; w < W; w += 32) {
-    uint64_t want = ~e[w];
-    if (w == W - 1) want &= tail;
-    ok &= (o[w] == want);
+    const uint64_t x = e[w], y = o[w];
+    pe += __popcll(x);
+    po += __popcll(y);
+    ok &= (y == ((w == W - 1) ? (~x & tail) : ~x));
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    pe += __shfl_xor_sync(kFull, pe, d);
+    po += __shfl_xor_sync(kFull, po, d);
   }
   ok = __all_sync(kFull, ok);
-  if (lane == 0) is_comp[j] = ok ? 1 : 0;
-}
-
-// set bits per row (load-balancing weights for the matvec partitions)
-__global__ void rowpop_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t nrows,
-                              uint32_t* __restrict__ pop) {
-  const uint64_t row = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= nrows) return;
-  uint32_t c = 0;
-  for (uint32_t w = lane; w < W; w += 32) c += __popcll(rows[row * W + w]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-  if (lane == 0) pop[row] = c;
+  if (lane == 0) {
+    pop[2 * j] = pe;
+    pop[2 * j + 1] = po;
+    is_comp[j] = ok ? 1 : 0;
+  }
 }
 
 __global__ void init_r_kernel(const double* __restrict__ sw,
@@ -220,8 +221,13 @@ __global__ void __launch_bounds__(kFwdThreads)
 // 32-bit half words. 16 lookups per word replace ~4 set bits at ~25
 // issued instructions each.
 
-// the 16 subset sums of (a, b, c, d), nibble bit i <-> element i
-__device__ __forceinline__ void subset_sums(double a, double b, double c, double d,
+// The 16 subset sums of (a, b, c, d), nibble bit i <-> element i. Table
+// rows are XOR-swizzled by the nibble group's index within its word
+// (key = j in 0..15, entry v stored at v ^ key): the builder's lanes own
+// different groups, so unswizzled rows would put a whole warp's stores in
+// one bank pair; the lookups (one table row per warp at a time) stay
+// conflict-free since the key is warp-uniform and folds into the mask op.
+__device__ __forceinline__ void subset_sums(double a, double b, double c, double d, uint32_t key,
                                             double* __restrict__ t) {
   const double ab = a + b, cd = c + d;
   const double lo[4] = {0.0, a, b, ab};
@@ -229,15 +235,17 @@ __device__ __forceinline__ void subset_sums(double a, double b, double c, double
 #pragma unroll
   for (int h = 0; h < 4; ++h)
 #pragma unroll
-    for (int l = 0; l < 4; ++l) t[h * 4 + l] = (h == 0) ? lo[l] : (l == 0 ? hi[h] : hi[h] + lo[l]);
+    for (int l = 0; l < 4; ++l) t[uint32_t(h * 4 + l) ^ key] = (h == 0) ? lo[l] : (l == 0 ? hi[h] : hi[h] + lo[l]);
 }
 
-// acc += sum over the 8 nibbles of x of tab[j][nibble_j] (tab: 8 rows of 16)
+// acc += sum over the 8 nibbles of x of tab[j][nibble_j] (tab: 8 swizzled
+// rows of 16, keys kbase + j)
+template <uint32_t kbase>
 __device__ __forceinline__ void nib8(uint32_t x, const double* __restrict__ tab, double& acc) {
   if (x == 0u) return;
   double t[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) t[j] = tab[j * 16 + ((x >> (4 * j)) & 15u)];
+  for (int j = 0; j < 8; ++j) t[j] = tab[j * 16 + (((x >> (4 * j)) & 15u) ^ (kbase + j))];
   acc += ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
 }
 
@@ -278,15 +286,15 @@ __global__ void __launch_bounds__(256)
         const double2 x = cp[0], y = cp[1];
         a = x.x, b = x.y, c = y.x, d = y.y;
       }
-      subset_sums(a, b, c, d, &tab[buf][q][j][0]);
+      subset_sums(a, b, c, d, uint32_t(j), &tab[buf][q][j][0]);
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kNbTT; ++q)
 #pragma unroll
       for (int p = 0; p < kNbPer; ++p) {
-        nib8(uint32_t(w[q][p]), &tab[buf][q][0][0], acc[p]);
-        nib8(uint32_t(w[q][p] >> 32), &tab[buf][q][8][0], acc[p]);
+        nib8<0>(uint32_t(w[q][p]), &tab[buf][q][0][0], acc[p]);
+        nib8<8>(uint32_t(w[q][p] >> 32), &tab[buf][q][8][0], acc[p]);
       }
   }
   double* out = s_part + uint64_t(blockIdx.y) * n;
@@ -297,21 +305,39 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// M u over the even rows, lane per pair: CTA = 256 pairs x one part of the
-// player axis, walked in chunks of kNbChunk players whose tables (built from
-// u) fill 64 KB of shared memory. Writes the even-row dots per part.
+// The dense pairs' even rows, word-major (rT[w][jl], jl = j - pd, padded with
+// zero rows to a whole number of 256-pair blocks), so the forward pass reads
+// one coalesced 8-byte word per lane. Built once per solve.
+__global__ void __launch_bounds__(256)
+    rows_word_major_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t pd, uint64_t pairs,
+                           uint64_t pstride, uint64_t* __restrict__ rT) {
+  __shared__ uint64_t t[32][33];
+  const uint32_t w0 = blockIdx.x * 32;
+  const uint64_t jl0 = blockIdx.y * 32ull;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {  // r: pair within the tile, tx: word
+    const uint64_t j = pd + jl0 + r;
+    t[r][tx] = (j < pairs && w0 + tx < W) ? rows[2 * j * W + w0 + tx] : 0ull;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8)  // r: word, tx: pair
+    if (w0 + r < W) rT[uint64_t(w0 + r) * pstride + jl0 + tx] = t[tx][r];
+}
+
+// M u over the dense pairs, lane per pair: CTA = 256 pairs x one part of
+// the player axis, walked in chunks of kNbChunk players whose tables (built
+// from u) fill 64 KB of shared memory. Writes the even-row dots per part.
 constexpr uint32_t kNbChunk = 2048;  // players per table chunk (a multiple of 64)
 
 __global__ void __launch_bounds__(256)
-    nib_forward_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t j0, uint64_t pairs,
+    nib_forward_kernel(const uint64_t* __restrict__ rT, uint64_t pstride, uint64_t pairs_n,
                        const double* __restrict__ u, uint32_t n, uint32_t part_players,
                        double* __restrict__ vpart) {
   extern __shared__ __align__(16) double ftab[];  // [kNbChunk / 4][16]
   const int tid = threadIdx.x;
-  const uint64_t j = j0 + blockIdx.x * 256ull + tid;
-  const bool live = j < pairs;
+  const uint64_t jl = blockIdx.x * 256ull + tid;
   const uint32_t p0 = blockIdx.y * part_players, p1 = min(n, p0 + part_players);
-  const uint64_t* rp = rows + 2 * (live ? j : 0) * W;
+  const uint64_t* col = rT + jl;
   double acc0 = 0.0, acc1 = 0.0;
   for (uint32_t c0 = p0; c0 < p1; c0 += kNbChunk) {
     const uint32_t cp = min(kNbChunk, p1 - c0);
@@ -325,30 +351,23 @@ __global__ void __launch_bounds__(256)
         if (e + 2 < p1) c = u[e + 2];
         if (e + 3 < p1) d = u[e + 3];
       }
-      subset_sums(a, b, c, d, ftab + g * 16);
+      subset_sums(a, b, c, d, g & 15u, ftab + g * 16);
     }
     __syncthreads();
     const uint32_t w0 = c0 / 64, nw = (cp + 63) / 64;
     for (uint32_t k = 0; k < nw; k += 8) {
-      // 8 words per lane in flight (rows are 16-byte aligned, w0 + k even);
-      // words past the chunk are zeroed (they belong to the next chunk)
       uint64_t x[8];
 #pragma unroll
-      for (int q = 0; q < 8; q += 2) {
-        ulonglong2 y = make_ulonglong2(0ull, 0ull);
-        if (live && k + q < nw) y = __ldcs(reinterpret_cast<const ulonglong2*>(rp + w0 + k + q));
-        x[q] = y.x;
-        x[q + 1] = (k + q + 1 < nw) ? y.y : 0ull;
-      }
+      for (int q = 0; q < 8; ++q) x[q] = (k + q < nw) ? __ldcs(col + uint64_t(w0 + k + q) * pstride) : 0ull;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const double* t = ftab + (k + q) * 256;
-        nib8(uint32_t(x[q]), t, (q & 1) ? acc1 : acc0);
-        nib8(uint32_t(x[q] >> 32), t + 128, (q & 1) ? acc1 : acc0);
+        nib8<0>(uint32_t(x[q]), t, (q & 1) ? acc1 : acc0);
+        nib8<8>(uint32_t(x[q] >> 32), t + 128, (q & 1) ? acc1 : acc0);
       }
     }
   }
-  if (live) vpart[uint64_t(blockIdx.y) * (pairs - j0) + (j - j0)] = acc0 + acc1;
+  if (jl < pairs_n) vpart[uint64_t(blockIdx.y) * pairs_n + jl] = acc0 + acc1;
 }
 
 // v (complement shortcut, solver.cpp:261-263) and per-block sums of v^2
@@ -375,6 +394,133 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < 8; ++i) t += red[i];
     dsq_part[blockIdx.x] = t;
   }
+}
+
+// ---------------------------------------------------------------- kept-set lists
+// The sparse pairs [0, pd) (small coalitions: most of the mask bytes, few of
+// the bits) are expanded once per solve into u32 index lists, so their
+// passes cost per kept player instead of per mask word:
+//   rows     per pair j, the even row's players, ascending      (M u)
+//   players  per player e, the pairs j < pd containing e, ascending (M^T r)
+// Lists are ascending and reduced in a fixed order (bitwise reproducible).
+constexpr uint32_t kListTiles = 128;  // pair tiles per counting segment
+
+__global__ void even_pop_kernel(const uint32_t* __restrict__ pop, uint64_t pd, uint64_t* __restrict__ cnt) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (j <= pd) cnt[j] = j < pd ? pop[2 * j] : 0;
+}
+
+// warp per pair: the even row's set bits in ascending order
+__global__ void row_list_fill_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t pd,
+                                     const uint64_t* __restrict__ off, uint32_t* __restrict__ idx) {
+  const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= pd) return;
+  const uint64_t* rp = rows + 2 * j * W;
+  uint64_t base = off[j];
+  for (uint32_t wb = 0; wb < W; wb += 32) {
+    const uint32_t w = wb + lane;
+    uint64_t x = w < W ? rp[w] : 0ull;
+    const uint32_t k = __popcll(x);
+    uint32_t incl = k;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint64_t pos = base + incl - k;
+    while (x) {
+      const int b = __ffsll(static_cast<long long>(x)) - 1;
+      x &= x - 1;
+      idx[pos++] = w * 64 + uint32_t(b);
+    }
+    base += __shfl_sync(kFull, incl, 31);
+  }
+}
+
+// thread per (segment g, player e) over the transposed tiles [0, tiles_b):
+// counts in player-major order so a player's list is contiguous
+__global__ void player_list_count_kernel(const uint64_t* __restrict__ mt, uint64_t Wp, uint32_t n,
+                                         uint64_t tiles_b, uint32_t segs, uint64_t* __restrict__ cnt) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (e >= n) return;
+  const uint64_t t0 = uint64_t(g) * kListTiles, t1 = min(tiles_b, t0 + kListTiles);
+  uint32_t k = 0;
+  for (uint64_t t = t0; t < t1; ++t) k += __popcll(mt[t * Wp + e]);
+  cnt[uint64_t(e) * segs + g] = k;
+}
+
+__global__ void player_list_fill_kernel(const uint64_t* __restrict__ mt, uint64_t Wp, uint32_t n,
+                                        uint64_t tiles_b, uint32_t segs, const uint64_t* __restrict__ off,
+                                        uint32_t* __restrict__ idx) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (e >= n) return;
+  const uint64_t t0 = uint64_t(g) * kListTiles, t1 = min(tiles_b, t0 + kListTiles);
+  uint64_t pos = off[uint64_t(e) * segs + g];
+  for (uint64_t t = t0; t < t1; ++t) {
+    uint64_t x = mt[t * Wp + e];
+    while (x) {
+      const int b = __ffsll(static_cast<long long>(x)) - 1;
+      x &= x - 1;
+      idx[pos++] = uint32_t(t * 64 + b);
+    }
+  }
+}
+
+// sum over list entries [a, b) of val[idx[i]], warp-strided, fixed order
+__device__ __forceinline__ double list_sum(const uint32_t* __restrict__ idx, uint64_t a, uint64_t b,
+                                           const double* __restrict__ val, int lane) {
+  double acc0 = 0.0, acc1 = 0.0;
+  uint64_t i = a + lane;
+  for (; i + 96 < b; i += 128) {
+    const uint32_t i0 = idx[i], i1 = idx[i + 32], i2 = idx[i + 64], i3 = idx[i + 96];
+    const double x0 = __ldg(val + i0), x1 = __ldg(val + i1), x2 = __ldg(val + i2), x3 = __ldg(val + i3);
+    acc0 += x0 + x2;
+    acc1 += x1 + x3;
+  }
+  for (; i < b; i += 32) acc0 += __ldg(val + idx[i]);
+  return warp_sum(acc0 + acc1);
+}
+
+// M u over the sparse pairs: CTA = 64 pairs (8 per warp); v by the
+// complement shortcut and the CTA's sum of v^2
+__global__ void __launch_bounds__(256)
+    list_forward_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ idx, uint64_t pd,
+                        const double* __restrict__ u, const double* __restrict__ sw,
+                        const double* __restrict__ sum_u, double* __restrict__ v,
+                        double* __restrict__ dsq_part) {
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double dsq = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    const uint64_t j = blockIdx.x * 64ull + warp * 8 + q;
+    if (j >= pd) break;
+    const double de = list_sum(idx, off[j], off[j + 1], u, lane);
+    const double ve = sw[2 * j] * de, vo = sw[2 * j + 1] * (*sum_u - de);
+    if (lane == 0) {
+      v[2 * j] = ve;
+      v[2 * j + 1] = vo;
+    }
+    dsq += ve * ve + vo * vo;
+  }
+  if (lane == 0) red[warp] = dsq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    dsq_part[blockIdx.x] = t;
+  }
+}
+
+// M^T coef over the sparse pairs: warp per player
+__global__ void __launch_bounds__(256)
+    list_transpose_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ idx, uint32_t n,
+                          uint32_t segs, const double* __restrict__ coef, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (e >= n) return;
+  const double acc = list_sum(idx, off[uint64_t(e) * segs], off[uint64_t(e + 1) * segs], coef, lane);
+  if (lane == 0) out[e] = acc;
 }
 
 // ---------------------------------------------------------------- updates
@@ -601,13 +747,15 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t pblocks = (n + 511) / 512;  // transpose: 512 players per CTA
   const uint64_t max_splits = std::max<uint64_t>(1, (8ull * sms) / pblocks);
   const uint64_t nib_pblocks = (n + kNbPlayers - 1) / kNbPlayers;
-  const uint64_t max_nsplits = (12ull * sms + nib_pblocks - 1) / nib_pblocks;
+  // nibble kernels run 3 CTAs per SM; ~8 waves keep the tail wave small
+  const uint64_t nib_ctas = 24ull * sms;
+  const uint64_t max_nsplits = (nib_ctas + nib_pblocks - 1) / nib_pblocks;
   const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2 + (pairs + 255) / 256 + 1;
   // nibble forward: the player axis in parts so the grid covers the SMs
   const uint32_t nb_parts_max = uint32_t((n + kNbChunk - 1) / kNbChunk);
   const uint64_t bytes = 2 * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
-                         (max_splits + max_nsplits) * n * 8 + std::min<uint64_t>(nb_parts_max, 6ull * sms) * pairs * 8 +
+                         (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
                          uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
   ctx.solver_work.reserve(bytes);
   Scratch sc{ctx.solver_work.p, 0};
@@ -622,8 +770,8 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   uint32_t* pop = sc.take<uint32_t>(rows);
   uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + max_nsplits + 4);
   double* kc = sc.take<double>(pairs);
-  double* s_part = sc.take<double>((max_splits + max_nsplits) * n);
-  double* vpart = sc.take<double>(std::min<uint64_t>(nb_parts_max, 6ull * sms) * pairs);
+  double* s_part = sc.take<double>((max_splits + max_nsplits + 1) * n);
+  double* vpart = sc.take<double>(std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs);
   double* s = sc.take<double>(n);
   double* tv = sc.take<double>(n + 1);  // fused mode: [A^T v ; ||v||^2]
   double* u = sc.take<double>(n);
@@ -651,11 +799,9 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
 
   launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, 2ull * W);
   if (pairs) {
-    comp_flags_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, is_comp);
+    pair_scan_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, pop, is_comp);
     SF_LAUNCHED(ctx);
     init_r_kernel<<<blocks_for(rows), 256, 0, st>>>(in.dev_sw, in.dev_targets, rows, r);
-    SF_LAUNCHED(ctx);
-    rowpop_kernel<<<blocks_for(rows * 32), 256, 0, st>>>(in.dev_rows, W, rows, pop);
     SF_LAUNCHED(ctx);
   }
   std::vector<uint32_t> h_pop(rows);
@@ -674,13 +820,13 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   // Dense tiles (pairs from pd on) take the nibble-table passes, sparse
   // tiles the set-bit loops: with every pair a complement pair, the first
   // tile whose mean kept-set size reaches n * density (SF_CGLS_NIB_DENSITY,
-  // default 1/32; the sampler orders pairs by size, so that is a suffix).
+  // default 1/64; the sampler orders pairs by size, so that is a suffix).
   // SF_CGLS_NIBBLE=0 keeps every tile on the set-bit loops.
   uint64_t pd = pairs;
   {
     bool nibble = pairs > 0 && !any_noncomp;
     if (const char* env = std::getenv("SF_CGLS_NIBBLE")) nibble = nibble && std::atoi(env) != 0;
-    double density = 1.0 / 32;
+    double density = 1.0 / 64;
     if (const char* env = std::getenv("SF_CGLS_NIB_DENSITY")) density = std::atof(env);
     if (nibble) {
       const double thr = density * n * 64;
@@ -694,7 +840,62 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       }
     }
   }
-  const uint64_t rows_b = 2 * pd, tiles_b = (pd + 63) / 64, pairs_n = pairs - pd;
+  const uint64_t tiles_b = (pd + 63) / 64, pairs_n = pairs - pd;
+  // the sparse pairs as kept-set lists (SF_CGLS_LISTS=0: set-bit loops)
+  bool lists = pd > 0 && pd < pairs + 1 && !any_noncomp;
+  if (const char* env = std::getenv("SF_CGLS_LISTS")) lists = lists && std::atoi(env) != 0;
+  const uint32_t lsegs = uint32_t(std::max<uint64_t>(1, (tiles_b + kListTiles - 1) / kListTiles));
+  const uint64_t* row_off = nullptr;
+  const uint32_t* row_idx = nullptr;
+  const uint64_t* pl_off = nullptr;
+  const uint32_t* pl_idx = nullptr;
+  if (lists) {
+    uint64_t entries = 0;
+    for (uint64_t j = 0; j < pd; ++j) entries += h_pop[2 * j];
+    const uint64_t nr = pd + 1, np = uint64_t(n) * lsegs + 1;
+    size_t tmp_r = 0, tmp_p = 0;
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_r, static_cast<const uint64_t*>(nullptr),
+                                          static_cast<uint64_t*>(nullptr), nr, st));
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_p, static_cast<const uint64_t*>(nullptr),
+                                          static_cast<uint64_t*>(nullptr), np, st));
+    const uint64_t tmp = std::max(tmp_r, tmp_p);
+    const uint64_t need = 2 * (nr + np) * 8 + tmp + 2 * entries * 4 + 8 * 256;
+    size_t free_b = 0, total_b = 0;
+    SF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (need > ctx.solver_lists.n && need - ctx.solver_lists.n > uint64_t(0.8 * double(free_b))) {
+      lists = false;  // does not fit: set-bit loops
+    } else {
+      ctx.solver_lists.reserve(need);
+      Scratch sp{ctx.solver_lists.p, 0};
+      uint64_t* r_cnt = sp.take<uint64_t>(nr);
+      uint64_t* r_off = sp.take<uint64_t>(nr);
+      uint64_t* p_cnt = sp.take<uint64_t>(np);
+      uint64_t* p_off = sp.take<uint64_t>(np);
+      void* tmp_buf = sp.take<unsigned char>(tmp);
+      uint32_t* r_idx = sp.take<uint32_t>(entries);
+      uint32_t* p_idx = sp.take<uint32_t>(entries);
+      even_pop_kernel<<<blocks_for(nr), 256, 0, st>>>(pop, pd, r_cnt);
+      SF_LAUNCHED(ctx);
+      SF_CUDA(cudaMemsetAsync(p_cnt + np - 1, 0, 8, st));
+      player_list_count_kernel<<<dim3(blocks_for(n), lsegs), 256, 0, st>>>(mte, Wp, n, tiles_b, lsegs, p_cnt);
+      SF_LAUNCHED(ctx);
+      size_t tb = tmp;
+      SF_CUDA(cub::DeviceScan::ExclusiveSum(tmp_buf, tb, r_cnt, r_off, nr, st));
+      tb = tmp;
+      SF_CUDA(cub::DeviceScan::ExclusiveSum(tmp_buf, tb, p_cnt, p_off, np, st));
+      row_list_fill_kernel<<<blocks_for(pd * 32), 256, 0, st>>>(in.dev_rows, W, pd, r_off, r_idx);
+      SF_LAUNCHED(ctx);
+      player_list_fill_kernel<<<dim3(blocks_for(n), lsegs), 256, 0, st>>>(mte, Wp, n, tiles_b, lsegs, p_off,
+                                                                         p_idx);
+      SF_LAUNCHED(ctx);
+      row_off = r_off;
+      row_idx = r_idx;
+      pl_off = p_off;
+      pl_idx = p_idx;
+    }
+  }
+  const uint64_t rows_b = lists ? 0 : 2 * pd;
+  const uint64_t lblocks = lists ? (pd + 63) / 64 : 0;
   // Load balance (rows are ordered by coalition size, so uniform splits put
   // every dense row in the last blocks): forward row blocks and transpose
   // tile splits of the set-bit part are cut at equal cumulative set-bit
@@ -718,7 +919,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   }
   const uint64_t fblocks = bounds.size() - 1;
   std::vector<uint32_t> sbounds{0};
-  if (tiles_b) {
+  if (tiles_b && !lists) {
     std::vector<uint64_t> tcost(tiles_b, (any_noncomp ? 2 : 1) * (n / 8 + 64));
     for (uint64_t i = 0; i < std::min(rows, tiles_b * 128); ++i)
       if (needed(i)) tcost[i / 128] += h_pop[i];
@@ -746,9 +947,18 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint32_t nsplits = uint32_t(nbounds.size() - 1);
   const uint64_t nb_rowblocks = (pairs_n + 255) / 256;
   const uint32_t nb_parts = uint32_t(std::max<uint64_t>(
-      1, std::min<uint64_t>({uint64_t(nb_parts_max), 6ull * sms,
-                             (6ull * sms + nb_rowblocks - 1) / std::max<uint64_t>(nb_rowblocks, 1)})));
+      1, std::min<uint64_t>({uint64_t(nb_parts_max), nib_ctas,
+                             (nib_ctas + nb_rowblocks - 1) / std::max<uint64_t>(nb_rowblocks, 1)})));
   const uint32_t nb_part_players = uint32_t(((uint64_t(n) + nb_parts - 1) / nb_parts + 63) / 64 * 64);
+  const uint64_t pstride = nb_rowblocks * 256;
+  uint64_t* rT = nullptr;
+  if (pairs_n) {
+    ctx.solver_dense.reserve(uint64_t(W) * pstride);
+    rT = ctx.solver_dense.p;
+    rows_word_major_kernel<<<dim3((W + 31) / 32, unsigned(pstride / 32)), 256, 0, st>>>(in.dev_rows, W, pd, pairs,
+                                                                                      pstride, rT);
+    SF_LAUNCHED(ctx);
+  }
   if (pairs_n) {
     SF_CUDA(cudaFuncSetAttribute(nib_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kNbChunk / 4 * 16 * 8)));
@@ -785,12 +995,18 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
         SF_LAUNCHED(ctx);
       }
     }
+    if (lists) {
+      list_transpose_kernel<<<blocks_for(uint64_t(n) * 32), 256, 0, st>>>(
+          pl_off, pl_idx, n, lsegs, coef_e, s_part + uint64_t(splits + nsplits) * n);
+      SF_LAUNCHED(ctx);
+    }
     if (nsplits) {
       nib_transpose_kernel<<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
           mte, Wp, n, ptiles, nsplit_start, coef_e, s_part + uint64_t(splits) * n);
       SF_LAUNCHED(ctx);
     }
-    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits + nsplits, n, scal + 4, out);
+    transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits + nsplits + (lists ? 1 : 0), n,
+                                                           scal + 4, out);
     SF_LAUNCHED(ctx);
   };
   // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
@@ -802,8 +1018,13 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   };
   // v (set-bit rows [0, rows_b), nibble pairs [pd, pairs)) and the per-block
   // sums of v^2 in dsq[0, fwd_blocks)
-  const uint64_t fwd_blocks = fblocks + nb_rowblocks;
+  const uint64_t fwd_blocks = fblocks + lblocks + nb_rowblocks;
   auto forward_v = [&](const double* x) {
+    if (lblocks) {
+      list_forward_kernel<<<unsigned(lblocks), 256, 0, st>>>(row_off, row_idx, pd, x, in.dev_sw, scal + 0, v,
+                                                              dsq + fblocks);
+      SF_LAUNCHED(ctx);
+    }
     if (fblocks) {
       forward_kernel<<<unsigned(fblocks), kFwdThreads, size_t(std::min<uint32_t>(n, kFwdChunk)) * 8, st>>>(
           in.dev_rows, W, row_start, is_comp, x, n, in.dev_sw, scal + 0, v, dsq);
@@ -811,10 +1032,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     }
     if (nb_rowblocks) {
       nib_forward_kernel<<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 4 * 16 * 8, st>>>(
-          in.dev_rows, W, pd, pairs, x, n, nb_part_players, vpart);
+          rT, pstride, pairs_n, x, n, nb_part_players, vpart);
       SF_LAUNCHED(ctx);
       nib_forward_finish<<<unsigned(nb_rowblocks), 256, 0, st>>>(vpart, nb_parts, pd, pairs, in.dev_sw,
-                                                                   scal + 0, v, dsq + fblocks);
+                                                                   scal + 0, v, dsq + fblocks + lblocks);
       SF_LAUNCHED(ctx);
     }
   };

@@ -231,6 +231,8 @@ struct Ctx {
   DevBuf<float> preds;
   DevBuf<unsigned char> work;  // engine workspace
   DevBuf<unsigned char> solver_work;
+  DevBuf<unsigned char> solver_lists;  // CGLS kept-set lists of the sparse pairs
+  DevBuf<uint64_t> solver_dense;       // CGLS dense pairs' even rows, word-major
   // sampler class table (pinned staging + device copy, reused per call)
   PinnedBuf<uint64_t> plan_host;
   PinnedBuf<uint32_t> plan_host32;

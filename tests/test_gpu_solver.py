@@ -158,26 +158,30 @@ def test_collective_counts_reference_protocol(ctx, port):
 
 @pytest.mark.parametrize("n,k,seed", [(999, 20000, 5), (3001, 40000, 6)])
 def test_cgls_pass_variants_agree(ctx, ref, port, n, k, seed, monkeypatch):
-    # The products run as set-bit loops on sparse tiles and as nibble-table
-    # lookups on dense ones (SF_CGLS_NIB_DENSITY picks the split): all-bit,
-    # all-nibble and the default split solve the same system.
+    # The products run as kept-set lists on the sparse pair tiles and as
+    # nibble-table lookups on the dense ones (SF_CGLS_NIB_DENSITY picks the
+    # split; SF_CGLS_LISTS=0 puts the sparse tiles on set-bit loops): every
+    # variant solves the same system.
     p = sf.plan_sizes(n, k, False)
     bits, ros = ctx.generate_masks(p, seed)
     vals = np.cos(np.arange(bits.shape[0]) * 0.11) * 0.5 + 0.5
     w = sf.assemble_weights(n, bits, ros)
     phi_ref, _, _, _ = ref.solve_cgls(n, bits, vals, 0.25, 0.75, max_iter=4 * n)
     out = {}
-    for name, env in [("bits", "1e9"), ("nibble", "0"), ("split", None)]:
-        if env is None:
-            monkeypatch.delenv("SF_CGLS_NIB_DENSITY", raising=False)
-        else:
-            monkeypatch.setenv("SF_CGLS_NIB_DENSITY", env)
+    variants = [("bits", "1e9", "0"), ("lists", "1e9", None), ("nibble", "0", None),
+                ("split_bits", None, "0"), ("split", None, None)]
+    for name, density, lists in variants:
+        for key, val in (("SF_CGLS_NIB_DENSITY", density), ("SF_CGLS_LISTS", lists)):
+            if val is None:
+                monkeypatch.delenv(key, raising=False)
+            else:
+                monkeypatch.setenv(key, val)
         r = ctx.solve_cgls(n, bits, w, vals - 0.25, 0.5, 1e6, max_iter=4 * n)
         assert r["converged"]
         out[name] = r["phi"]
         err = np.linalg.norm(r["phi"] - phi_ref) / np.linalg.norm(phi_ref)
         assert err <= 1e-3, (name, err)
         assert (sf.rank_edges(r["phi"])[:10] == port.rank_edges(phi_ref)[:10]).all()
-    for name in ("nibble", "split"):
+    for name in out:
         d = np.linalg.norm(out[name] - out["bits"]) / np.linalg.norm(out["bits"])
         assert d <= 1e-8, (name, d)
