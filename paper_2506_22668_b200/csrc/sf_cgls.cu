@@ -17,6 +17,7 @@
 // PairwiseFolder; here the parity bar is 1e-3 relative L2).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -699,6 +700,18 @@ __global__ void weight_products_kernel(const double* __restrict__ sw,
   wt[i] = i < rows ? ww * tgt[i] : 0.0;
 }
 
+// order-preserving key of -phi (+0 and -0 share a key: they compare equal)
+__global__ void rank_keys_kernel(const double* __restrict__ phi, uint32_t n, uint64_t* __restrict__ key,
+                                 uint32_t* __restrict__ idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = phi[i] == 0.0 ? 0.0 : phi[i];
+  uint64_t b = uint64_t(__double_as_longlong(v));
+  b = (b >> 63) ? ~b : (b | (1ull << 63));  // ascending in v
+  key[i] = ~b;                              // descending
+  idx[i] = i;
+}
+
 inline unsigned blocks_for(uint64_t n, unsigned t = 256) {
   return unsigned((n + t - 1) / t);
 }
@@ -1257,6 +1270,37 @@ std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in) {
     phi[i] = t / L[uint64_t(i) * n + i];
   }
   return phi;
+}
+
+// solver.cpp:430-440: a stable LSD radix sort of the keys over the index
+// order gives phi descending with ties by ascending index. NaN never gets
+// here (the solver rejects non-finite values).
+std::vector<uint32_t> rank_players(Ctx& ctx, const std::vector<double>& phi) {
+  const uint32_t n = uint32_t(phi.size());
+  std::vector<uint32_t> out(n);
+  if (n == 0) return out;
+  size_t tmp = 0;
+  SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const uint64_t*>(nullptr),
+                                          static_cast<uint64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                          static_cast<uint32_t*>(nullptr), n, 0, 64, ctx.stream));
+  ctx.rank_work.reserve(uint64_t(n) * (8 + 8 + 8 + 4 + 4) + tmp + 5 * 256);
+  Scratch sc{ctx.rank_work.p, 0};
+  double* d_phi = sc.take<double>(n);
+  uint64_t* k0 = sc.take<uint64_t>(n);
+  uint64_t* k1 = sc.take<uint64_t>(n);
+  uint32_t* i0 = sc.take<uint32_t>(n);
+  uint32_t* i1 = sc.take<uint32_t>(n);
+  void* t = sc.take<unsigned char>(tmp);
+  cudaStream_t st = ctx.stream;
+  SF_CUDA(cudaMemcpyAsync(d_phi, phi.data(), uint64_t(n) * 8, cudaMemcpyHostToDevice, st));
+  ctx.h2d_bytes += uint64_t(n) * 8;
+  rank_keys_kernel<<<blocks_for(n), 256, 0, st>>>(d_phi, n, k0, i0);
+  SF_LAUNCHED(ctx);
+  SF_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, k0, k1, i0, i1, n, 0, 64, st));
+  SF_CUDA(cudaMemcpyAsync(out.data(), i1, uint64_t(n) * 4, cudaMemcpyDeviceToHost, st));
+  ctx.d2h_bytes += uint64_t(n) * 4;
+  SF_CUDA(cudaStreamSynchronize(st));
+  return out;
 }
 
 }  // namespace sfb

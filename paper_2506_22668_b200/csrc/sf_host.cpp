@@ -411,13 +411,38 @@ static uint32_t kept_at_sparsity(uint32_t n, double sparsity) {  // fidelity.cpp
   return std::min(kept, n);
 }
 
-static std::vector<uint32_t> ranking(const std::vector<double>& phi) {  // solver.cpp:430-440
-  std::vector<uint32_t> o(phi.size());
-  std::iota(o.begin(), o.end(), 0u);
-  std::sort(o.begin(), o.end(), [&](uint32_t a, uint32_t b) {
-    if (phi[a] != phi[b]) return phi[a] > phi[b];
-    return a < b;
-  });
+// solver.cpp:430-440: players by phi descending, ties by index ascending.
+// LSD radix sort (8 stable byte passes) on an order-preserving key of phi
+// (+0 and -0 share a key, as they compare equal): input in index order, so
+// stability gives the index tie-break. NaN never reaches here (the solver
+// rejects non-finite values).
+static std::vector<uint32_t> ranking(const std::vector<double>& phi) {
+  const size_t n = phi.size();
+  if (n == 0) return {};
+  std::vector<uint64_t> key(n), key2(n);
+  std::vector<uint32_t> o(n), o2(n);
+  for (size_t i = 0; i < n; ++i) {
+    const double v = phi[i] == 0.0 ? 0.0 : phi[i];
+    uint64_t b;
+    std::memcpy(&b, &v, 8);
+    b = (b >> 63) ? ~b : (b | (uint64_t{1} << 63));  // ascending in v
+    key[i] = ~b;                                     // descending
+    o[i] = uint32_t(i);
+  }
+  for (int pass = 0; pass < 8; ++pass) {
+    const int sh = pass * 8;
+    size_t cnt[257] = {0};
+    for (size_t i = 0; i < n; ++i) ++cnt[((key[i] >> sh) & 255) + 1];
+    if (cnt[((key[0] >> sh) & 255) + 1] == n) continue;  // all equal: nothing to do
+    for (int b = 0; b < 256; ++b) cnt[b + 1] += cnt[b];
+    for (size_t i = 0; i < n; ++i) {
+      const size_t d = cnt[(key[i] >> sh) & 255]++;
+      key2[d] = key[i];
+      o2[d] = o[i];
+    }
+    key.swap(key2);
+    o.swap(o2);
+  }
   return o;
 }
 
@@ -433,13 +458,15 @@ struct FidelityOut {
 static FidelityOut fidelity(Ctx& ctx, const Subgraph& sg, const Model& m, uint32_t cls,
                             const std::vector<double>& phi, const std::vector<uint32_t>& counts,
                             const std::vector<double>& sparsities, uint64_t seed,
-                            uint32_t trials) {
+                            uint32_t trials, const std::vector<uint32_t>* ranked_in = nullptr) {
   const uint32_t n = uint32_t(sg.num_players());
   if (phi.size() != n)
     throw DataError("attribution vector has " + std::to_string(phi.size()) + " entries for " +
                     std::to_string(n) + " players");
+  DebugTimer dt("fidelity");
   const uint32_t W = std::max<uint32_t>(1, (n + 63) / 64);
-  const std::vector<uint32_t> ranked = ranking(phi);
+  const std::vector<uint32_t> ranked = ranked_in ? *ranked_in : ranking(phi);
+  dt.lap("ranking");
   const uint64_t tail = (n % 64) ? ((uint64_t{1} << (n % 64)) - 1) : ~uint64_t{0};
   std::vector<uint64_t> full(W, ~uint64_t{0});
   if (n == 0) full.assign(W, 0);
@@ -480,6 +507,7 @@ static FidelityOut fidelity(Ctx& ctx, const Subgraph& sg, const Model& m, uint32
       job_rows.push_back(mbase + ns + i * trials + t);
     }
   }
+  dt.lap("host rows");
   // device: deterministic rows, then the Floyd jobs written in place
   ctx.masks.reserve(rows * W);
   SF_CUDA(cudaMemcpyAsync(ctx.masks.p, host.data(), rows * W * 8, cudaMemcpyHostToDevice, ctx.stream));
@@ -505,8 +533,10 @@ static FidelityOut fidelity(Ctx& ctx, const Subgraph& sg, const Model& m, uint32
     }
     SF_CUDA(cudaStreamSynchronize(ctx.stream));
   }
+  dt.lap("random baselines");
   std::vector<float> score(rows);
   predict_rows(ctx, sg, m, ctx.masks.p, rows, cls, score.data(), nullptr);
+  dt.lap("predict");
   const double f0 = double(score[0]);
   for (size_t i = 0; i < nc; ++i) {
     out.plus.push_back(std::abs(f0 - double(score[1 + i])));
@@ -668,7 +698,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
   }
   DebugTimer tail("explain tail");
   out->phi = dup_array(phi);
-  const std::vector<uint32_t> ranked = ranking(phi);
+  const std::vector<uint32_t> ranked = rank_players(ctx, phi);
   tail.lap("ranking");
   const size_t keep = std::min<size_t>(o.top_k, ranked.size());
   std::vector<uint32_t> tp(ranked.begin(), ranked.begin() + keep);
@@ -683,7 +713,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
                                                 : std::vector<uint32_t>{5, 10, 20};
     std::vector<double> sp = o.sparsities ? std::vector<double>(o.sparsities, o.sparsities + o.num_sparsities)
                                           : std::vector<double>{0.1, 0.3, 0.5, 0.7, 0.9};
-    FidelityOut f = fidelity(ctx, sg, m, out->predicted_class, phi, counts, sp, seed, o.baseline_trials);
+    FidelityOut f = fidelity(ctx, sg, m, out->predicted_class, phi, counts, sp, seed, o.baseline_trials, &ranked);
     out->has_fidelity = 1;
     out->num_counts = uint32_t(f.counts.size());
     out->fid_counts = dup_array(f.counts);

@@ -233,6 +233,7 @@ struct Ctx {
   DevBuf<unsigned char> solver_work;
   DevBuf<unsigned char> solver_lists;  // CGLS kept-set lists of the sparse pairs
   DevBuf<uint64_t> solver_dense;       // CGLS dense pairs' even rows, word-major
+  DevBuf<unsigned char> rank_work;     // rank_players scratch
   // sampler class table (pinned staging + device copy, reused per call)
   PinnedBuf<uint64_t> plan_host;
   PinnedBuf<uint32_t> plan_host32;
@@ -344,6 +345,8 @@ struct CglsInput {
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
 std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in);
+// players by phi descending, ties by index (solver.cpp:430-440), on the device
+std::vector<uint32_t> rank_players(Ctx& ctx, const std::vector<double>& phi);
 
 // sf_assemble (sf_cgls.cu): per-row sqrt(weight) and targets on device from
 // per-size weights and float predictions.

@@ -165,3 +165,13 @@ def test_select_nodes_matches_reference(ref):
             ref.select_nodes(rg, rule)
         assert theirs.value.code == 2
         assert str(ours.value).endswith(str(theirs.value).split("] ", 1)[1]), rule
+
+
+def test_rank_edges_ties_and_signed_zero():
+    # solver.cpp:430-440: descending phi, ties by ascending index; +0 == -0
+    rng = np.random.default_rng(4)
+    for n in (1, 2, 7, 1000, 50000):
+        phi = rng.choice([-1.5, -0.0, 0.0, 1e-300, -1e-300, 2.0, 3.25], size=n)
+        phi[: n // 3] = rng.standard_normal(n // 3) * 10.0 ** rng.integers(-300, 300, n // 3)
+        want = sorted(range(n), key=lambda i: (-phi[i], i))
+        assert list(sf.rank_edges(phi)) == want
