@@ -44,17 +44,18 @@ __device__ __forceinline__ uint32_t find_class(const ClassTable& ct,
 
 // Bitset accessors for the two storage variants: shared memory (one row per
 // warp, fast path) or the output row itself in global memory (large n).
+// (shared memory has native 32-bit atomics only; 64-bit ones are CAS loops.
+// Bit t of u64 word t/64 is bit t%32 of u32 word t/32 on little-endian.)
 struct SmemSet {
   uint64_t* w;
-  __device__ bool test(uint32_t t) const { return (w[t >> 6] >> (t & 63)) & 1ull; }
+  __device__ uint32_t* w32() const { return reinterpret_cast<uint32_t*>(w); }
+  __device__ bool test(uint32_t t) const { return (w32()[t >> 5] >> (t & 31)) & 1u; }
   __device__ bool test_and_set(uint32_t t) const {
-    const unsigned long long b = 1ull << (t & 63);
-    return atomicOr(reinterpret_cast<unsigned long long*>(&w[t >> 6]), b) & b;
+    const uint32_t b = 1u << (t & 31);
+    return atomicOr(&w32()[t >> 5], b) & b;
   }
   __device__ void set(uint32_t t) const { test_and_set(t); }
-  __device__ void clear(uint32_t t) const {
-    atomicAnd(reinterpret_cast<unsigned long long*>(&w[t >> 6]), ~(1ull << (t & 63)));
-  }
+  __device__ void clear(uint32_t t) const { atomicAnd(&w32()[t >> 5], ~(1u << (t & 31))); }
 };
 struct GmemSet {
   uint64_t* w;
