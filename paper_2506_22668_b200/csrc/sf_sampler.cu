@@ -204,26 +204,33 @@ __global__ void __launch_bounds__(kSamplerWarps * 32)
   }
 }
 
+template <bool kSmem>
 __global__ void __launch_bounds__(kSamplerWarps * 32)
     floyd_jobs_kernel(uint32_t n, uint32_t W, uint64_t seed,
                       const uint64_t* __restrict__ streams,
                       const uint32_t* __restrict__ sizes,
                       const uint8_t* __restrict__ invert, uint64_t jobs,
                       uint64_t* __restrict__ rows) {
+  extern __shared__ uint64_t smem_sets[];
   const int lane = threadIdx.x & 31;
   const uint64_t j = blockIdx.x * uint64_t(kSamplerWarps) + (threadIdx.x >> 5);
   if (j >= jobs) return;
   const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
   uint64_t* row = rows + j * W;
-  for (uint32_t w = lane; w < W; w += 32) row[w] = 0;
+  uint64_t* bits = kSmem ? smem_sets + size_t(threadIdx.x >> 5) * W : row;
+  for (uint32_t w = lane; w < W; w += 32) bits[w] = 0;
   __syncwarp();
-  floyd_warp(GmemSet{row}, n, sizes[j], seed, streams[j], lane);
+  if (kSmem)
+    floyd_warp(SmemSet{bits}, n, sizes[j], seed, streams[j], lane);
+  else
+    floyd_warp(GmemSet{bits}, n, sizes[j], seed, streams[j], lane);
   __syncwarp();
-  if (invert[j])
-    for (uint32_t w = lane; w < W; w += 32) {
-      const uint64_t v = ~__ldcg(&row[w]);
-      row[w] = (w == W - 1) ? (v & tail) : v;
-    }
+  const bool inv = invert[j] != 0;
+  for (uint32_t w = lane; w < W; w += 32) {
+    uint64_t v = kSmem ? bits[w] : __ldcg(&bits[w]);
+    if (inv) v = (w == W - 1) ? (~v & tail) : ~v;
+    row[w] = v;
+  }
 }
 
 __global__ void philox_stream_kernel(uint64_t seed, uint64_t stream,
@@ -363,8 +370,17 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
                        uint64_t* dev_rows) {
   if (jobs == 0) return;
   const uint32_t W = (n + 63) / 64;
-  floyd_jobs_kernel<<<unsigned((jobs + kSamplerWarps - 1) / kSamplerWarps), kSamplerWarps * 32, 0,
-                      ctx.stream>>>(n, W, seed, dev_streams, dev_sizes, dev_invert, jobs, dev_rows);
+  const unsigned grid = unsigned((jobs + kSamplerWarps - 1) / kSamplerWarps);
+  const size_t smem = size_t(kSamplerWarps) * W * 8;
+  if (smem <= 200 * 1024) {  // the set in shared memory (one row per warp)
+    auto k = floyd_jobs_kernel<true>;
+    SF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k<<<grid, kSamplerWarps * 32, smem, ctx.stream>>>(n, W, seed, dev_streams, dev_sizes, dev_invert, jobs,
+                                                      dev_rows);
+  } else {
+    floyd_jobs_kernel<false><<<grid, kSamplerWarps * 32, 0, ctx.stream>>>(n, W, seed, dev_streams, dev_sizes,
+                                                                          dev_invert, jobs, dev_rows);
+  }
   SF_LAUNCHED(ctx);
 }
 
