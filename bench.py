@@ -245,8 +245,10 @@ def run_ours(args):
     if args.explain_only:  # profiling: one warm explain_node, then one more (ncu launch lists)
         from paper_2506_22668_b200.api import ExplainOptions
 
-        for _ in range(2):
+        for _ in range(int(os.environ.get("SF_EXPLAIN_REPEAT", "2"))):
             ex = ctx.explain_node(g, m, d["target"], ExplainOptions(samples=k, seed=cfg.explain_seed))
+            if os.environ.get("SF_EXPLAIN_REPEAT") and rank == 0:
+                print("explain", round(ex.timings["solve_ms"], 2), round(ex.timings["total_ms"], 2), flush=True)
         if rank == 0:
             print(json.dumps({"explain_only": True, "iterations": ex.iterations, "timings_ms": ex.timings}))
         ctx.close()
@@ -323,8 +325,8 @@ def run_ours(args):
     from paper_2506_22668_b200.api import ExplainOptions
 
     opts = ExplainOptions(samples=k, seed=cfg.explain_seed)
-    e2e_steps = 0 if args.no_e2e else max(1, min(args.steps, 3))
-    for _ in range(2 if e2e_steps else 0):  # warm-up calls (allocations, first-touch)
+    e2e_steps = 0 if args.no_e2e else max(1, min(args.steps, 5))
+    for _ in range(3 if e2e_steps else 0):  # warm-up calls (allocations, first-touch)
         ex = ctx.explain_node(g, m, d["target"], opts)
     h2d0, d2h0 = C.c_uint64(), C.c_uint64()
     sf.lib.sf_ctx_io_bytes(ctx.h, C.byref(h2d0), C.byref(d2h0))

@@ -810,6 +810,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     SF_CUDA(cudaStreamSynchronize(st));
   };
 
+  DebugTimer dt("cgls");
   launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, 2ull * W);
   if (pairs) {
     pair_scan_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, pop, is_comp);
@@ -825,6 +826,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     SF_CUDA(cudaStreamSynchronize(st));
     ctx.d2h_bytes += rows * 4 + pairs;
   }
+  dt.lap("tiles + pair scan");
   auto needed = [&](uint64_t row) { return !((row & 1) && h_comp[row >> 1]); };
   bool any_noncomp = false;
   for (uint64_t j = 0; j < pairs; ++j) any_noncomp |= !h_comp[j];
@@ -906,6 +908,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       pl_off = p_off;
       pl_idx = p_idx;
     }
+  }
+  if (lists) {
+    SF_CUDA(cudaStreamSynchronize(st));
+    dt.lap("lists");
   }
   const uint64_t rows_b = lists ? 0 : 2 * pd;
   const uint64_t lblocks = lists ? (pd + 63) / 64 : 0;
@@ -1065,6 +1071,8 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     delta += v_c * v_c;
   };
 
+  SF_CUDA(cudaStreamSynchronize(st));
+  dt.lap("setup");
   SF_CUDA(cudaMemsetAsync(phi, 0, uint64_t(n) * 8, st));
   transpose_product();
   reduce(s, n, 1, 0.0, scal + 2);                // gamma = ||s||^2
@@ -1149,7 +1157,9 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     download_phi();
     return res;
   }
+  DebugTimer di("cgls iteration");
   while (res.iterations < maxit) {
+    di.lap("");
     double delta = 0.0, v_c = 0.0;
     forward_product(delta, v_c);
     if (!std::isfinite(delta))

@@ -83,7 +83,14 @@ __global__ void __launch_bounds__(256)
     const uint64_t* mt = maskt + t * Wp;
     uint32_t clo = 1, chi = 1;
     const uint32_t beg = row_ptr[u], end = row_ptr[u + 1];
-    for (uint32_t i = beg + lane; i - lane < end; i += 32) {
+    uint32_t i = beg + lane;
+    for (; i + 32 - lane < end; i += 64) {  // two chunks in flight
+      const uint64_t x0 = __ldg(&mt[__ldg(&ep[i])]);
+      const uint64_t x1 = i + 32 < end ? __ldg(&mt[__ldg(&ep[i + 32])]) : 0ull;
+      clo += __popc(bfly32(uint32_t(x0))) + __popc(bfly32(uint32_t(x1)));
+      chi += __popc(bfly32(uint32_t(x0 >> 32))) + __popc(bfly32(uint32_t(x1 >> 32)));
+    }
+    for (; i - lane < end; i += 32) {
       const uint64_t x = i < end ? __ldg(&mt[__ldg(&ep[i])]) : 0ull;
       clo += __popc(bfly32(uint32_t(x)));
       chi += __popc(bfly32(uint32_t(x >> 32)));
@@ -120,20 +127,32 @@ __global__ void __launch_bounds__(256)
   const uint32_t slot = lane & (G - 1), sub = lane >> lg;
   const uint32_t p = slot < deg ? __ldg(&ep[beg + slot]) : 0u;
   const uint32_t fmask = G == 32 ? 0xFFFFFFFFu : (1u << G) - 1u;
-  for (uint32_t t0 = 0; t0 < ntiles; t0 += per) {
-    const uint32_t t = t0 + sub;
-    const uint64_t x = (slot < deg && t < ntiles) ? __ldg(&maskt[uint64_t(t) * Wp + p]) : 0ull;
-    const uint32_t lo = bfly32(uint32_t(x)), hi = bfly32(uint32_t(x >> 32));
-    for (uint32_t q = 0; q < per && t0 + q < ntiles; ++q) {
-      const uint32_t sh = q << lg;
-      float* out = isd + (uint64_t(t0 + q) * V + u) * kTile;
-      const uint32_t dlo = 1 + __popc((lo >> sh) & fmask), dhi = 1 + __popc((hi >> sh) & fmask);
-      out[lane] = __ldg(&tab[dlo]);
-      out[lane + 32] = __ldg(&tab[dhi]);
-      if (deg16) {
-        uint16_t* o16 = deg16 + (uint64_t(t0 + q) * V + u) * kTile;
-        o16[lane] = uint16_t(dlo);
-        o16[lane + 32] = uint16_t(dhi);
+  // kIsdAhead groups of `per` tiles per step: their mask words are all in
+  // flight before the first transpose (the loop is latency-bound otherwise)
+  constexpr int kIsdAhead = 4;
+  for (uint32_t t0 = 0; t0 < ntiles; t0 += kIsdAhead * per) {
+    uint64_t xs[kIsdAhead];
+#pragma unroll
+    for (int k = 0; k < kIsdAhead; ++k) {
+      const uint32_t t = t0 + k * per + sub;
+      xs[k] = (slot < deg && t < ntiles) ? __ldg(&maskt[uint64_t(t) * Wp + p]) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < kIsdAhead; ++k) {
+      const uint32_t tb = t0 + k * per;
+      if (tb >= ntiles) break;  // warp-uniform
+      const uint32_t lo = bfly32(uint32_t(xs[k])), hi = bfly32(uint32_t(xs[k] >> 32));
+      for (uint32_t q = 0; q < per && tb + q < ntiles; ++q) {
+        const uint32_t sh = q << lg;
+        float* out = isd + (uint64_t(tb + q) * V + u) * kTile;
+        const uint32_t dlo = 1 + __popc((lo >> sh) & fmask), dhi = 1 + __popc((hi >> sh) & fmask);
+        out[lane] = __ldg(&tab[dlo]);
+        out[lane + 32] = __ldg(&tab[dhi]);
+        if (deg16) {
+          uint16_t* o16 = deg16 + (uint64_t(tb + q) * V + u) * kTile;
+          o16[lane] = uint16_t(dlo);
+          o16[lane + 32] = uint16_t(dhi);
+        }
       }
     }
   }

@@ -810,6 +810,21 @@ int sf_ctx_create(int device, sf_ctx** out) {
     auto* c = new sf_ctx;
     c->c.device = device;
     try {
+      // Host wait policy for stream syncs (the CGLS loop syncs twice per
+      // iteration): spin by default (blocking/yield waits measured +1 to
+      // +25 ms per C2 solve); SF_SCHED=auto|yield|blocking overrides. Only
+      // takes effect if the device's context is not active yet.
+      {
+        const char* sch = std::getenv("SF_SCHED");
+        const std::string p = sch ? sch : "spin";
+        if (p != "auto") {
+          const unsigned f = p == "yield"      ? cudaDeviceScheduleYield
+                             : p == "blocking" ? cudaDeviceScheduleBlockingSync
+                                               : cudaDeviceScheduleSpin;
+          cudaSetDevice(device);
+          if (cudaSetDeviceFlags(f) != cudaSuccess) cudaGetLastError();
+        }
+      }
       SF_CUDA(cudaSetDevice(device));
       SF_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
     } catch (...) {
