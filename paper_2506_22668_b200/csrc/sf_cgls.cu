@@ -875,12 +875,18 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                                           static_cast<uint64_t*>(nullptr), np, st));
     const uint64_t tmp = std::max(tmp_r, tmp_p);
     const uint64_t need = 2 * (nr + np) * 8 + tmp + 2 * entries * 4 + 8 * 256;
-    size_t free_b = 0, total_b = 0;
-    SF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (need > ctx.solver_lists.n && need - ctx.solver_lists.n > uint64_t(0.8 * double(free_b))) {
-      lists = false;  // does not fit: set-bit loops
-    } else {
-      ctx.solver_lists.reserve(need);
+    // (no cudaMemGetInfo: it measured 0.15-45 ms per call; an allocation
+    // that fails falls back to the set-bit loops instead)
+    if (need > ctx.solver_lists.n) {
+      try {
+        ctx.solver_lists.reserve(need);
+      } catch (const std::exception&) {
+        cudaGetLastError();
+        ctx.solver_lists.release();
+        lists = false;
+      }
+    }
+    if (lists) {
       Scratch sp{ctx.solver_lists.p, 0};
       uint64_t* r_cnt = sp.take<uint64_t>(nr);
       uint64_t* r_off = sp.take<uint64_t>(nr);
@@ -894,10 +900,18 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       SF_CUDA(cudaMemsetAsync(p_cnt + np - 1, 0, 8, st));
       player_list_count_kernel<<<dim3(blocks_for(n), lsegs), 256, 0, st>>>(mte, Wp, n, tiles_b, lsegs, p_cnt);
       SF_LAUNCHED(ctx);
+      if (dt.on) {
+        SF_CUDA(cudaStreamSynchronize(st));
+        dt.lap("lists: counts");
+      }
       size_t tb = tmp;
       SF_CUDA(cub::DeviceScan::ExclusiveSum(tmp_buf, tb, r_cnt, r_off, nr, st));
       tb = tmp;
       SF_CUDA(cub::DeviceScan::ExclusiveSum(tmp_buf, tb, p_cnt, p_off, np, st));
+      if (dt.on) {
+        SF_CUDA(cudaStreamSynchronize(st));
+        dt.lap("lists: scans");
+      }
       row_list_fill_kernel<<<blocks_for(pd * 32), 256, 0, st>>>(in.dev_rows, W, pd, r_off, r_idx);
       SF_LAUNCHED(ctx);
       player_list_fill_kernel<<<dim3(blocks_for(n), lsegs), 256, 0, st>>>(mte, Wp, n, tiles_b, lsegs, p_off,
