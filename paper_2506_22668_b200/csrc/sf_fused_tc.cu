@@ -535,11 +535,13 @@ bool tc_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
 // (segments padded to multiples of e.tc_kstep entries).
 void build_tc_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   const uint32_t U = uint32_t(e.ball[e.L - 2]);
-  // padded entries per work item: 1024 measured best on C2 (512: 78.7 ms/step,
-  // 1024: 73.9, 1536: 82.9 — per-CTA pipeline fill/drain vs wave
-  // quantization); SF_TC_ITEM overrides for experiments
+  // padded entries per work item (per-CTA pipeline fill/drain and item
+  // partials for the tail vs wave quantization). C2 value ms/step with the
+  // B bank, 768 MB batches and the 16-coalition tail: 768: 51.3, 1024: 49.2,
+  // 1536: 48.3, 2048: 47.4, 3072: 47.5, 4096: 48.4, 8192: 50.8.
+  // SF_TC_ITEM overrides for experiments.
   static const uint64_t kItem =
-      std::getenv("SF_TC_ITEM") ? std::strtoull(std::getenv("SF_TC_ITEM"), nullptr, 10) : 1024;
+      std::getenv("SF_TC_ITEM") ? std::strtoull(std::getenv("SF_TC_ITEM"), nullptr, 10) : 2048;
   std::vector<uint32_t> ent;        // 2 words per entry
   std::vector<uint8_t> kfl;         // per 8 entries
   std::vector<uint32_t> segs;       // 2 words per segment
