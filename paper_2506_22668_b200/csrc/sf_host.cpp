@@ -109,11 +109,18 @@ SizePlan plan_sizes(uint32_t n, uint64_t k, bool allow_exhaustive) {
     assigned += q;
     order.emplace_back(-(ideal - double(q)), s);
   }
-  std::sort(order.begin(), order.end());
-  for (size_t i = 0; assigned < total_pairs; ++i) {
-    ++quota[order[i % order.size()].second];
-    ++assigned;
+  // the reference sorts and hands one extra pair to the first R entries,
+  // cycling; only the SET of the first R % size entries matters, so a
+  // selection (same comparator, ties to the smaller size) replaces the sort
+  const uint64_t R = total_pairs - assigned;
+  const uint64_t rounds = R / order.size(), rest = R % order.size();
+  if (rounds)
+    for (uint32_t s = 1; s <= half; ++s) quota[s] += rounds;
+  if (rest) {
+    std::nth_element(order.begin(), order.begin() + (rest - 1), order.end());
+    for (uint64_t i = 0; i < rest; ++i) ++quota[order[i].second];
   }
+  assigned = total_pairs;
   uint64_t next = 0;
   for (uint32_t s = 1; s <= half; ++s) {
     if (quota[s] == 0) continue;
@@ -637,12 +644,16 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     const uint64_t k = o.samples ? o.samples : sf_auto_samples(n);
     comm_barrier(ctx);
     auto t_stage = Clock::now();
+    DebugTimer sdt("sampling");
     const SizePlan plan = plan_sizes(n, k, o.allow_exhaustive != 0);
+    sdt.lap("plan");
     const uint64_t pairs = local_pair_count(plan.total_pairs(), ctx.rank, ctx.world);
     const uint64_t rows = 2 * pairs;
     ctx.masks.reserve(std::max<uint64_t>(rows * W, 1));
     launch_generate_masks(ctx, plan, seed, ctx.rank, ctx.world, ctx.masks.p);
+    sdt.lap("launch");
     comm_barrier(ctx);
+    sdt.lap("masks");
     out->sampling_ms = ms_since(t_stage);
     out->exhaustive = plan.exhaustive ? 1 : 0;
     out->rows = plan.total_pairs() * 2;

@@ -175,3 +175,15 @@ def test_rank_edges_ties_and_signed_zero():
         phi[: n // 3] = rng.standard_normal(n // 3) * 10.0 ** rng.integers(-300, 300, n // 3)
         want = sorted(range(n), key=lambda i: (-phi[i], i))
         assert list(sf.rank_edges(phi)) == want
+
+
+def test_plan_sizes_random_vs_port(port):
+    # sampler.cpp:93-151 largest-remainder quotas (selection instead of a full
+    # sort on the library side; wrap-around when pairs exceed sizes)
+    rng = np.random.default_rng(0)
+    for _ in range(80):
+        n = int(rng.integers(2, 5000))
+        k = int(rng.integers(1, 200000))
+        a, b = sf.plan_sizes(n, k, False), port.plan_sizes(n, k, False)
+        for key in ("sizes", "pairs", "first"):
+            assert np.array_equal(a[key], b[key]), (n, k, key)
