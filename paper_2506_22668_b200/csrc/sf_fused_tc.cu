@@ -48,7 +48,7 @@ constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
 constexpr int kRawStages = 4, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
-constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 6;
+constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 7;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
 constexpr int kBLoadWarp = kMmaWarp + 1;  // one warp, one lane: B tiles from the B bank
 constexpr int kThreads = (kBLoadWarp + 1) * 32;
