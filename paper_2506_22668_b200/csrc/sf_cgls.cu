@@ -657,6 +657,49 @@ __global__ void assemble_kernel(const uint64_t* __restrict__ rows, uint64_t nrow
   }
 }
 
+// warp per pair: assemble_kernel for rows 2j and 2j+1 plus pair_scan_kernel
+// (set bits per row, complement flag), one read of both rows
+__global__ void assemble_pairs_kernel(const uint64_t* __restrict__ rows, uint64_t pairs, uint32_t W,
+                                      uint32_t n, const double* __restrict__ wsize,
+                                      const float* __restrict__ values, double base,
+                                      double* __restrict__ sw, double* __restrict__ tgt,
+                                      int* __restrict__ bad, uint32_t* __restrict__ pop,
+                                      uint8_t* __restrict__ is_comp) {
+  const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= pairs) return;
+  const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  const uint64_t* e = rows + 2 * j * W;
+  const uint64_t* o = e + W;
+  uint32_t pe = 0, po = 0;
+  bool ok = true;
+  for (uint32_t w = lane; w < W; w += 32) {
+    const uint64_t x = e[w], y = o[w];
+    pe += __popcll(x);
+    po += __popcll(y);
+    ok &= (y == ((w == W - 1) ? (~x & tail) : ~x));
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    pe += __shfl_xor_sync(kFull, pe, d);
+    po += __shfl_xor_sync(kFull, po, d);
+  }
+  ok = __all_sync(kFull, ok);
+  if (lane < 2) {
+    const uint64_t row = 2 * j + lane;
+    const uint32_t cnt = lane ? po : pe;
+    if (cnt == 0 || cnt >= n) {
+      atomicMin(bad, row < 0x7fffffffull ? int(row) : 0x7fffffff);
+      sw[row] = 0.0;
+    } else {
+      sw[row] = sqrt(wsize[cnt]);
+    }
+    tgt[row] = double(values[row]) - base;
+    pop[row] = cnt;
+    if (lane == 0) is_comp[j] = ok ? 1 : 0;
+  }
+}
+
 // ---------------------------------------------------------------- Gram
 // G[a][b] = sum_i w_i bit_i(a) bit_i(b) (+ pin), rhs[a] = sum_i w_i t_i bit_i(a)
 __global__ void gram_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
@@ -741,6 +784,17 @@ void launch_assemble(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   SF_LAUNCHED(ctx);
 }
 
+void launch_assemble_pairs(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows, uint32_t W, uint32_t n,
+                           const double* dev_wsize, const float* dev_values, double base, double* dev_sw,
+                           double* dev_targets, int* dev_bad_row, uint32_t* dev_pop, uint8_t* dev_is_comp) {
+  if (rows == 0) return;
+  if (rows % 2) throw DataError("assemble_pairs needs adjacent row pairs");
+  assemble_pairs_kernel<<<blocks_for(rows / 2 * 32), 256, 0, ctx.stream>>>(
+      dev_rows, rows / 2, W, n, dev_wsize, dev_values, base, dev_sw, dev_targets, dev_bad_row, dev_pop,
+      dev_is_comp);
+  SF_LAUNCHED(ctx);
+}
+
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace) {
   if (mode != 0 && mode != 1) throw DataError("solver mode must be 0 (reference protocol) or 1 (fused)");
@@ -774,13 +828,13 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   Scratch sc{ctx.solver_work.p, 0};
   uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
   uint64_t* mto = sc.take<uint64_t>(ptiles * Wp);  // odd rows (non-complement pairs only)
-  uint8_t* is_comp = sc.take<uint8_t>(pairs);
+  uint8_t* is_comp = in.dev_is_comp ? const_cast<uint8_t*>(in.dev_is_comp) : sc.take<uint8_t>(pairs);
   double* r = sc.take<double>(rows);
   double* v = sc.take<double>(rows);
   double* coef_e = sc.take<double>(ptiles * 64);
   double* coef_o = sc.take<double>(ptiles * 64);
   double* dsq = sc.take<double>(fblocks_max);
-  uint32_t* pop = sc.take<uint32_t>(rows);
+  uint32_t* pop = in.dev_pop ? const_cast<uint32_t*>(in.dev_pop) : sc.take<uint32_t>(rows);
   uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + max_nsplits + 4);
   double* kc = sc.take<double>(pairs);
   double* s_part = sc.take<double>((max_splits + max_nsplits + 1) * n);
@@ -813,8 +867,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   DebugTimer dt("cgls");
   launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, 2ull * W);
   if (pairs) {
-    pair_scan_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, pop, is_comp);
-    SF_LAUNCHED(ctx);
+    if (!in.dev_pop || !in.dev_is_comp) {
+      pair_scan_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, pop, is_comp);
+      SF_LAUNCHED(ctx);
+    }
     init_r_kernel<<<blocks_for(rows), 256, 0, st>>>(in.dev_sw, in.dev_targets, rows, r);
     SF_LAUNCHED(ctx);
   }

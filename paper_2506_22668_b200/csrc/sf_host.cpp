@@ -676,8 +676,10 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     d_tgt.reserve(std::max<uint64_t>(rows, 1));
     const int big = 0x7fffffff;
     d_bad.upload(&big, 1, ctx.stream);
-    launch_assemble(ctx, ctx.masks.p, rows, W, n, d_wsize.p, ctx.preds.p, out->base_score, d_sw.p,
-                    d_tgt.p, d_bad.p);
+    ctx.pop_dev.reserve(std::max<uint64_t>(rows, 1));
+    ctx.comp_dev.reserve(std::max<uint64_t>(rows / 2, 1));
+    launch_assemble_pairs(ctx, ctx.masks.p, rows, W, n, d_wsize.p, ctx.preds.p, out->base_score, d_sw.p,
+                          d_tgt.p, d_bad.p, ctx.pop_dev.p, ctx.comp_dev.p);
     ctx.h2d_bytes += wsize.size() * 8 + 4;
     ctx.d2h_bytes += 4;
     int bad = big;
@@ -695,6 +697,8 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     in.constraint_target = out->full_score - out->base_score;
     in.constraint_weight = o.constraint_scale;
     in.global_pair_count = plan.total_pairs();
+    in.dev_pop = ctx.pop_dev.p;
+    in.dev_is_comp = ctx.comp_dev.p;
     DebugTimer("explain").lap("assemble done");
     CglsResult res = cgls_solve(ctx, in, o.tol, o.max_iter, o.solver_mode, false);
     comm_barrier(ctx);

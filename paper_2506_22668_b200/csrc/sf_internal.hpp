@@ -244,6 +244,8 @@ struct Ctx {
   // per-call scratch kept across calls (no allocation on the explain path)
   DevBuf<double> wsize_dev, sw_dev, tgt_dev;
   DevBuf<int> bad_dev;
+  DevBuf<uint32_t> pop_dev;     // set bits per row (assemble_pairs)
+  DevBuf<uint8_t> comp_dev;     // complement flag per pair
   PinnedBuf<double> solver_host;  // CGLS scalars fetched by the host loop
   DevBuf<float> feat_dev, w0_dev; // engine_prepare temporaries (X, W0 for P0 = X W0)
   DevBuf<float> graph_feat;       // device copy of a graph's features (explain path)
@@ -341,6 +343,9 @@ struct CglsInput {
   const double* dev_targets = nullptr; // value - base per local row
   double constraint_target = 0.0, constraint_weight = 0.0;
   uint64_t global_pair_count = 0;
+  // optional, from launch_assemble_pairs: set bits per row, complement flags
+  const uint32_t* dev_pop = nullptr;
+  const uint8_t* dev_is_comp = nullptr;
 };
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
@@ -354,5 +359,12 @@ void launch_assemble(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                      uint32_t W, uint32_t n, const double* dev_wsize,
                      const float* dev_values, double base, double* dev_sw,
                      double* dev_targets, int* dev_bad_row);
+// the same for adjacent row pairs in one read of both rows, also writing the
+// set bits per row and the complement flags the solver needs
+void launch_assemble_pairs(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
+                           uint32_t W, uint32_t n, const double* dev_wsize,
+                           const float* dev_values, double base, double* dev_sw,
+                           double* dev_targets, int* dev_bad_row, uint32_t* dev_pop,
+                           uint8_t* dev_is_comp);
 
 }  // namespace sfb
