@@ -252,6 +252,7 @@ static Subgraph extract(const Graph& g, uint32_t target, int hops, bool with_fea
   // with edge_player, feature slice.
   if (target >= g.num_nodes) throw DataError("target node " + std::to_string(target) + " out of range");
   if (hops < 0) throw DataError("hop count must be nonnegative");
+  DebugTimer dt("extract");
   std::vector<uint32_t> local_of(g.num_nodes, 0xFFFFFFFFu);
   Subgraph sg;
   sg.target_global = target;
@@ -274,20 +275,39 @@ static Subgraph extract(const Graph& g, uint32_t target, int hops, bool with_fea
     }
     fb = fe;
   }
+  dt.lap("bfs");
   const uint32_t V = sg.num_nodes();
-  // lexicographic (lu, lv) order: lu ascending by construction, each node's
-  // lv sorted locally (the global sort of all pairs cost ~2 ms at C2)
-  std::vector<uint32_t> nbr;
-  for (uint32_t lu = 0; lu < V; ++lu) {
-    const uint32_t u = sg.local_to_global[lu];
-    nbr.clear();
-    for (uint64_t k = g.row_ptr[u]; k < g.row_ptr[u + 1]; ++k) {
-      const uint32_t lv = local_of[g.col[k]];
-      if (lv != 0xFFFFFFFFu && lu < lv) nbr.push_back(lv);
+  // lexicographic (lu, lv) order without a sort: walking the larger
+  // endpoint lv in ascending order and appending it to bucket lu fills every
+  // bucket in ascending lv; buckets laid out in lu order (counting pass
+  // first). Multi-edges stay adjacent, as after a sort.
+  // (branch-free: the lu < lv test is a coin flip per entry; rejected
+  // entries go to a dummy bucket V whose cursor never moves)
+  std::vector<uint64_t> bstart(size_t(V) + 2, 0);
+  for (uint32_t lv = 0; lv < V; ++lv) {
+    const uint32_t v = sg.local_to_global[lv];
+    for (uint64_t k = g.row_ptr[v]; k < g.row_ptr[v + 1]; ++k) {
+      const uint32_t lu = local_of[g.col[k]];  // unmapped ids are 0xFFFFFFFF > lv
+      const bool keep = lu < lv;
+      bstart[(keep ? lu : V) + 1] += keep;
     }
-    std::sort(nbr.begin(), nbr.end());
-    for (const uint32_t lv : nbr) sg.players.emplace_back(lu, lv);
   }
+  for (uint32_t u = 0; u < V; ++u) bstart[u + 1] += bstart[u];
+  const uint64_t total = bstart[V];
+  bstart[V] = total;  // the dummy bucket's cursor: one scratch slot past the end
+  sg.players.resize(total + 1);
+  for (uint32_t lv = 0; lv < V; ++lv) {
+    const uint32_t v = sg.local_to_global[lv];
+    for (uint64_t k = g.row_ptr[v]; k < g.row_ptr[v + 1]; ++k) {
+      const uint32_t lu = local_of[g.col[k]];
+      const bool keep = lu < lv;
+      uint64_t& cur = bstart[keep ? lu : V];
+      sg.players[cur] = {lu, lv};
+      cur += keep;
+    }
+  }
+  sg.players.pop_back();
+  dt.lap("edges");
   std::vector<uint64_t> deg(V, 0);
   for (const auto& [u, v] : sg.players) {
     deg[u]++;
@@ -305,6 +325,7 @@ static Subgraph extract(const Graph& g, uint32_t target, int hops, bool with_fea
     sg.col[cursor[v]] = u;
     sg.edge_player[cursor[v]++] = e;
   }
+  dt.lap("csr");
   if (!with_features) {  // the engine gathers the rows from a device copy of the graph's features
     sg.source = &g;
     return sg;
@@ -593,6 +614,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
   DebugTimer("explain").lap("start");
   const Subgraph sg = extract(g, node, m.depth(), false);
   out->extract_ms = ms_since(t_start);
+  DebugTimer("explain").lap("extracted");
   const uint64_t n_raw = sg.num_players();
   if (o.player_cap != 0 && n_raw > o.player_cap) {
     out->skipped = 1;
