@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(256)
       chi += __popc(bfly32(uint32_t(x >> 32)));
     }
     float* out = isd + (t * V + u) * kTile;
-    out[lane] = __ldg(&tab[clo]);
-    out[lane + 32] = __ldg(&tab[chi]);
+    __stcs(&out[lane], __ldg(&tab[clo]));
+    __stcs(&out[lane + 32], __ldg(&tab[chi]));
     if (deg16) {
       uint16_t* o16 = deg16 + (t * V + u) * kTile;
       o16[lane] = uint16_t(min(clo, 0xFFFFu));
@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(256)
         const uint32_t sh = q << lg;
         float* out = isd + (uint64_t(tb + q) * V + u) * kTile;
         const uint32_t dlo = 1 + __popc((lo >> sh) & fmask), dhi = 1 + __popc((hi >> sh) & fmask);
-        out[lane] = __ldg(&tab[dlo]);
-        out[lane + 32] = __ldg(&tab[dhi]);
+        __stcs(&out[lane], __ldg(&tab[dlo]));
+        __stcs(&out[lane + 32], __ldg(&tab[dhi]));
         if (deg16) {
           uint16_t* o16 = deg16 + (uint64_t(tb + q) * V + u) * kTile;
           o16[lane] = uint16_t(dlo);

@@ -254,7 +254,7 @@ __device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t keep, 
   return (x & keep) | __shfl_xor_sync(kFull, send, s);
 }
 
-constexpr int kTWords = 16;  // words per CTA (a multiple of 8: one or more per warp)
+constexpr int kTWords = 32;  // words per CTA (a multiple of 8: one or more per warp)
 
 __global__ void __launch_bounds__(256)
     transpose_tiles_kernel(const uint64_t* __restrict__ in, uint64_t rows,
