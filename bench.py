@@ -427,7 +427,7 @@ def run_batch(args):
         if dist is not None:
             dist.barrier()
 
-    ctx.explain_nodes(g, m, mine[: min(len(mine), 8)], opts)  # warm-up (allocations)
+    ctx.explain_nodes(g, m, mine, opts)  # warm-up pass over the batch (buffers grow to the largest target)
     times, players = [], 0
     for _ in range(args.steps):
         barrier()
@@ -436,6 +436,8 @@ def run_batch(args):
         barrier()
         times.append(time.perf_counter() - t0)
         players = sum(len(e.phi) for e in ex)
+    if rank == 0:
+        print("c5 step seconds", [round(x, 3) for x in times], file=sys.stderr, flush=True)
     dt = float(np.median(times))
     if dist is not None:
         import torch
