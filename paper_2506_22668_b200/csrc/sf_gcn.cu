@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(256)
                const uint32_t* __restrict__ row_ptr,
                const uint32_t* __restrict__ ep, const uint32_t* __restrict__ order,
                uint32_t nbig, const float* __restrict__ tab, uint32_t V,
-               float* __restrict__ isd, uint16_t* __restrict__ deg16) {
+               float* __restrict__ isd, uint16_t* __restrict__ deg16,
+               uint32_t tsplit, uint32_t tchunk) {
   const int lane = threadIdx.x & 31;
   const Bfly bfly32(lane);
   const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -105,13 +106,17 @@ __global__ void __launch_bounds__(256)
     }
     return;
   }
-  const uint32_t j = nbig + (w - big_warps);
+  // small nodes: warp per (node, chunk of tchunk tiles); tsplit chunks per
+  // node so that few-node subgraphs still fill the GPU
+  const uint32_t j = nbig + (w - big_warps) / tsplit;
   if (j >= V) return;
+  const uint32_t tb0 = ((w - big_warps) % tsplit) * tchunk;
+  const uint32_t te = min(ntiles, tb0 + tchunk);
   const uint32_t u = order[j];
   const uint32_t beg = row_ptr[u], deg = row_ptr[u + 1] - beg;
   if (deg == 0) {
     const float one = __ldg(&tab[1]);
-    for (uint32_t t = 0; t < ntiles; ++t) {
+    for (uint32_t t = tb0; t < te; ++t) {
       float* out = isd + (uint64_t(t) * V + u) * kTile;
       out[lane] = one;
       out[lane + 32] = one;
@@ -130,19 +135,19 @@ __global__ void __launch_bounds__(256)
   // kIsdAhead groups of `per` tiles per step: their mask words are all in
   // flight before the first transpose (the loop is latency-bound otherwise)
   constexpr int kIsdAhead = 4;
-  for (uint32_t t0 = 0; t0 < ntiles; t0 += kIsdAhead * per) {
+  for (uint32_t t0 = tb0; t0 < te; t0 += kIsdAhead * per) {
     uint64_t xs[kIsdAhead];
 #pragma unroll
     for (int k = 0; k < kIsdAhead; ++k) {
       const uint32_t t = t0 + k * per + sub;
-      xs[k] = (slot < deg && t < ntiles) ? __ldg(&maskt[uint64_t(t) * Wp + p]) : 0ull;
+      xs[k] = (slot < deg && t < te) ? __ldg(&maskt[uint64_t(t) * Wp + p]) : 0ull;
     }
 #pragma unroll
     for (int k = 0; k < kIsdAhead; ++k) {
       const uint32_t tb = t0 + k * per;
-      if (tb >= ntiles) break;  // warp-uniform
+      if (tb >= te) break;  // warp-uniform
       const uint32_t lo = bfly32(uint32_t(xs[k])), hi = bfly32(uint32_t(xs[k] >> 32));
-      for (uint32_t q = 0; q < per && tb + q < ntiles; ++q) {
+      for (uint32_t q = 0; q < per && tb + q < te; ++q) {
         const uint32_t sh = q << lg;
         float* out = isd + (uint64_t(tb + q) * V + u) * kTile;
         const uint32_t dlo = 1 + __popc((lo >> sh) & fmask), dhi = 1 + __popc((hi >> sh) & fmask);
@@ -1120,10 +1125,20 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
     const uint64_t ntp = wide ? (nt + 1) & ~uint64_t(1) : nt;  // tiles the fused kernel covers
     launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, ntp, maskt);
     {
-      const uint64_t warps = uint64_t(e.isd_nbig) * ntp + (e.V - e.isd_nbig);
+      // small-node warps: split the tiles when there are too few nodes to
+      // fill 148 SMs x 64 warps (chunks of a multiple of 32 tiles)
+      const uint64_t small = e.V - e.isd_nbig;
+      uint64_t tchunk = ntp;
+      if (small && small < 148ull * 64) {
+        const uint64_t want = (148ull * 64 + small - 1) / small;
+        tchunk = std::max<uint64_t>(32, ((ntp + want - 1) / want + 31) / 32 * 32);
+        tchunk = std::min(tchunk, ntp);
+      }
+      const uint64_t tsplit = (ntp + tchunk - 1) / tchunk;
+      const uint64_t warps = uint64_t(e.isd_nbig) * ntp + small * tsplit;
       isd_kernel<<<unsigned((warps + 7) / 8), 256, 0, ctx.stream>>>(
           maskt, Wp, uint32_t(ntp), e.row_ptr.p, e.edge_player.p, e.isd_order.p, e.isd_nbig,
-          e.isd_tab.p, e.V, isd, deg16);
+          e.isd_tab.p, e.V, isd, deg16, uint32_t(tsplit), uint32_t(tchunk));
       SF_LAUNCHED(ctx);
     }
     const float* X = e.p0.p;  // current layer input: P0 (shared) or per-coalition H
