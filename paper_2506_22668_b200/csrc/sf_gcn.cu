@@ -1171,9 +1171,11 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
       if (L <= 3) {  // fused tail: reduce + layer 1 + last layer + softmax in one kernel
         // coalitions per CTA: 16 when the tile fits (the weights are staged
-        // once per CTA; 16 measured 49.1 vs 50.5 ms/step for 4 at C2)
-        static const uint32_t cpb0 = std::getenv("SF_TAIL_CPB") ? uint32_t(std::atoi(std::getenv("SF_TAIL_CPB"))) : 16u;
-        uint32_t cpb = cpb0;
+        // once per CTA; 16 measured 49.1 vs 50.5 ms/step for 4 at C2); the
+        // whole tile when U == 1 (2-layer: little work per coalition, C5
+        // 2.40 -> 2.28 s per 1,024-target batch)
+        static const uint32_t cpb_env = std::getenv("SF_TAIL_CPB") ? uint32_t(std::atoi(std::getenv("SF_TAIL_CPB"))) : 0u;
+        uint32_t cpb = cpb_env ? cpb_env : (e.U == 1 ? uint32_t(kTile) : 16u);
         while (cpb > 1 && tail_smem(e.U, K, N, C, cpb, L == 3) > kTailSmem) cpb /= 2;
         if (tail_smem(e.U, K, N, C, cpb, L == 3) <= kTailSmem) {
           const size_t smem = tail_smem(e.U, K, N, C, cpb, L == 3);
