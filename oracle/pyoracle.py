@@ -461,6 +461,24 @@ class Port:
             raise OracleError(rc, "cgls failed")
         return phi, it.value, res.value, bool(conv.value)
 
+    def cgls_sparse(self, n, bits, rows_of_size, values, base, full, cscale=1e6, tol=1e-6, max_iter=0,
+                    threads=None):
+        """port_cgls_sparse: the bit-row CGLS for large k x n (set-bit passes,
+        pthreads), agreeing with port_cgls / the reference to rounding."""
+        bits = np.ascontiguousarray(bits, np.uint64)
+        values = np.ascontiguousarray(values, np.float64)
+        ros = np.ascontiguousarray(rows_of_size, np.uint64)
+        threads = threads or min(64, os.cpu_count() or 1)
+        phi = np.zeros(n, np.float64)
+        it, res, conv = C.c_uint64(), C.c_double(), C.c_int()
+        rc = self.L.port_cgls_sparse(C.c_uint32(n), _p(bits), C.c_uint64(bits.shape[0]), C.c_uint64(bits.shape[1]),
+                                     _p(ros), _p(values), C.c_double(base), C.c_double(full), C.c_double(cscale),
+                                     C.c_double(tol), C.c_uint64(max_iter), C.c_int(threads), _p(phi),
+                                     C.byref(it), C.byref(res), C.byref(conv))
+        if rc:
+            raise OracleError(rc, "cgls_sparse failed")
+        return phi, it.value, res.value, bool(conv.value)
+
     def rank_edges(self, phi):
         phi = np.ascontiguousarray(phi, np.float64)
         order = np.zeros(len(phi), np.uint32)

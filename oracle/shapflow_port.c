@@ -627,3 +627,252 @@ void port_rank_edges(const double* phi, uint32_t n, uint32_t* order) {
   g_rank_phi = phi;
   qsort(order, n, sizeof(uint32_t), rank_cmp);
 }
+
+/* ------------------------------------------------------------ CGLS, large k·n
+ * The same algorithm as port_cgls (solver.cpp:158-362: assemble weights
+ * 125-138, targets 153, pin row 111-112, complement fast paths 209-223 and
+ * 261-263, stop rule / blow-up / non-finite checks 289-360) for shapes where
+ * the dense leaves of the fixed-order tree are infeasible (C2: 250K pairs x
+ * 50K players). Differences from port_cgls, all inside the 1e-3 parity bar:
+ *   - sums over pairs run in per-thread blocks folded in thread order (not the
+ *     PairwiseFolder tree), so results agree with port_cgls / the reference to
+ *     rounding (tests/test_oracle_port.py pins this at ~1e-12);
+ *   - M^T r visits only the set bits of each pair's even row:
+ *     s_i = sum_j co_j + sum_{j : bit_e(i)} (ce_j - co_j) for complement pairs
+ *     (the reference's leaf co + beta * bit, solver.cpp:209-217).
+ * `threads` worker threads (pthreads); rows of size 0 or n are a DataError. */
+#include <pthread.h>
+
+typedef struct {
+  uint32_t n;
+  const uint64_t* bits;
+  uint64_t words, pl, j0, j1;
+  const double* sw;
+  const double* r;
+  double* v;
+  const uint8_t* is_comp;
+  const double* u;
+  double sum_u;
+  double* s_part; /* n doubles: this thread's transpose partial */
+  double acc;     /* this thread's scalar partial */
+  int op;         /* 0 forward, 1 transpose */
+} cg_task;
+
+static void* cg_worker(void* arg) {
+  cg_task* t = (cg_task*)arg;
+  const uint64_t W = t->words;
+  if (t->op == 0) {
+    double acc = 0.0;
+    for (uint64_t j = t->j0; j < t->j1; ++j) {
+      const uint64_t e = 2 * j;
+      const uint64_t* re = t->bits + e * W;
+      double dot = 0.0;
+      for (uint64_t w = 0; w < W; ++w)
+        for (uint64_t x = re[w]; x; x &= x - 1) dot += t->u[w * 64 + (uint64_t)__builtin_ctzll(x)];
+      t->v[e] = t->sw[e] * dot;
+      if (t->is_comp[j]) {
+        t->v[e + 1] = t->sw[e + 1] * (t->sum_u - dot);
+      } else {
+        const uint64_t* ro = re + W;
+        double d2 = 0.0;
+        for (uint64_t w = 0; w < W; ++w)
+          for (uint64_t x = ro[w]; x; x &= x - 1) d2 += t->u[w * 64 + (uint64_t)__builtin_ctzll(x)];
+        t->v[e + 1] = t->sw[e + 1] * d2;
+      }
+      acc += t->v[e] * t->v[e] + t->v[e + 1] * t->v[e + 1];
+    }
+    t->acc = acc;
+  } else {
+    double* s = t->s_part;
+    memset(s, 0, sizeof(double) * t->n);
+    double cbase = 0.0;
+    for (uint64_t j = t->j0; j < t->j1; ++j) {
+      const uint64_t e = 2 * j;
+      const double ce = t->sw[e] * t->r[e], co = t->sw[e + 1] * t->r[e + 1];
+      const uint64_t* re = t->bits + e * W;
+      if (t->is_comp[j]) {
+        cbase += co;
+        const double beta = ce - co;
+        for (uint64_t w = 0; w < W; ++w)
+          for (uint64_t x = re[w]; x; x &= x - 1) s[w * 64 + (uint64_t)__builtin_ctzll(x)] += beta;
+      } else {
+        const uint64_t* ro = re + W;
+        for (uint64_t w = 0; w < W; ++w) {
+          for (uint64_t x = re[w]; x; x &= x - 1) s[w * 64 + (uint64_t)__builtin_ctzll(x)] += ce;
+          for (uint64_t x = ro[w]; x; x &= x - 1) s[w * 64 + (uint64_t)__builtin_ctzll(x)] += co;
+        }
+      }
+    }
+    t->acc = cbase;
+  }
+  return NULL;
+}
+
+static void cg_run(cg_task* tasks, int threads) {
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  for (int i = 1; i < threads; ++i) pthread_create(&th[i], NULL, cg_worker, &tasks[i]);
+  cg_worker(&tasks[0]);
+  for (int i = 1; i < threads; ++i) pthread_join(th[i], NULL);
+  free(th);
+}
+
+int port_cgls_sparse(uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
+                     const uint64_t* rows_of_size, const double* values, double base, double full,
+                     double cscale, double tol, uint64_t max_iter, int threads, double* phi,
+                     uint64_t* iters_out, double* resid_out, int* converged_out) {
+  *iters_out = 0;
+  *resid_out = 0.0;
+  *converged_out = 0;
+  memset(phi, 0, sizeof(double) * n);
+  if (n == 0) {
+    *converged_out = 1;
+    return 0;
+  }
+  if (rows % 2) return 2;
+  if (threads < 1) threads = 1;
+  double* wsize = (double*)calloc(n + 1, sizeof(double));
+  double scale = 0.0;
+  for (uint32_t sz = 1; sz < n; ++sz) {
+    if (rows_of_size[sz] == 0) continue;
+    const double rho = (n - 1.0) / ((double)sz * (double)(n - sz));
+    const double w = rho / (double)rows_of_size[sz];
+    if (scale == 0.0) scale = w;
+    wsize[sz] = w / scale;
+  }
+  const uint64_t pl = rows / 2;
+  double* sw = (double*)malloc(sizeof(double) * (rows ? rows : 1));
+  double* r = (double*)malloc(sizeof(double) * (rows ? rows : 1));
+  double* v = (double*)malloc(sizeof(double) * (rows ? rows : 1));
+  uint8_t* is_comp = (uint8_t*)malloc(pl ? pl : 1);
+  double* s = (double*)calloc(n, sizeof(double));
+  double* u = (double*)calloc(n, sizeof(double));
+  double* parts = (double*)malloc(sizeof(double) * (size_t)n * (size_t)threads);
+  cg_task* tasks = (cg_task*)calloc((size_t)threads, sizeof(cg_task));
+  int rc = 0;
+  const uint64_t tail = (n % 64) ? (((uint64_t)1 << (n % 64)) - 1) : ~0ull;
+  for (uint64_t i = 0; i < rows; ++i) {
+    uint64_t size = 0;
+    for (uint64_t w = 0; w < words; ++w) size += (uint64_t)__builtin_popcountll(bits[i * words + w]);
+    if (size == 0 || size >= n) rc = 2;
+    sw[i] = sqrt(wsize[size < n ? size : 0]);
+    r[i] = sw[i] * (values[i] - base);
+  }
+  for (uint64_t j = 0; j < pl; ++j) {
+    const uint64_t* e = bits + 2 * j * words;
+    const uint64_t* o = e + words;
+    is_comp[j] = 1;
+    for (uint64_t w = 0; w < words; ++w) {
+      uint64_t want = ~e[w];
+      if (w == words - 1) want &= tail;
+      if (o[w] != want) is_comp[j] = 0;
+    }
+  }
+  for (int t = 0; t < threads; ++t) {
+    tasks[t].n = n;
+    tasks[t].bits = bits;
+    tasks[t].words = words;
+    tasks[t].pl = pl;
+    tasks[t].j0 = pl * (uint64_t)t / (uint64_t)threads;
+    tasks[t].j1 = pl * (uint64_t)(t + 1) / (uint64_t)threads;
+    tasks[t].sw = sw;
+    tasks[t].r = r;
+    tasks[t].v = v;
+    tasks[t].is_comp = is_comp;
+    tasks[t].u = u;
+    tasks[t].s_part = parts + (size_t)n * (size_t)t;
+  }
+  const double sc = sqrt(cscale);
+  double r_c = sc * (full - base);
+  if (rc) goto done;
+
+#define SPARSE_TRANSPOSE()                                                 \
+  do {                                                                     \
+    for (int t_ = 0; t_ < threads; ++t_) tasks[t_].op = 1;                 \
+    cg_run(tasks, threads);                                                \
+    double cb_ = 0.0;                                                      \
+    for (int t_ = 0; t_ < threads; ++t_) cb_ += tasks[t_].acc;             \
+    const double pin_ = sc * r_c;                                          \
+    for (uint32_t i = 0; i < n; ++i) {                                     \
+      double x_ = 0.0;                                                     \
+      for (int t_ = 0; t_ < threads; ++t_) x_ += parts[(size_t)n * t_ + i]; \
+      s[i] = (cb_ + x_) + pin_;                                            \
+    }                                                                      \
+  } while (0)
+
+  SPARSE_TRANSPOSE();
+  double gamma = 0.0;
+  for (uint32_t i = 0; i < n; ++i) gamma += s[i] * s[i];
+  const double gamma0 = gamma;
+  if (gamma0 == 0.0) {
+    *converged_out = 1;
+    goto done;
+  }
+  double data0 = 0.0;
+  {
+    const double pin = sc * r_c;
+    for (uint32_t i = 0; i < n; ++i) {
+      const double d = s[i] - pin;
+      data0 += d * d;
+    }
+  }
+  const double reference = data0 > 0.0 ? data0 : gamma0;
+  double rel = sqrt(gamma0 / reference);
+  memcpy(u, s, sizeof(double) * n);
+  const double blowup = 1.0e12 * (rel > 1.0 ? rel : 1.0);
+  const uint64_t maxit = max_iter ? max_iter : (n < 5000 ? n : 5000);
+  uint64_t it = 0;
+  int conv = 0;
+  while (it < maxit) {
+    double sum_u = 0.0;
+    for (uint32_t i = 0; i < n; ++i) sum_u += u[i];
+    for (int t = 0; t < threads; ++t) {
+      tasks[t].op = 0;
+      tasks[t].sum_u = sum_u;
+    }
+    cg_run(tasks, threads);
+    double delta = 0.0;
+    for (int t = 0; t < threads; ++t) delta += tasks[t].acc;
+    const double v_c = sc * sum_u;
+    delta += v_c * v_c;
+    if (!isfinite(delta)) {
+      rc = 3;
+      break;
+    }
+    if (delta <= 0.0) break;
+    const double theta = gamma / delta;
+    for (uint32_t i = 0; i < n; ++i) phi[i] += theta * u[i];
+    for (uint64_t i = 0; i < rows; ++i) r[i] -= theta * v[i];
+    r_c -= theta * v_c;
+    SPARSE_TRANSPOSE();
+    double gn = 0.0;
+    for (uint32_t i = 0; i < n; ++i) gn += s[i] * s[i];
+    ++it;
+    rel = sqrt(gn / reference);
+    if (!isfinite(gn) || rel > blowup) {
+      rc = 3;
+      break;
+    }
+    if (rel <= tol) {
+      conv = 1;
+      break;
+    }
+    const double beta = gn / gamma;
+    for (uint32_t i = 0; i < n; ++i) u[i] = s[i] + beta * u[i];
+    gamma = gn;
+  }
+  *iters_out = it;
+  *resid_out = rel;
+  *converged_out = conv;
+#undef SPARSE_TRANSPOSE
+done:
+  free(wsize);
+  free(sw);
+  free(r);
+  free(v);
+  free(is_comp);
+  free(s);
+  free(u);
+  free(parts);
+  free(tasks);
+  return rc;
+}

@@ -1068,7 +1068,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   // out = M^T (sw x) (+ the pair constants); x = r (reference protocol) or
   // v (fused mode, coefficients sw * v). Local: no collective here.
   auto transpose_local = [&](const double* x, double* out) {
-    SF_CUDA(cudaMemsetAsync(kc, 0, pairs * 8 + 8, st));
+    SF_CUDA(cudaMemsetAsync(kc, 0, std::max<uint64_t>(pairs, 1) * 8, st));
     if (pairs) {
       coef_kernel<<<blocks_for(ptiles * 64), 256, 0, st>>>(in.dev_sw, x, is_comp, pairs, ptiles * 64,
                                                           coef_e, coef_o, kc);

@@ -7,10 +7,24 @@
 #include <dlfcn.h>
 
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "sf_internal.hpp"
 
 namespace sfb {
+
+void set_max_dynamic_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  SF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kernel, dev, bytes})) return;
+  SF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({kernel, dev, bytes});
+}
 
 namespace {
 // nccl.h (2.27/2.28): ncclUniqueId is 128 bytes, ncclFloat64 = 8, ncclSum = 0

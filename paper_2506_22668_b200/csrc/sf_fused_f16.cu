@@ -498,12 +498,7 @@ template <int D, bool PROF>
 void launch_f16_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
                      const uint16_t* deg16, uint64_t ntp, float* apart, unsigned long long* prof) {
   using Cfg = F16Cfg<D>;
-  static bool configured = false;
-  if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_f16_kernel<D, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM + kTabCap * 4));
-    configured = true;
-  }
+  set_max_dynamic_smem(fused_f16_kernel<D, PROF>, int(Cfg::SMEM + kTabCap * 4));
   const size_t smem = Cfg::SMEM + size_t(e.isd_tab_n) * 4;
   const uint32_t npairs = uint32_t(ntp / 2), units = e.tc_items * npairs;
   fused_f16_kernel<D, PROF><<<units, kThreads, smem, ctx.stream>>>(

@@ -479,12 +479,7 @@ template <int D, bool PROF>
 void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
                     const uint16_t* deg16, uint64_t ntp, float* apart, unsigned long long* prof) {
   using Cfg = TcCfg<D>;
-  static bool configured = false;
-  if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_tc_kernel<D, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM));
-    configured = true;
-  }
+  set_max_dynamic_smem(fused_tc_kernel<D, PROF>, int(Cfg::SMEM));
   const size_t smem = Cfg::SMEM;
   dim3 grid(e.tc_items, unsigned(ntp / 2));
   fused_tc_kernel<D, PROF><<<grid, kThreads, smem, ctx.stream>>>(

@@ -13,7 +13,8 @@
 // the (L-1-l)-hop ball, which is a prefix of the BFS-ordered local ids; the
 // last layer produces only the target row (gcn.cpp:134-140).
 //
-// Arithmetic: FP32 on the CUDA cores (SIMT FFMA), accuracy mode "FP32".
+// Arithmetic: FP32 (FFMA) in the SIMT kernels of this file; the default
+// layer-0 path is the tcgen05 3xTF32 kernel in sf_fused_tc.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -895,14 +896,10 @@ bool try_fused(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
                uint64_t nt, float* apart) {
   if (e.dims[1] != uint64_t(D)) return false;
   using Cfg = FusedCfg<D>;
-  static bool configured = false;
-  if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    // two CTAs per SM need the maximum shared-memory carveout
-    SF_CUDA(cudaFuncSetAttribute(fused_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 int(cudaSharedmemCarveoutMaxShared)));
-    configured = true;
-  }
+  set_max_dynamic_smem(fused_kernel<D>, int(Cfg::SMEM));
+  // two CTAs per SM need the maximum shared-memory carveout
+  SF_CUDA(cudaFuncSetAttribute(fused_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               int(cudaSharedmemCarveoutMaxShared)));
   dim3 grid(e.items, unsigned(nt));
   fused_kernel<D><<<grid, kConsumers + 32, Cfg::SMEM, ctx.stream>>>(
       maskt, Wp, isd, e.V, e.p0.p, e.b[0]->p, reinterpret_cast<const uint4*>(e.ent.p), e.item_ent.p,
@@ -1179,12 +1176,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         while (cpb > 1 && tail_smem(e.U, K, N, C, cpb, L == 3) > kTailSmem) cpb /= 2;
         if (tail_smem(e.U, K, N, C, cpb, L == 3) <= kTailSmem) {
           const size_t smem = tail_smem(e.U, K, N, C, cpb, L == 3);
-          static bool attr = false;
-          if (!attr) {
-            SF_CUDA(cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kTailSmem)));
-            attr = true;
-          }
+          set_max_dynamic_smem(tail_kernel, int(kTailSmem));
           dim3 grid(unsigned(nt), kTile / cpb);
           tail_kernel<<<grid, kTailThreads, smem, ctx.stream>>>(
               reinterpret_cast<const float4*>(pbuf), e.tc ? e.tc_items : e.items,

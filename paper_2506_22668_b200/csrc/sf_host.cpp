@@ -1360,12 +1360,9 @@ static void solve_common(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t
   if (rows && words < W) throw DataError("rows narrower than the player count");
   SF_CUDA(cudaSetDevice(ctx->c.device));
   std::vector<double> sw(rows);
-  for (uint64_t i = 0; i < rows; ++i) {
-    sw[i] = std::sqrt(weights[i]);
-    if (!std::isfinite(targets[i]) || !std::isfinite(sw[i])) {
-      // surfaces as a non-finite step norm exactly like the reference
-    }
-  }
+  // non-finite weights/targets are passed through: like the reference they
+  // surface as a non-finite step norm (NumericalError) inside the solve
+  for (uint64_t i = 0; i < rows; ++i) sw[i] = std::sqrt(weights[i]);
   upload_rows(ctx->c, bits, rows, words, std::max<uint32_t>(W, 1));
   d_sw.upload(sw.data(), rows, ctx->c.stream);
   d_tgt.upload(targets, rows, ctx->c.stream);

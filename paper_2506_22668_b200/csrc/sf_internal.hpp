@@ -47,6 +47,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file,
     (ctx).launches++;                                                     \
   } while (0)
 
+// cudaFuncSetAttribute applies to the current device only; remember which
+// (kernel, device, bytes) combinations are set so one process can drive
+// several devices (thread-per-GPU ranks).
+void set_max_dynamic_smem(const void* kernel, int bytes);
+template <class K>
+inline void set_max_dynamic_smem(K* kernel, int bytes) {
+  set_max_dynamic_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 inline uint64_t next_object_id() {
   static std::atomic<uint64_t> id{1};
   return id++;

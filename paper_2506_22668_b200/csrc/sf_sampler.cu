@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kSamplerWarps * 32)
   const int lane = threadIdx.x & 31;
   const uint64_t j = blockIdx.x * uint64_t(kSamplerWarps) + (threadIdx.x >> 5);
   if (j >= jobs) return;
-  const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  const uint64_t tail = n == 0 ? 0ull : (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
   uint64_t* row = rows + j * W;
   uint64_t* bits = kSmem ? smem_sets + size_t(threadIdx.x >> 5) * W : row;
   for (uint32_t w = lane; w < W; w += 32) bits[w] = 0;
@@ -369,7 +369,8 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
                        const uint8_t* dev_invert, uint64_t jobs,
                        uint64_t* dev_rows) {
   if (jobs == 0) return;
-  const uint32_t W = (n + 63) / 64;
+  // same row stride as the caller's mask layout (one word even when n == 0)
+  const uint32_t W = std::max<uint32_t>((n + 63) / 64, 1);
   const unsigned grid = unsigned((jobs + kSamplerWarps - 1) / kSamplerWarps);
   const size_t smem = size_t(kSamplerWarps) * W * 8;
   if (smem <= 200 * 1024) {  // the set in shared memory (one row per warp)

@@ -124,6 +124,33 @@ def test_cgls_port_vs_reference(port, ref):
         assert (a[0] == b[0]).all()
 
 
+def test_cgls_sparse_vs_reference(port, ref):
+    """port_cgls_sparse (the large-shape checker used by the C2/C3/C5 parity
+    tests) agrees with the compiled reference solve_cgls to rounding, for any
+    thread count, on complement pairs and on non-complement (user) rows."""
+    for n, k, seed in [(40, 3000, 3), (200, 4000, 9), (1000, 6000, 21)]:
+        p = port.plan_sizes(n, k, False)
+        bits = port.generate_masks(n, p, seed)
+        ros = port.rows_of_size(n, p)
+        vals = np.sin(np.arange(bits.shape[0]) * 0.37) * 0.5 + 0.5
+        a = ref.solve_cgls(n, bits, vals, 0.25, 0.75, max_iter=4 * n)
+        for threads in (1, 3, 8):
+            b = port.cgls_sparse(n, bits, ros, vals, 0.25, 0.75, max_iter=4 * n, threads=threads)
+            # same stop rule; near tol the rounding can move the stop by a few iterations
+            assert b[3] == a[3] and abs(b[1] - a[1]) <= max(3, a[1] // 10)
+            assert np.linalg.norm(b[0] - a[0]) <= 1e-8 * np.linalg.norm(a[0])
+    # non-complement rows: swap the odd rows of two pairs
+    n, k = 64, 2000
+    p = port.plan_sizes(n, k, False)
+    bits = port.generate_masks(n, p, 5).copy()
+    bits[[1, 3]] = bits[[3, 1]]
+    vals = np.cos(np.arange(bits.shape[0]) * 0.11) * 0.5 + 0.5
+    ros = port.rows_of_size(n, p)
+    a = ref.solve_cgls(n, bits, vals, 0.1, 0.9, max_iter=4 * n)
+    b = port.cgls_sparse(n, bits, ros, vals, 0.1, 0.9, max_iter=4 * n, threads=4)
+    assert np.linalg.norm(b[0] - a[0]) <= 1e-8 * np.linalg.norm(a[0])
+
+
 def test_rank_edges_ties(port):
     # test_solver.cpp:278-286
     assert port.rank_edges(np.array([0.5, 0.7, 0.5, -1.0])).tolist() == [1, 0, 2, 3]
