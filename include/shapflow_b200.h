@@ -51,6 +51,19 @@ int sf_ctx_world(const sf_ctx* ctx);
 int sf_nccl_unique_id(void* out_128_bytes);
 int sf_ctx_join_nccl(sf_ctx* ctx, const void* unique_id_128, int rank,
                      int world);
+/* A caller-provided communicator instead of NCCL (the reference's
+ * Communicator behind the ABI: thread or socket workers, comm.hpp:28-52).
+ * all_reduce sums `count` doubles in place across ranks, barrier waits for
+ * every rank; both return 0 on success. The library stages device buffers
+ * through pinned host memory for each call. Replaces any NCCL communicator. */
+int sf_ctx_set_host_comm(sf_ctx* ctx, int rank, int world, void* user,
+                         int (*all_reduce)(void* user, double* buf,
+                                           uint64_t count),
+                         int (*barrier)(void* user));
+/* Bound on a collective's wait (default 60000 ms, the reference's
+ * kDefaultCommTimeout, comm.hpp:54). A rank that never joins aborts the NCCL
+ * communicator and the call fails with SF_ERR_PROTOCOL. */
+int sf_ctx_set_comm_timeout(sf_ctx* ctx, int timeout_ms);
 /* CollectiveStats (comm.hpp:13-19) */
 int sf_ctx_stats(const sf_ctx* ctx, uint64_t* scalar_allreduce,
                  uint64_t* vector_allreduce, uint64_t* barriers,
@@ -86,6 +99,14 @@ int sf_ctx_fused_plan(const sf_ctx* ctx, uint64_t* entries,
 int sf_ctx_time_dominant(sf_ctx* ctx, int enable);
 int sf_ctx_dominant_stats(sf_ctx* ctx, double* total_ms, uint64_t* launches,
                           uint64_t* pairs);
+/* Stage outputs for stage-wise parity checks (no reference counterpart;
+ * the reference's explain.cpp:100-102 keeps its predictions in a local):
+ * with keep on, sf_explain_node retains this rank's predictions of the node
+ * (rank-local row order, rows 2j / 2j+1 of local pair j) on the host;
+ * sf_ctx_stage_predictions copies them out (NULL `out` to query *rows). */
+int sf_ctx_keep_stages(sf_ctx* ctx, int enable);
+int sf_ctx_stage_predictions(const sf_ctx* ctx, float* out, uint64_t cap,
+                             uint64_t* rows);
 /* Algorithmic bytes of the masked SpMM per complement pair for a
  * (subgraph, model): (sum_{u in R} deg(u) + 2|R|) d 4
  * gathered + 2|R| d 4 written + 2 W 8 mask, R = rows layer 0 produces. */

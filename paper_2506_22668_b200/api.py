@@ -464,6 +464,17 @@ class Context:
 
     FUSED_KERNELS = {"auto": 0, "simt": 1, "tc": 2, "tc16": 3}
 
+    def keep_stages(self, enable=True):
+        _chk(lib.sf_ctx_keep_stages(self.h, C.c_int(int(enable))))
+
+    def stage_predictions(self):
+        """This rank's predictions of the last explain_node (keep_stages on)."""
+        rows = C.c_uint64()
+        _chk(lib.sf_ctx_stage_predictions(self.h, None, C.c_uint64(0), C.byref(rows)))
+        out = np.zeros(rows.value, np.float32)
+        _chk(lib.sf_ctx_stage_predictions(self.h, _p(out), C.c_uint64(rows.value), C.byref(rows)))
+        return out
+
     def set_fused_kernel(self, kind):
         """Select the fused layer-0/1 kernel: "auto" (tcgen05 3xTF32 where
         the hidden width allows), "simt" (FP32 SIMT), "tc" (3xTF32) or "tc16"

@@ -861,7 +861,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     ctx.d2h_bytes += uint64_t(count) * sizeof(double);
     SF_CUDA(cudaMemcpyAsync(host + idx, scal + idx, count * sizeof(double),
                             cudaMemcpyDeviceToHost, st));
-    SF_CUDA(cudaStreamSynchronize(st));
+    comm_sync(ctx);
   };
 
   DebugTimer dt("cgls");
@@ -1184,7 +1184,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       comm_allreduce_sum(ctx, tv, uint64_t(n) + 1);
       fetch(0, 1);
       SF_CUDA(cudaMemcpyAsync(host + 1, tv + n, sizeof(double), cudaMemcpyDeviceToHost, st));
-      SF_CUDA(cudaStreamSynchronize(st));
+      comm_sync(ctx);
       ctx.d2h_bytes += sizeof(double);
       const double v_c = scw * host[0];
       const double delta = host[1] + v_c * v_c;

@@ -6,7 +6,9 @@
 // reference (scalar = length 1, vector otherwise), also for world == 1.
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -36,6 +38,8 @@ using GetUniqueId = int (*)(UniqueId*);
 using CommInitRank = int (*)(ncclComm_t*, int, UniqueId, int);
 using AllReduce = int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
 using CommDestroy = int (*)(ncclComm_t);
+using CommAbort = int (*)(ncclComm_t);
+using CommGetAsyncError = int (*)(ncclComm_t, int*);
 using GetErrorString = const char* (*)(int);
 constexpr int kFloat64 = 8;
 constexpr int kSum = 0;
@@ -62,9 +66,12 @@ struct Nccl {
   ncclComm_t comm = nullptr;
   AllReduce all_reduce = nullptr;
   CommDestroy destroy = nullptr;
+  CommAbort abort = nullptr;
+  CommGetAsyncError async_error = nullptr;
   GetErrorString err = nullptr;
+  bool aborted = false;
   ~Nccl() {
-    if (comm && destroy) destroy(comm);
+    if (comm && destroy && !aborted) destroy(comm);
   }
   void check(int rc, const char* what) const {
     if (rc != 0)
@@ -93,6 +100,8 @@ void nccl_join(Ctx& ctx, const void* id128, int rank, int world) {
   auto n = std::make_unique<Nccl>();
   n->all_reduce = sym<AllReduce>(lib, "ncclAllReduce");
   n->destroy = sym<CommDestroy>(lib, "ncclCommDestroy");
+  n->abort = sym<CommAbort>(lib, "ncclCommAbort");
+  n->async_error = sym<CommGetAsyncError>(lib, "ncclCommGetAsyncError");
   n->err = sym<GetErrorString>(lib, "ncclGetErrorString");
   auto init = sym<CommInitRank>(lib, "ncclCommInitRank");
   UniqueId id;
@@ -102,6 +111,38 @@ void nccl_join(Ctx& ctx, const void* id128, int rank, int world) {
   ctx.nccl = std::move(n);
 }
 
+void comm_drop_nccl(Ctx& ctx) { ctx.nccl.reset(); }
+
+void comm_sync(Ctx& ctx) {
+  if (!(ctx.world > 1 && ctx.nccl)) {
+    SF_CUDA(cudaStreamSynchronize(ctx.stream));
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(ctx.stream);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) SF_CUDA(q);
+    int async = 0;
+    if (ctx.nccl->async_error(ctx.nccl->comm, &async) == 0 && async != 0 && async != 7 /* ncclInProgress */) {
+      ctx.nccl->abort(ctx.nccl->comm);
+      ctx.nccl->aborted = true;
+      throw ProtocolError(std::string("collective failed: ") + (ctx.nccl->err ? ctx.nccl->err(async) : "nccl error"));
+    }
+    const auto waited = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+    if (waited.count() > ctx.comm_timeout_ms) {
+      // a peer never entered the collective: abort so the pending NCCL
+      // kernel exits, then fail like the reference's rendezvous timeout
+      ctx.nccl->abort(ctx.nccl->comm);
+      ctx.nccl->aborted = true;
+      cudaStreamSynchronize(ctx.stream);
+      throw ProtocolError("collective timed out after " + std::to_string(ctx.comm_timeout_ms) +
+                          " ms (rank " + std::to_string(ctx.rank) + " of " + std::to_string(ctx.world) + ")");
+    }
+    if (spin > 1000) std::this_thread::yield();
+  }
+}
+
 void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count) {
   if (count == 1)
     ++ctx.stats.scalar_allreduce;
@@ -109,7 +150,20 @@ void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count) {
     ++ctx.stats.vector_allreduce;
   ctx.stats.doubles_reduced += count;
   if (ctx.world == 1 || count == 0) return;
+  if (ctx.host_comm.all_reduce) {
+    ctx.comm_stage.reserve(count);
+    SF_CUDA(cudaMemcpyAsync(ctx.comm_stage.p, dev_buf, count * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    SF_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (ctx.host_comm.all_reduce(ctx.host_comm.user, ctx.comm_stage.p, count) != 0)
+      throw ProtocolError("host communicator all_reduce_sum failed");
+    SF_CUDA(cudaMemcpyAsync(dev_buf, ctx.comm_stage.p, count * 8, cudaMemcpyHostToDevice, ctx.stream));
+    SF_CUDA(cudaStreamSynchronize(ctx.stream));  // the staging buffer is reused
+    ctx.d2h_bytes += count * 8;
+    ctx.h2d_bytes += count * 8;
+    return;
+  }
   if (!ctx.nccl) throw ProtocolError("multi-rank context without a communicator");
+  if (ctx.nccl->aborted) throw ProtocolError("communicator aborted after an earlier failure");
   ctx.nccl->check(ctx.nccl->all_reduce(dev_buf, dev_buf, count, kFloat64, kSum,
                                        ctx.nccl->comm, ctx.stream),
                   "ncclAllReduce");
@@ -117,8 +171,14 @@ void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count) {
 
 void comm_barrier(Ctx& ctx) {
   ++ctx.stats.barriers;
+  if (ctx.world > 1 && ctx.host_comm.barrier) {
+    SF_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (ctx.host_comm.barrier(ctx.host_comm.user) != 0) throw ProtocolError("host communicator barrier failed");
+    return;
+  }
   if (ctx.world > 1) {
     if (!ctx.nccl) throw ProtocolError("multi-rank context without a communicator");
+    if (ctx.nccl->aborted) throw ProtocolError("communicator aborted after an earlier failure");
     DevBuf<double>& one = ctx.barrier_buf;
     one.reserve(1);
     SF_CUDA(cudaMemsetAsync(one.p, 0, sizeof(double), ctx.stream));
@@ -126,7 +186,7 @@ void comm_barrier(Ctx& ctx) {
                                          ctx.stream),
                     "ncclAllReduce(barrier)");
   }
-  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+  comm_sync(ctx);
 }
 
 Ctx::Ctx() = default;

@@ -686,6 +686,11 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     engine_predict(ctx, ctx.masks.p, rows, out->predicted_class, ctx.preds.p, nullptr, nullptr);
     comm_barrier(ctx);
     out->prediction_ms = ms_since(t_stage);
+    if (ctx.keep_stages) {
+      ctx.kept_preds.resize(rows);
+      SF_CUDA(cudaMemcpyAsync(ctx.kept_preds.data(), ctx.preds.p, rows * 4, cudaMemcpyDeviceToHost, ctx.stream));
+      SF_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
 
     t_stage = Clock::now();
     const std::vector<double> wsize = weight_of_size(n, global_rows_of_size(plan));
@@ -952,6 +957,26 @@ int sf_ctx_synchronize(sf_ctx* ctx) {
   });
 }
 
+int sf_ctx_keep_stages(sf_ctx* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "context");
+    ctx->c.keep_stages = enable != 0;
+    if (!enable) std::vector<float>().swap(ctx->c.kept_preds);
+  });
+}
+
+int sf_ctx_stage_predictions(const sf_ctx* ctx, float* out, uint64_t cap, uint64_t* rows) {
+  return guard([&] {
+    need(ctx, "context");
+    const auto& k = ctx->c.kept_preds;
+    if (rows) *rows = k.size();
+    if (out) {
+      if (cap < k.size()) throw DataError("prediction buffer too small");
+      std::memcpy(out, k.data(), k.size() * 4);
+    }
+  });
+}
+
 int sf_ctx_time_dominant(sf_ctx* ctx, int enable) {
   return guard([&] {
     need(ctx, "context");
@@ -1008,7 +1033,30 @@ int sf_ctx_join_nccl(sf_ctx* ctx, const void* id, int rank, int world) {
     need(ctx, "context");
     if (world > 1) need(id, "unique id");
     SF_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.host_comm = HostComm{};
     nccl_join(ctx->c, id, rank, world);
+  });
+}
+
+int sf_ctx_set_host_comm(sf_ctx* ctx, int rank, int world, void* user,
+                         int (*all_reduce)(void*, double*, uint64_t), int (*barrier)(void*)) {
+  return guard([&] {
+    need(ctx, "context");
+    if (world < 1 || rank < 0 || rank >= world)
+      throw DataError("invalid worker rank " + std::to_string(rank) + " of " + std::to_string(world));
+    if (world > 1 && (!all_reduce || !barrier)) throw DataError("host communicator needs all_reduce and barrier");
+    comm_drop_nccl(ctx->c);
+    ctx->c.rank = rank;
+    ctx->c.world = world;
+    ctx->c.host_comm = HostComm{user, all_reduce, barrier};
+  });
+}
+
+int sf_ctx_set_comm_timeout(sf_ctx* ctx, int timeout_ms) {
+  return guard([&] {
+    need(ctx, "context");
+    if (timeout_ms <= 0) throw DataError("communicator timeout must be positive");
+    ctx->c.comm_timeout_ms = timeout_ms;
   });
 }
 

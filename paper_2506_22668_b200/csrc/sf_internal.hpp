@@ -217,11 +217,23 @@ struct CommStats {  // comm.hpp:13-19
 
 struct Nccl;  // dlopen'ed NCCL (sf_comm.cpp)
 
+// A caller-provided host communicator (the reference's Communicator behind
+// the C-ABI, e.g. thread or socket workers, comm.hpp:28-52): all-reduces of
+// device buffers are staged through pinned host memory and handed to it.
+struct HostComm {
+  void* user = nullptr;
+  int (*all_reduce)(void* user, double* buf, uint64_t count) = nullptr;
+  int (*barrier)(void* user) = nullptr;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
   std::unique_ptr<Nccl> nccl;
+  HostComm host_comm;
+  PinnedBuf<double> comm_stage;  // host staging for host_comm all-reduces
+  int comm_timeout_ms = 60000;   // kDefaultCommTimeout (comm.hpp:54)
   CommStats stats;
   uint64_t launches = 0;
   int fused_kind = 0;  // SF_KERNEL_AUTO / SIMT / TC
@@ -263,6 +275,9 @@ struct Ctx {
   DevBuf<uint64_t> fid_streams, fid_rows;  // fidelity random-baseline jobs
   DevBuf<uint32_t> fid_sizes;
   DevBuf<uint8_t> fid_inv;
+  // stage outputs retained for stage-wise parity checks (sf_ctx_keep_stages)
+  bool keep_stages = false;
+  std::vector<float> kept_preds;  // this rank's predictions of the last explain_node
   Ctx();
   ~Ctx();
 };
@@ -272,6 +287,11 @@ void nccl_unique_id(void* out128);
 void nccl_join(Ctx& ctx, const void* id128, int rank, int world);
 void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count);
 void comm_barrier(Ctx& ctx);
+void comm_drop_nccl(Ctx& ctx);
+// Waits for the context stream; with a multi-rank NCCL communicator the wait
+// is bounded by ctx.comm_timeout_ms (a rank that never joins a collective
+// aborts the communicator and raises ProtocolError instead of hanging).
+void comm_sync(Ctx& ctx);
 
 // ---------------------------------------------------------------- plan
 struct SizeClass {
