@@ -60,6 +60,9 @@ int sf_ctx_set_host_comm(sf_ctx* ctx, int rank, int world, void* user,
                          int (*all_reduce)(void* user, double* buf,
                                            uint64_t count),
                          int (*barrier)(void* user));
+/* Communicator::all_reduce_sum on a host span through the context's
+ * communicator (NCCL or host); counted in the context stats. */
+int sf_ctx_allreduce_host(sf_ctx* ctx, double* buf, uint64_t count);
 /* Bound on a collective's wait (default 60000 ms, the reference's
  * kDefaultCommTimeout, comm.hpp:54). A rank that never joins aborts the NCCL
  * communicator and the call fails with SF_ERR_PROTOCOL. */
@@ -156,6 +159,12 @@ int sf_graph_build(uint32_t num_nodes, const uint64_t* edges_uv,
                    sf_graph** out);
 /* graph.hpp:64 load_graph, binary SFG1 (graph.cpp:35-64) */
 int sf_graph_load(const char* path, sf_graph** out);
+/* An already-built symmetric CSR (Graph, graph.hpp:16-31: rows sorted, no
+ * duplicates, both directions stored) taken as-is; labels may be NULL. */
+int sf_graph_from_csr(uint32_t num_nodes, const uint64_t* row_ptr,
+                      const uint32_t* col, const float* features,
+                      uint64_t feature_dim, const uint32_t* labels,
+                      sf_graph** out);
 /* graph.hpp:65 save_graph (graph.cpp:171-193) */
 int sf_graph_save(const sf_graph* g, const char* path);
 int sf_graph_free(sf_graph* g);
@@ -179,6 +188,14 @@ int sf_model_layer(const sf_model* m, int l, float* weight, float* bias);
 int sf_extract(const sf_graph* g, uint32_t target, int hops,
                sf_subgraph** out);
 int sf_subgraph_free(sf_subgraph* sg);
+/* A ComputationalGraph built by the caller (graph.hpp:36-53 layout: local
+ * ids BFS order, players_uv 2n local endpoints u < v sorted, symmetric CSR
+ * with edge_player, V x dim features). */
+int sf_subgraph_create(uint32_t target_global, uint32_t V, uint64_t n,
+                       const uint64_t* row_ptr, const uint32_t* col,
+                       const uint32_t* edge_player, const uint32_t* players_uv,
+                       const uint32_t* local_to_global, const float* features,
+                       uint64_t feature_dim, sf_subgraph** out);
 int sf_subgraph_dims(const sf_subgraph* sg, uint32_t* V, uint64_t* n,
                      uint64_t* nnz, uint64_t* feature_dim);
 int sf_subgraph_copy(const sf_subgraph* sg, uint64_t* row_ptr, uint32_t* col,

@@ -1052,6 +1052,20 @@ int sf_ctx_set_host_comm(sf_ctx* ctx, int rank, int world, void* user,
   });
 }
 
+int sf_ctx_allreduce_host(sf_ctx* ctx, double* buf, uint64_t count) {
+  return guard([&] {
+    need(ctx, "context");
+    if (count) need(buf, "buffer");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    DevBuf<double>& d = ctx->c.barrier_buf;
+    d.reserve(std::max<uint64_t>(count, 1));
+    SF_CUDA(cudaMemcpyAsync(d.p, buf, count * 8, cudaMemcpyHostToDevice, ctx->c.stream));
+    comm_allreduce_sum(ctx->c, d.p, count);
+    SF_CUDA(cudaMemcpyAsync(buf, d.p, count * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    comm_sync(ctx->c);
+  });
+}
+
 int sf_ctx_set_comm_timeout(sf_ctx* ctx, int timeout_ms) {
   return guard([&] {
     need(ctx, "context");
@@ -1174,6 +1188,33 @@ int sf_graph_build(uint32_t num_nodes, const uint64_t* edges, uint64_t num_edges
   });
 }
 
+int sf_graph_from_csr(uint32_t num_nodes, const uint64_t* row_ptr, const uint32_t* col, const float* features,
+                      uint64_t dim, const uint32_t* labels, sf_graph** out) {
+  return guard([&] {
+    need(out, "output");
+    need(row_ptr, "row_ptr");
+    const uint64_t nnz = row_ptr[num_nodes];
+    if (nnz) need(col, "col");
+    if (uint64_t(num_nodes) * dim != 0) need(features, "features");
+    Graph g;
+    g.num_nodes = num_nodes;
+    g.feature_dim = dim;
+    g.row_ptr.assign(row_ptr, row_ptr + num_nodes + 1);
+    g.col.assign(col, col + nnz);
+    for (uint32_t u = 0; u < num_nodes; ++u) {
+      if (g.row_ptr[u] > g.row_ptr[u + 1]) throw DataError("row_ptr is not monotone");
+      for (uint64_t i = g.row_ptr[u]; i < g.row_ptr[u + 1]; ++i) {
+        if (g.col[i] >= num_nodes) throw DataError("edge endpoint out of range");
+        if (i > g.row_ptr[u] && g.col[i] <= g.col[i - 1]) throw DataError("CSR rows must be sorted and unique");
+      }
+    }
+    g.features.assign(features, features + uint64_t(num_nodes) * dim);
+    g.labels.assign(num_nodes, 0xFFFFFFFFu);
+    if (labels) g.labels.assign(labels, labels + num_nodes);
+    *out = new sf_graph{std::move(g)};
+  });
+}
+
 int sf_graph_load(const char* path, sf_graph** out) {
   return guard([&] {
     need(path, "path");
@@ -1276,6 +1317,39 @@ int sf_extract(const sf_graph* g, uint32_t target, int hops, sf_subgraph** out) 
     need(g, "graph");
     need(out, "output");
     *out = new sf_subgraph{extract(g->g, target, hops)};
+  });
+}
+
+int sf_subgraph_create(uint32_t target_global, uint32_t V, uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
+                       const uint32_t* edge_player, const uint32_t* players_uv, const uint32_t* local_to_global,
+                       const float* features, uint64_t dim, sf_subgraph** out) {
+  return guard([&] {
+    need(out, "output");
+    need(row_ptr, "row_ptr");
+    const uint64_t nnz = row_ptr[V];
+    if (nnz) {
+      need(col, "col");
+      need(edge_player, "edge_player");
+    }
+    if (n) need(players_uv, "players");
+    if (V) need(local_to_global, "local_to_global");
+    if (uint64_t(V) * dim) need(features, "features");
+    Subgraph sg;
+    sg.target_global = target_global;
+    sg.feature_dim = dim;
+    sg.local_to_global.assign(local_to_global, local_to_global + V);
+    sg.players.resize(n);
+    for (uint64_t e = 0; e < n; ++e) {
+      sg.players[e] = {players_uv[2 * e], players_uv[2 * e + 1]};
+      if (sg.players[e].first >= V || sg.players[e].second >= V) throw DataError("player endpoint out of range");
+    }
+    sg.row_ptr.assign(row_ptr, row_ptr + V + 1);
+    sg.col.assign(col, col + nnz);
+    sg.edge_player.assign(edge_player, edge_player + nnz);
+    for (uint64_t i = 0; i < nnz; ++i)
+      if (sg.col[i] >= V || sg.edge_player[i] >= n) throw DataError("subgraph CSR entry out of range");
+    sg.features.assign(features, features + uint64_t(V) * dim);
+    *out = new sf_subgraph{std::move(sg)};
   });
 }
 
