@@ -223,7 +223,10 @@ int sf_predict_probs(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
  * WlsProblem (solver.hpp:22-38). Collective across the context's ranks.
  * mode: 0 = reference protocol (1 vector + 1 scalar all-reduce per
  * iteration, solver.hpp:82-85), 1 = fused (one (n+1)-double all-reduce per
- * iteration). trace != 0 records per-iteration residuals (out arrays of
+ * iteration), 2 = reference protocol with fixed-order (exact, layout-
+ * independent) sums: CglsOptions::fixed_order (solver.hpp:62-65), phi
+ * bitwise identical for any worker count; it adds one all-reduce at init and
+ * sends delta as 3 doubles. trace != 0 records per-iteration residuals (out arrays of
  * capacity trace_cap, may be NULL). */
 int sf_solve_cgls(sf_ctx* ctx, uint32_t n, const uint64_t* bits,
                   uint64_t rows, uint64_t words, const double* weights,
@@ -248,6 +251,15 @@ int sf_solve_direct(sf_ctx* ctx, uint32_t n, const uint64_t* bits,
 int sf_rank_edges(const double* phi, uint64_t n, uint32_t* order);
 
 /* ------------------------------------------------------------ pipeline */
+/* Solver of explain_node: SF_SOLVER_CGLS = reference CGLS protocol
+ * (solver.hpp:82-95: 1 vector + 1 scalar all-reduce per iteration),
+ * SF_SOLVER_FUSED = CGLS with one (n+1)-double all-reduce per iteration,
+ * SF_SOLVER_DIRECT = normal equations (tcgen05 Gram + device Cholesky,
+ * solve_direct semantics, one worker), SF_SOLVER_AUTO (default) = DIRECT
+ * when one worker holds the system and n <= 256 (env SF_DIRECT_MAX), else
+ * CGLS. DIRECT reports iterations 0 and residual 0. */
+enum { SF_SOLVER_CGLS = 0, SF_SOLVER_FUSED = 1, SF_SOLVER_DIRECT = 2, SF_SOLVER_AUTO = 3 };
+
 /* explain.hpp:15-32 ExplainOptions */
 typedef struct sf_explain_options {
   uint64_t samples;         /* 0: sf_auto_samples(n) */
@@ -261,11 +273,15 @@ typedef struct sf_explain_options {
   double constraint_scale;
   int fidelity;
   uint32_t baseline_trials;
-  int solver_mode;          /* 0 reference protocol, 1 fused all-reduce */
+  int solver_mode;          /* SF_SOLVER_* below */
   const uint32_t* top_counts; /* default {5,10,20} when NULL */
   uint32_t num_top_counts;
   const double* sparsities;   /* default {.1,.3,.5,.7,.9} when NULL */
   uint32_t num_sparsities;
+  /* ExplainOptions::fixed_order (explain.hpp:31): CGLS sums in a
+   * layout-independent (exact) order, phi bitwise identical for any worker
+   * count; costs 3 passes per transpose/forward product. Default 0. */
+  int fixed_order;
 } sf_explain_options;
 
 void sf_explain_options_default(sf_explain_options* o);

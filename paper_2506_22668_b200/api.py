@@ -325,7 +325,7 @@ class _OptionsC(C.Structure):
         ("allow_exhaustive", C.c_int), ("constraint_scale", C.c_double), ("fidelity", C.c_int),
         ("baseline_trials", C.c_uint32), ("solver_mode", C.c_int),
         ("top_counts", C.POINTER(C.c_uint32)), ("num_top_counts", C.c_uint32),
-        ("sparsities", C.POINTER(C.c_double)), ("num_sparsities", C.c_uint32),
+        ("sparsities", C.POINTER(C.c_double)), ("num_sparsities", C.c_uint32), ("fixed_order", C.c_int),
     ]
 
 
@@ -397,7 +397,8 @@ class ExplainOptions:
     constraint_scale: float = 1e6
     fidelity: bool = True
     baseline_trials: int = 8
-    solver_mode: int = 0
+    solver_mode: int = 3  # SF_SOLVER_AUTO (0 CGLS, 1 fused CGLS, 2 direct)
+    fixed_order: bool = False  # explain.hpp:31 (exact, layout-independent CGLS sums)
     _keep: list = field(default_factory=list, repr=False)
 
     def c(self):
@@ -407,7 +408,7 @@ class ExplainOptions:
         return _OptionsC(self.samples, self.batch_size, self.top_k, self.seed & (2**64 - 1), self.tol,
                          self.max_iter, self.player_cap, int(self.allow_exhaustive), self.constraint_scale,
                          int(self.fidelity), self.baseline_trials, self.solver_mode, tc, len(self.top_counts),
-                         sp, len(self.sparsities))
+                         sp, len(self.sparsities), int(self.fixed_order))
 
 
 class Context:

@@ -625,6 +625,108 @@ __global__ void transpose_finish_kernel(const double* __restrict__ s_part,
   s[e] = acc;
 }
 
+// ---------------------------------------------------------------- fixed order
+// Reproducible summation (fixed-order mode). A value x with |x| <= 2^E that
+// enters a sum of at most 2^(H-1) terms is split into three parts on fixed
+// grids q1 = 2^(E+H-52), q2 = q1 2^(H-53), q3 = q2 2^(H-53): x1 = rint(x/q1)
+// q1, x2 = rint((x-x1)/q2) q2, x3 = rint((x-x1-x2)/q3) q3 (every step exact).
+// Any sum of same-level parts is then exact in FP64 in any order and
+// grouping, so the level sums — and ((S1 + S2) + S3) — do not depend on how
+// rows are split across ranks, tiles, CTAs or NCCL's reduction order. The
+// grids come from bounds that every rank computes identically.
+__device__ __forceinline__ void split3(double x, const double* g, double& a, double& b, double& c) {
+  a = rint(x * (1.0 / g[0])) * g[0];
+  const double r1 = x - a;
+  b = rint(r1 * (1.0 / g[1])) * g[1];
+  const double r2 = r1 - b;
+  c = rint(r2 * (1.0 / g[2])) * g[2];
+}
+
+// out[k * stride + i] = part k of x[i] (0 past count)
+__global__ void split3_kernel(const double* __restrict__ x, uint64_t count, uint64_t padded,
+                              const double* __restrict__ grid, double* __restrict__ out, uint64_t stride) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= padded) return;
+  double a = 0.0, b = 0.0, c = 0.0;
+  if (i < count) split3(x[i], grid, a, b, c);
+  out[i] = a;
+  out[stride + i] = b;
+  out[2 * stride + i] = c;
+}
+
+// max_i |x_i * (y ? y_i : 1)|, one CTA
+__global__ void __launch_bounds__(1024) absmax_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                      uint64_t count, double* __restrict__ out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) m = fmax(m, fabs(x[i] * (y ? y[i] : 1.0)));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = red[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *out = m;
+  }
+}
+
+__device__ __forceinline__ void make_grid(int E, int H, double* g) {
+  g[0] = ldexp(1.0, E + H - 52);
+  g[1] = ldexp(g[0], H - 53);
+  g[2] = ldexp(g[1], H - 53);
+}
+
+// per-iteration grids from the replicated direction u: gU for the parts of
+// u (row dots of <= n terms, complements sum_u - dot), gD for v^2 (rows)
+__global__ void iter_grids_kernel(const double* __restrict__ umax, int e_sw, int log_n, int h_u, int h_rows,
+                                  double* __restrict__ gU, double* __restrict__ gD) {
+  int e = 0;
+  frexp(*umax, &e);  // umax < 2^e
+  if (*umax == 0.0) e = -1000;
+  make_grid(e, h_u, gU);
+  // |v| <= max sw * n * umax
+  make_grid(2 * (e_sw + e + log_n), h_rows, gD);
+}
+
+// s = (((L0 + L1) + L2) + ((K0 + K1) + K2)) + pin
+__global__ void combine_s_kernel(const double* __restrict__ lev, uint32_t n, double pin, double* __restrict__ s) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double* k = lev + 3ull * n;
+  s[e] = (((lev[e] + lev[n + e]) + lev[2ull * n + e]) + ((k[0] + k[1]) + k[2])) + pin;
+}
+
+// v = sw ((V0 + V1) + V2) per row, and the parts of v^2 for delta
+__global__ void combine_v_kernel(const double* __restrict__ vl, uint64_t rows, const double* __restrict__ sw,
+                                 const double* __restrict__ gD, double* __restrict__ v,
+                                 double* __restrict__ dparts) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= rows) return;
+  const double x = sw[i] * ((vl[i] + vl[rows + i]) + vl[2 * rows + i]);
+  v[i] = x;
+  double a, b, c;
+  split3(x * x, gD, a, b, c);
+  dparts[i] = a;
+  dparts[rows + i] = b;
+  dparts[2 * rows + i] = c;
+}
+
+__global__ void sq_parts_kernel(const double* __restrict__ r, uint64_t rows, const double* __restrict__ g,
+                                double* __restrict__ parts) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= rows) return;
+  double a, b, c;
+  split3(r[i] * r[i], g, a, b, c);
+  parts[i] = a;
+  parts[rows + i] = b;
+  parts[2 * rows + i] = c;
+}
+
+__global__ void fill_kernel(double* __restrict__ x, double value, uint64_t count) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < count) x[i] = value;
+}
+
 __global__ void add_scalar_kernel(double* __restrict__ s, double c, uint32_t n) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n) s[e] += c;
@@ -700,48 +802,6 @@ __global__ void assemble_pairs_kernel(const uint64_t* __restrict__ rows, uint64_
   }
 }
 
-// ---------------------------------------------------------------- Gram
-// G[a][b] = sum_i w_i bit_i(a) bit_i(b) (+ pin), rhs[a] = sum_i w_i t_i bit_i(a)
-__global__ void gram_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp,
-                           uint32_t n, uint64_t tiles, const double* __restrict__ w,
-                           const double* __restrict__ wt, double cw, double ct,
-                           double* __restrict__ G, double* __restrict__ rhs) {
-  const uint32_t a = blockIdx.y;
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n || b < a) return;
-  double acc = 0.0, racc = 0.0;
-  for (uint64_t t = 0; t < tiles; ++t) {
-    const uint64_t xa = maskt[t * Wp + a];
-    uint64_t x = xa & maskt[t * Wp + b];
-    while (x) {
-      const int i = __ffsll(static_cast<long long>(x)) - 1;
-      x &= x - 1;
-      acc += w[t * 64 + i];
-    }
-    if (b == a) {
-      uint64_t y = xa;
-      while (y) {
-        const int i = __ffsll(static_cast<long long>(y)) - 1;
-        y &= y - 1;
-        racc += wt[t * 64 + i];
-      }
-    }
-  }
-  G[uint64_t(a) * n + b] = acc + cw;
-  G[uint64_t(b) * n + a] = acc + cw;
-  if (b == a) rhs[a] = racc + cw * ct;
-}
-
-__global__ void weight_products_kernel(const double* __restrict__ sw,
-                                       const double* __restrict__ tgt, uint64_t rows,
-                                       uint64_t padded, double* __restrict__ w,
-                                       double* __restrict__ wt) {
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i >= padded) return;
-  const double ww = i < rows ? sw[i] * sw[i] : 0.0;
-  w[i] = ww;
-  wt[i] = i < rows ? ww * tgt[i] : 0.0;
-}
 
 // order-preserving key of -phi (+0 and -0 share a key: they compare equal)
 __global__ void rank_keys_kernel(const double* __restrict__ phi, uint32_t n, uint64_t* __restrict__ key,
@@ -824,7 +884,14 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
                          (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
                          uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
-  ctx.solver_work.reserve(bytes);
+  const bool repro = in.fixed_order;
+  if (repro && mode != 0) throw DataError("fixed-order summation runs the reference protocol (solver mode 0)");
+  constexpr int kBins = 2201;  // frexp exponents -1100..1100
+  const uint64_t repro_bytes =
+      repro ? (3ull * n + 8 + 3 * rows * 2 + 3 * ptiles * 64 * 2 + 3 * std::max<uint64_t>(pairs, 1) + rows +
+               (2ull * kBins + 8) + 64) * 8 + 16 * 256
+            : 0;
+  ctx.solver_work.reserve(bytes + repro_bytes);
   Scratch sc{ctx.solver_work.p, 0};
   uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
   uint64_t* mto = sc.take<uint64_t>(ptiles * Wp);  // odd rows (non-complement pairs only)
@@ -843,6 +910,21 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* tv = sc.take<double>(n + 1);  // fused mode: [A^T v ; ||v||^2]
   double* u = sc.take<double>(n);
   double* phi = sc.take<double>(n);
+  // fixed-order mode buffers
+  double *lev = nullptr, *ul = nullptr, *vl = nullptr, *dparts = nullptr, *cel = nullptr, *col = nullptr,
+         *kcl = nullptr, *ones = nullptr, *flags = nullptr, *grids = nullptr;
+  if (repro) {
+    lev = sc.take<double>(3ull * n + 3);     // all-reduced: 3 level sums of M^T r, 3 of the pair constants
+    ul = sc.take<double>(3ull * n + 3);      // parts of u, then their 3 sums
+    vl = sc.take<double>(3 * rows);          // per-level row dots
+    dparts = sc.take<double>(3 * rows);      // parts of v^2 (or r^2 for the trace)
+    cel = sc.take<double>(3 * ptiles * 64);  // parts of the even-row coefficients
+    col = sc.take<double>(3 * ptiles * 64);  // parts of the odd-row coefficients
+    kcl = sc.take<double>(3 * std::max<uint64_t>(pairs, 1));
+    ones = sc.take<double>(rows);
+    flags = sc.take<double>(2 * kBins + 8);
+    grids = sc.take<double>(64);  // gT[0..3) gU[8..11) gD[16..19) gR[24..27) zero[32] maxes[40..42) dsum[48..51)
+  }
   double* red = sc.take<double>(kRedBlocks);
   // device scalars: 0 sum_u, 1 delta, 2 gamma, 3 gamma_next, 4 kconst,
   // 5 sse, 6 data0
@@ -1063,43 +1145,81 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   ctx.h2d_bytes += (bounds.size() + sbounds.size() + nbounds.size()) * 4;
   SF_CUDA(cudaStreamSynchronize(st));
   const double scw = std::sqrt(in.constraint_weight);
+  int rp_esw = 0, rp_logn = 0, rp_hu = 0, rp_hrows = 0;  // fixed-order bounds (set at init)
   double r_c = scw * in.constraint_target;
 
   // out = M^T (sw x) (+ the pair constants); x = r (reference protocol) or
   // v (fused mode, coefficients sw * v). Local: no collective here.
-  auto transpose_local = [&](const double* x, double* out) {
+  auto coefs = [&](const double* x) {
     SF_CUDA(cudaMemsetAsync(kc, 0, std::max<uint64_t>(pairs, 1) * 8, st));
     if (pairs) {
       coef_kernel<<<blocks_for(ptiles * 64), 256, 0, st>>>(in.dev_sw, x, is_comp, pairs, ptiles * 64,
                                                           coef_e, coef_o, kc);
       SF_LAUNCHED(ctx);
     }
-    reduce(kc, pairs, 0, 0.0, scal + 4);
+  };
+  // out = sum over pairs of the coefficients on their set bits + *kconst
+  auto passes = [&](const double* ce, const double* co, const double* kconst, double* out) {
     if (splits) {
       dim3 grid(unsigned(pblocks), splits);
-      transpose_partial_kernel<<<grid, 256, 0, st>>>(mte, Wp, n, split_start, coef_e, 0, s_part);
+      transpose_partial_kernel<<<grid, 256, 0, st>>>(mte, Wp, n, split_start, ce, 0, s_part);
       SF_LAUNCHED(ctx);
       if (any_noncomp) {
-        transpose_partial_kernel<<<grid, 256, 0, st>>>(mto, Wp, n, split_start, coef_o, 1, s_part);
+        transpose_partial_kernel<<<grid, 256, 0, st>>>(mto, Wp, n, split_start, co, 1, s_part);
         SF_LAUNCHED(ctx);
       }
     }
     if (lists) {
       list_transpose_kernel<<<blocks_for(uint64_t(n) * 32), 256, 0, st>>>(
-          pl_off, pl_idx, n, lsegs, coef_e, s_part + uint64_t(splits + nsplits) * n);
+          pl_off, pl_idx, n, lsegs, ce, s_part + uint64_t(splits + nsplits) * n);
       SF_LAUNCHED(ctx);
     }
     if (nsplits) {
       nib_transpose_kernel<<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
-          mte, Wp, n, ptiles, nsplit_start, coef_e, s_part + uint64_t(splits) * n);
+          mte, Wp, n, ptiles, nsplit_start, ce, s_part + uint64_t(splits) * n);
       SF_LAUNCHED(ctx);
     }
     transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits + nsplits + (lists ? 1 : 0), n,
-                                                           scal + 4, out);
+                                                           kconst, out);
     SF_LAUNCHED(ctx);
+  };
+  // out = M^T (sw x) (+ the pair constants); x = r (reference protocol) or
+  // v (fused mode, coefficients sw * v). Local: no collective here.
+  auto transpose_local = [&](const double* x, double* out) {
+    coefs(x);
+    reduce(kc, pairs, 0, 0.0, scal + 4);
+    passes(coef_e, coef_o, scal + 4, out);
+  };
+  // fixed-order mode: the three level sums of M^T (sw r) and of the pair
+  // constants into lev[0, 3n + 3), exact on every rank
+  auto transpose_levels = [&](const double* x) {
+    coefs(x);
+    const uint64_t P = ptiles * 64;
+    if (P) {
+      split3_kernel<<<blocks_for(P), 256, 0, st>>>(coef_e, P, P, grids + 0, cel, P);
+      SF_LAUNCHED(ctx);
+      if (any_noncomp) {
+        split3_kernel<<<blocks_for(P), 256, 0, st>>>(coef_o, P, P, grids + 0, col, P);
+        SF_LAUNCHED(ctx);
+      }
+    }
+    const uint64_t KP = std::max<uint64_t>(pairs, 1);
+    split3_kernel<<<blocks_for(KP), 256, 0, st>>>(kc, pairs, KP, grids + 0, kcl, KP);
+    SF_LAUNCHED(ctx);
+    for (int k = 0; k < 3; ++k) {
+      passes(cel + k * P, col + k * P, grids + 32, lev + uint64_t(k) * n);
+      reduce(kcl + k * KP, pairs, 0, 0.0, lev + 3ull * n + k);
+    }
   };
   // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
   auto transpose_product = [&]() {
+    if (repro) {
+      transpose_levels(r);
+      comm_allreduce_sum(ctx, lev, 3ull * n + 3);
+      combine_s_kernel<<<blocks_for(n), 256, 0, st>>>(lev, n, scw * r_c, s);
+      SF_LAUNCHED(ctx);
+      return;
+    }
     transpose_local(r, s);
     comm_allreduce_sum(ctx, s, n);
     add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw * r_c, n);
@@ -1108,31 +1228,58 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   // v (set-bit rows [0, rows_b), nibble pairs [pd, pairs)) and the per-block
   // sums of v^2 in dsq[0, fwd_blocks)
   const uint64_t fwd_blocks = fblocks + lblocks + nb_rowblocks;
-  auto forward_v = [&](const double* x) {
+  auto forward_v = [&](const double* x, const double* swp, const double* sum_u, double* vout) {
     if (lblocks) {
-      list_forward_kernel<<<unsigned(lblocks), 256, 0, st>>>(row_off, row_idx, pd, x, in.dev_sw, scal + 0, v,
+      list_forward_kernel<<<unsigned(lblocks), 256, 0, st>>>(row_off, row_idx, pd, x, swp, sum_u, vout,
                                                               dsq + fblocks);
       SF_LAUNCHED(ctx);
     }
     if (fblocks) {
       forward_kernel<<<unsigned(fblocks), kFwdThreads, size_t(std::min<uint32_t>(n, kFwdChunk)) * 8, st>>>(
-          in.dev_rows, W, row_start, is_comp, x, n, in.dev_sw, scal + 0, v, dsq);
+          in.dev_rows, W, row_start, is_comp, x, n, swp, sum_u, vout, dsq);
       SF_LAUNCHED(ctx);
     }
     if (nb_rowblocks) {
       nib_forward_kernel<<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 4 * 16 * 8, st>>>(
           rT, pstride, pairs_n, x, n, nb_part_players, vpart);
       SF_LAUNCHED(ctx);
-      nib_forward_finish<<<unsigned(nb_rowblocks), 256, 0, st>>>(vpart, nb_parts, pd, pairs, in.dev_sw,
-                                                                   scal + 0, v, dsq + fblocks + lblocks);
+      nib_forward_finish<<<unsigned(nb_rowblocks), 256, 0, st>>>(vpart, nb_parts, pd, pairs, swp,
+                                                                   sum_u, vout, dsq + fblocks + lblocks);
       SF_LAUNCHED(ctx);
     }
   };
   SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdChunk * 8)));
   // v = sqrt(W) M u; delta = ||v||^2 all-reduced + v_c^2 (solver.cpp:252-287)
   auto forward_product = [&](double& delta, double& v_c) {
+    if (repro) {
+      // parts of u on a grid from max|u| (u is replicated: same grid on
+      // every rank), exact per-level row dots, v = sw ((V0 + V1) + V2),
+      // delta from the parts of v^2
+      reduce(u, n, 0, 0.0, scal + 0);  // sum_u for the pin row
+      absmax_kernel<<<1, 1024, 0, st>>>(u, nullptr, n, grids + 40);
+      SF_LAUNCHED(ctx);
+      iter_grids_kernel<<<1, 1, 0, st>>>(grids + 40, rp_esw, rp_logn, rp_hu, rp_hrows, grids + 8, grids + 16);
+      SF_LAUNCHED(ctx);
+      split3_kernel<<<blocks_for(n), 256, 0, st>>>(u, n, n, grids + 8, ul, n);
+      SF_LAUNCHED(ctx);
+      for (int k = 0; k < 3; ++k) reduce(ul + uint64_t(k) * n, n, 0, 0.0, ul + 3ull * n + k);
+      if (rows) {
+        for (int k = 0; k < 3; ++k) forward_v(ul + uint64_t(k) * n, ones, ul + 3ull * n + k, vl + k * rows);
+        combine_v_kernel<<<blocks_for(rows), 256, 0, st>>>(vl, rows, in.dev_sw, grids + 16, v, dparts);
+        SF_LAUNCHED(ctx);
+      }
+      for (int k = 0; k < 3; ++k) reduce(dparts + k * rows, rows, 0, 0.0, grids + 48 + k);
+      comm_allreduce_sum(ctx, grids + 48, 3);
+      ctx.d2h_bytes += 4 * sizeof(double);
+      SF_CUDA(cudaMemcpyAsync(host + 12, grids + 48, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      fetch(0, 1);
+      delta = (host[12] + host[13]) + host[14];
+      v_c = scw * host[0];
+      delta += v_c * v_c;
+      return;
+    }
     reduce(u, n, 0, 0.0, scal + 0);  // sum_u
-    if (rows) forward_v(u);
+    if (rows) forward_v(u, in.dev_sw, scal + 0, v);
     reduce(dsq, rows ? fwd_blocks : 0, 0, 0.0, scal + 1);
     comm_allreduce_sum(ctx, scal + 1, 1);
     fetch(0, 2);
@@ -1144,6 +1291,68 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   SF_CUDA(cudaStreamSynchronize(st));
   dt.lap("setup");
   SF_CUDA(cudaMemsetAsync(phi, 0, uint64_t(n) * 8, st));
+  if (repro) {
+    // Global bounds, identical on every rank: exponent flags of max |sw t|
+    // and max sw plus the global pair count, summed over ranks (one extra
+    // vector all-reduce at init; flags are 0/1 so the sum is exact).
+    absmax_kernel<<<1, 1024, 0, st>>>(in.dev_sw, in.dev_targets, rows, grids + 40);
+    SF_LAUNCHED(ctx);
+    absmax_kernel<<<1, 1024, 0, st>>>(in.dev_sw, nullptr, rows, grids + 41);
+    SF_LAUNCHED(ctx);
+    SF_CUDA(cudaMemcpyAsync(host + 12, grids + 40, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> fl(2 * kBins + 1, 0.0);
+    for (int q = 0; q < 2; ++q) {
+      if (host[12 + q] > 0.0 && std::isfinite(host[12 + q])) {
+        int e = 0;
+        std::frexp(host[12 + q], &e);
+        fl[q * kBins + std::clamp(e + 1100, 0, kBins - 1)] = 1.0;
+      }
+    }
+    fl[2 * kBins] = double(pairs);
+    SF_CUDA(cudaMemcpyAsync(flags, fl.data(), fl.size() * 8, cudaMemcpyHostToDevice, st));
+    comm_allreduce_sum(ctx, flags, fl.size());
+    SF_CUDA(cudaMemcpyAsync(fl.data(), flags, fl.size() * 8, cudaMemcpyDeviceToHost, st));
+    comm_sync(ctx);
+    ctx.h2d_bytes += fl.size() * 8;
+    ctx.d2h_bytes += fl.size() * 8;
+    auto top = [&](int q) {
+      for (int b = kBins - 1; b >= 0; --b)
+        if (fl[q * kBins + b] != 0.0) return b - 1100;
+      return -1000;
+    };
+    const int e_b = top(0);  // max |sw t| < 2^e_b
+    rp_esw = top(1);         // max sw < 2^rp_esw
+    const double gpairs = fl[2 * kBins];
+    const double grows = 2.0 * gpairs;
+    auto clog2 = [](double x) { return int(std::ceil(std::log2(std::max(x, 1.0)))); };
+    // ||[r; r_c]|| never exceeds its start (CGLS minimises it): |r_i| <= R
+    const double rc0 = std::fabs(scw * in.constraint_target);
+    const double R = 2.0 * std::sqrt(grows * std::ldexp(1.0, 2 * e_b) + rc0 * rc0);
+    int e_r = 0;
+    std::frexp(R, &e_r);
+    const int h_pairs = clog2(gpairs + 1) + 1;
+    rp_hrows = clog2(grows + 1) + 1;
+    rp_logn = clog2(double(n) + 1);
+    rp_hu = rp_logn + 2;
+    // pair coefficients: |c_e - c_o| <= 2 max sw R
+    double g[3];
+    auto host_grid = [&](int E, int H) {
+      g[0] = std::ldexp(1.0, E + H - 52);
+      g[1] = std::ldexp(g[0], H - 53);
+      g[2] = std::ldexp(g[1], H - 53);
+    };
+    host_grid(rp_esw + 1 + e_r, h_pairs);
+    SF_CUDA(cudaMemcpyAsync(grids + 0, g, 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    host_grid(2 * e_r, rp_hrows);  // r^2 for the trace
+    SF_CUDA(cudaMemcpyAsync(grids + 24, g, 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    SF_CUDA(cudaMemsetAsync(grids + 32, 0, sizeof(double), st));
+    if (rows) {
+      fill_kernel<<<blocks_for(rows), 256, 0, st>>>(ones, 1.0, rows);
+      SF_LAUNCHED(ctx);
+    }
+    SF_CUDA(cudaStreamSynchronize(st));
+  }
   transpose_product();
   reduce(s, n, 1, 0.0, scal + 2);                // gamma = ||s||^2
   reduce(s, n, 2, scw * r_c, scal + 6);          // data0 = ||s - pin||^2
@@ -1175,7 +1384,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     while (res.iterations < maxit) {
       reduce(u, n, 0, 0.0, scal + 0);  // sum_u (pin row: v_c = scw sum_u)
       if (rows) {
-        forward_v(u);
+        forward_v(u, in.dev_sw, scal + 0, v);
         transpose_local(v, tv);
       } else {
         SF_CUDA(cudaMemsetAsync(tv, 0, uint64_t(n) * 8, st));
@@ -1248,7 +1457,15 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       SF_LAUNCHED(ctx);
     }
     r_c -= theta * v_c;
-    if (trace) {
+    if (trace && repro) {
+      sq_parts_kernel<<<blocks_for(std::max<uint64_t>(rows, 1)), 256, 0, st>>>(r, rows, grids + 24, dparts);
+      SF_LAUNCHED(ctx);
+      for (int k = 0; k < 3; ++k) reduce(dparts + k * rows, rows, 0, 0.0, grids + 48 + k);
+      comm_allreduce_sum(ctx, grids + 48, 3);
+      SF_CUDA(cudaMemcpyAsync(host + 12, grids + 48, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      comm_sync(ctx);
+      res.row_residual_trace.push_back(std::sqrt(((host[12] + host[13]) + host[14]) + r_c * r_c));
+    } else if (trace) {
       reduce(r, rows, 1, 0.0, scal + 5);
       comm_allreduce_sum(ctx, scal + 5, 1);
       fetch(5, 1);
@@ -1277,79 +1494,6 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   }
   download_phi();
   return res;
-}
-
-std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in) {
-  const uint32_t n = in.n;
-  if (n == 0) return {};
-  const uint64_t rows = in.rows;
-  const uint32_t W = in.W;
-  const uint64_t tiles = (rows + 63) / 64;
-  const uint64_t Wp = uint64_t(W) * 64;
-  DevBuf<uint64_t> maskt;
-  DevBuf<double> w, wt, G, rhs;
-  maskt.reserve(std::max<uint64_t>(tiles * Wp, 1));
-  w.reserve(tiles * 64 + 1);
-  wt.reserve(tiles * 64 + 1);
-  G.reserve(uint64_t(n) * n);
-  rhs.reserve(n);
-  cudaStream_t st = ctx.stream;
-  launch_transpose_tiles(ctx, in.dev_rows, rows, W, tiles, maskt.p);
-  if (tiles) {
-    weight_products_kernel<<<blocks_for(tiles * 64), 256, 0, st>>>(in.dev_sw, in.dev_targets,
-                                                                    rows, tiles * 64, w.p, wt.p);
-    SF_LAUNCHED(ctx);
-  }
-  dim3 grid(blocks_for(n), n);
-  gram_kernel<<<grid, 256, 0, st>>>(maskt.p, Wp, n, tiles, w.p, wt.p, in.constraint_weight,
-                                    in.constraint_target, G.p, rhs.p);
-  SF_LAUNCHED(ctx);
-  std::vector<double> gram(uint64_t(n) * n), b(n);
-  SF_CUDA(cudaMemcpyAsync(gram.data(), G.p, gram.size() * 8, cudaMemcpyDeviceToHost, st));
-  SF_CUDA(cudaMemcpyAsync(b.data(), rhs.p, uint64_t(n) * 8, cudaMemcpyDeviceToHost, st));
-  SF_CUDA(cudaStreamSynchronize(st));
-  // Cholesky with one jitter retry (solver.cpp:383-405), on the host
-  auto factor = [&](std::vector<double> a, std::vector<double>& out) -> uint32_t {
-    for (uint32_t c = 0; c < n; ++c) {
-      double d = a[uint64_t(c) * n + c];
-      for (uint32_t k = 0; k < c; ++k) d -= a[uint64_t(c) * n + k] * a[uint64_t(c) * n + k];
-      if (!(d > 0.0) || !std::isfinite(d)) return c;
-      const double piv = std::sqrt(d);
-      a[uint64_t(c) * n + c] = piv;
-      for (uint32_t rr = c + 1; rr < n; ++rr) {
-        double t = a[uint64_t(rr) * n + c];
-        for (uint32_t k = 0; k < c; ++k) t -= a[uint64_t(rr) * n + k] * a[uint64_t(c) * n + k];
-        a[uint64_t(rr) * n + c] = t / piv;
-      }
-    }
-    out = std::move(a);
-    return n;
-  };
-  std::vector<double> L;
-  if (factor(gram, L) != n) {
-    double tr = 0.0;
-    for (uint32_t a = 0; a < n; ++a) tr += gram[uint64_t(a) * n + a];
-    const double jitter = 1.0e-10 * tr / n;
-    for (uint32_t a = 0; a < n; ++a) gram[uint64_t(a) * n + a] += jitter;
-    const uint32_t bad = factor(gram, L);
-    if (bad != n)
-      throw NumericalError("normal equations are singular: factorization failed at pivot " +
-                           std::to_string(bad) + " of " + std::to_string(n) +
-                           " even after diagonal jitter");
-  }
-  std::vector<double> z(n), phi(n);
-  for (uint32_t i = 0; i < n; ++i) {
-    double t = b[i];
-    for (uint32_t k = 0; k < i; ++k) t -= L[uint64_t(i) * n + k] * z[k];
-    z[i] = t / L[uint64_t(i) * n + i];
-  }
-  for (uint32_t ii = n; ii > 0; --ii) {
-    const uint32_t i = ii - 1;
-    double t = z[i];
-    for (uint32_t k = i + 1; k < n; ++k) t -= L[uint64_t(k) * n + i] * phi[k];
-    phi[i] = t / L[uint64_t(i) * n + i];
-  }
-  return phi;
 }
 
 // solver.cpp:430-440: a stable LSD radix sort of the keys over the index

@@ -608,6 +608,8 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
   out->node = node;
   out->converged = 1;
   if (o.batch_size == 0) throw DataError("batch_size must be positive");
+  if (o.solver_mode < SF_SOLVER_CGLS || o.solver_mode > SF_SOLVER_AUTO)
+    throw DataError("unknown solver mode " + std::to_string(o.solver_mode));
   if (m.layers.front().in != g.feature_dim)
     throw DataError("model expects " + std::to_string(m.layers.front().in) +
                     " input features but the graph has " + std::to_string(g.feature_dim));
@@ -727,7 +729,35 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     in.dev_pop = ctx.pop_dev.p;
     in.dev_is_comp = ctx.comp_dev.p;
     DebugTimer("explain").lap("assemble done");
-    CglsResult res = cgls_solve(ctx, in, o.tol, o.max_iter, o.solver_mode, false);
+    // Solver dispatch: the direct (tcgen05 Gram + device Cholesky) path
+    // for small player counts on one worker, CGLS otherwise. Crossover
+    // measured at k = 100K (profiles/round2/solver_crossover.jsonl): direct
+    // 0.53-0.99 ms vs CGLS 0.83-1.08 ms up to n = 250, slower from n = 500.
+    static const uint64_t direct_max =
+        std::getenv("SF_DIRECT_MAX") ? std::strtoull(std::getenv("SF_DIRECT_MAX"), nullptr, 10) : 256;
+    const bool direct = o.solver_mode == SF_SOLVER_DIRECT ||
+                        (o.solver_mode == SF_SOLVER_AUTO && ctx.world == 1 && n <= direct_max);
+    if (o.solver_mode == SF_SOLVER_DIRECT && ctx.world != 1)
+      throw DataError("direct solve needs the full system on a single worker");
+    CglsResult res;
+    if (direct) {
+      // one weight run per size class (w_s == w_{n-s}: both rows of a pair)
+      std::vector<GramRun> runs;
+      for (const SizeClass& c : plan.classes) {
+        const double we = wsize[c.size], wo = wsize[n - c.size];
+        const uint64_t r0 = 2 * c.first_pair, r1 = 2 * (c.first_pair + c.pairs);
+        if (we == wo) {
+          runs.push_back(GramRun{r0, r1, we});
+        } else {
+          for (uint64_t r = r0; r < r1; ++r) runs.push_back(GramRun{r, r + 1, (r & 1) ? wo : we});
+        }
+      }
+      res.phi = gram_solve(ctx, in, runs);
+      res.converged = true;
+    } else {
+      in.fixed_order = o.fixed_order != 0 && o.solver_mode != SF_SOLVER_FUSED;
+      res = cgls_solve(ctx, in, o.tol, o.max_iter, o.solver_mode == SF_SOLVER_FUSED ? 1 : 0, false);
+    }
     comm_barrier(ctx);
     out->solve_ms = ms_since(t_stage);
     phi = std::move(res.phi);
@@ -1333,7 +1363,7 @@ int sf_subgraph_create(uint32_t target_global, uint32_t V, uint64_t n, const uin
     }
     if (n) need(players_uv, "players");
     if (V) need(local_to_global, "local_to_global");
-    if (uint64_t(V) * dim) need(features, "features");
+    if (uint64_t(V) * dim != 0) need(features, "features");
     Subgraph sg;
     sg.target_global = target_global;
     sg.feature_dim = dim;
@@ -1475,9 +1505,9 @@ int sf_assemble_weights(uint32_t n, const uint64_t* bits, uint64_t rows, uint64_
 
 static void solve_common(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows,
                          uint64_t words, const double* weights, const double* targets,
-                         DevBuf<double>& d_sw, DevBuf<double>& d_tgt, CglsInput& in) {
+                         DevBuf<double>& d_sw, DevBuf<double>& d_tgt, CglsInput& in, bool pairs = true) {
   need(ctx, "context");
-  if (rows % 2) throw DataError("local rows must come in adjacent pairs");
+  if (pairs && rows % 2) throw DataError("local rows must come in adjacent pairs");
   const uint32_t W = uint32_t((n + 63) / 64);
   if (rows && words < W) throw DataError("rows narrower than the player count");
   SF_CUDA(cudaSetDevice(ctx->c.device));
@@ -1514,7 +1544,9 @@ int sf_solve_cgls(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows, 
     in.constraint_target = ct;
     in.constraint_weight = cw;
     in.global_pair_count = rows / 2;
-    CglsResult r = cgls_solve(ctx->c, in, tol, max_iter, mode, trace || row_trace);
+    if (mode < 0 || mode > 2) throw DataError("solver mode must be 0 (reference protocol), 1 (fused) or 2 (fixed order)");
+    in.fixed_order = mode == 2;
+    CglsResult r = cgls_solve(ctx->c, in, tol, max_iter, mode == 2 ? 0 : mode, trace || row_trace);
     std::memcpy(phi, r.phi.data(), uint64_t(n) * 8);
     if (iterations) *iterations = r.iterations;
     if (rel) *rel = r.relative_residual;
@@ -1535,12 +1567,49 @@ int sf_solve_direct(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows
     if (n > 20000) throw DataError("direct solve limited to 20000 players, got " + std::to_string(n));
     if (n == 0) return;
     need(phi, "output");
+    if (rows) {
+      need(bits, "rows");
+      need(weights, "weights");
+      need(targets, "targets");
+    }
+    // runs of equal weight; rows in many short runs are first ordered by
+    // weight (G and rhs are sums over rows, so row order is free)
+    auto count_runs = [&](const double* w) {
+      uint64_t c = 0;
+      for (uint64_t i = 0; i < rows; ++i) c += (i == 0 || w[i] != w[i - 1]);
+      return c;
+    };
+    std::vector<uint64_t> pb;
+    std::vector<double> pw, pt;
+    const uint64_t* ub = bits;
+    const double *uw = weights, *ut = targets;
+    if (count_runs(weights) > std::max<uint64_t>(64, rows / 16)) {
+      std::vector<uint64_t> order(rows);
+      for (uint64_t i = 0; i < rows; ++i) order[i] = i;
+      std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return weights[a] < weights[b]; });
+      pb.resize(rows * words);
+      pw.resize(rows);
+      pt.resize(rows);
+      for (uint64_t i = 0; i < rows; ++i) {
+        std::memcpy(pb.data() + i * words, bits + order[i] * words, words * 8);
+        pw[i] = weights[order[i]];
+        pt[i] = targets[order[i]];
+      }
+      ub = pb.data();
+      uw = pw.data();
+      ut = pt.data();
+    }
+    std::vector<GramRun> runs;
+    for (uint64_t i = 0; i < rows; ++i) {
+      if (i == 0 || uw[i] != uw[i - 1]) runs.push_back(GramRun{i, i, uw[i]});
+      runs.back().end = i + 1;
+    }
     DevBuf<double> d_sw, d_tgt;
     CglsInput in;
-    solve_common(ctx, n, bits, rows, words, weights, targets, d_sw, d_tgt, in);
+    solve_common(ctx, n, ub, rows, words, uw, ut, d_sw, d_tgt, in, /*pairs=*/false);
     in.constraint_target = ct;
     in.constraint_weight = cw;
-    const auto r = gram_solve(ctx->c, in);
+    const auto r = gram_solve(ctx->c, in, runs);
     std::memcpy(phi, r.data(), uint64_t(n) * 8);
   });
 }
@@ -1562,6 +1631,7 @@ void sf_explain_options_default(sf_explain_options* o) {
   o->constraint_scale = 1.0e6;
   o->fidelity = 1;
   o->baseline_trials = 8;
+  o->solver_mode = SF_SOLVER_AUTO;
 }
 
 int sf_explain_node(sf_ctx* ctx, const sf_graph* g, const sf_model* m, uint32_t node,

@@ -275,6 +275,9 @@ struct Ctx {
   DevBuf<uint64_t> fid_streams, fid_rows;  // fidelity random-baseline jobs
   DevBuf<uint32_t> fid_sizes;
   DevBuf<uint8_t> fid_inv;
+  DevBuf<uint64_t> gram_maskt;      // direct solve: tile-transposed rows
+  DevBuf<unsigned char> gram_work;  // direct solve: plan, run weights, targets
+  DevBuf<double> gram_g;            // direct solve: Gram partials, factor, copy, rhs
   // stage outputs retained for stage-wise parity checks (sf_ctx_keep_stages)
   bool keep_stages = false;
   std::vector<float> kept_preds;  // this rank's predictions of the last explain_node
@@ -375,10 +378,21 @@ struct CglsInput {
   // optional, from launch_assemble_pairs: set bits per row, complement flags
   const uint32_t* dev_pop = nullptr;
   const uint8_t* dev_is_comp = nullptr;
+  // fixed-order mode (CglsOptions::fixed_order, solver.hpp:62-65): every
+  // cross-row sum exact, so phi is bitwise identical for any worker layout
+  bool fixed_order = false;
 };
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
-std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in);
+// Runs of rows with one weight (explain_node: a size class; solve_direct:
+// equal caller weights), rows [begin, end)
+struct GramRun {
+  uint64_t begin = 0, end = 0;
+  double weight = 0.0;
+};
+// solve_direct (solver.cpp:364-428) on the device: tcgen05 Gram, blocked
+// FP64 Cholesky with the reference's jitter retry, triangular solves
+std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in, const std::vector<GramRun>& runs);
 // players by phi descending, ties by index (solver.cpp:430-440), on the device
 std::vector<uint32_t> rank_players(Ctx& ctx, const std::vector<double>& phi);
 

@@ -396,7 +396,8 @@ CglsResult solve_cgls(const WlsProblem& p, Communicator& comm, const CglsOptions
   int conv = 0;
   bind.check_call(sf_solve_cgls(bind.ctx(), p.num_players, bits.data(), p.num_rows, W, p.weights.data(),
                                 p.targets.data(), p.constraint_target, p.constraint_weight, opts.tol, opts.max_iter,
-                                /*mode=*/0, res.phi.data(), &it, &rel, &conv, opts.trace ? trace.data() : nullptr,
+                                /*mode=*/opts.fixed_order ? 2 : 0, res.phi.data(), &it, &rel, &conv,
+                                opts.trace ? trace.data() : nullptr,
                                 opts.trace ? row_trace.data() : nullptr, cap));
   res.iterations = it;
   res.relative_residual = rel;
@@ -465,7 +466,8 @@ NodeExplanation explain_node(const Graph& g, const GcnModel& m, std::uint32_t no
   o.constraint_scale = opts.constraint_scale;
   o.fidelity = opts.fidelity ? 1 : 0;
   o.baseline_trials = opts.baseline_trials;
-  o.solver_mode = 0;
+  o.solver_mode = SF_SOLVER_CGLS;  // the reference's solver and protocol
+  o.fixed_order = opts.fixed_order ? 1 : 0;
   o.top_counts = opts.top_counts.data();
   o.num_top_counts = std::uint32_t(opts.top_counts.size());
   o.sparsities = opts.sparsities.data();

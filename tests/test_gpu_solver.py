@@ -185,3 +185,99 @@ def test_cgls_pass_variants_agree(ctx, ref, port, n, k, seed, monkeypatch):
     for name in out:
         d = np.linalg.norm(out[name] - out["bits"]) / np.linalg.norm(out["bits"])
         assert d <= 1e-8, (name, d)
+
+
+@pytest.mark.parametrize("n", [40, 300, 1000, 2100])
+def test_direct_gram_path_vs_reference(ctx, ref, port, n):
+    """solve_direct (solver.cpp:364-428) on the device: tcgen05 Gram over the
+    bit rows (per-size weight runs), blocked FP64 Cholesky, triangular
+    solves. Bar: 1e-8 of the reference's host solve_direct. Sizes cover
+    one and several 128-player tiles and the split row axis."""
+    k = max(20 * n, 4000)
+    p = sf.plan_sizes(n, k, False)
+    bits, ros = ctx.generate_masks(p, 77 + n)
+    vals = toy_game_values(bits, port)
+    base, full = 0.2, 0.8
+    want = ref.solve_direct(n, bits, vals, base, full)
+    w = sf.assemble_weights(n, bits, ros)
+    got = ctx.solve_direct(n, bits, w, vals - base, full - base, 1e6)
+    scale = max(np.abs(want).max(), 1e-12)
+    assert np.abs(got - want).max() <= 1e-8 * scale
+
+
+def test_direct_arbitrary_rows_and_weights(ctx):
+    """Caller rows (odd count, not pairs) with a distinct weight per row:
+    the rows are regrouped by weight; checked against an FP64 normal-equation
+    solve in numpy."""
+    rng = np.random.default_rng(5)
+    n, rows = 150, 901
+    dense = (rng.random((rows, n)) < 0.3)
+    dense[:, 0] |= ~dense.any(1)
+    W = (n + 63) // 64
+    bits = np.zeros((rows, W), np.uint64)
+    for e in range(n):
+        bits[:, e // 64] |= dense[:, e].astype(np.uint64) << np.uint64(e % 64)
+    w = rng.random(rows) + 0.1
+    t = rng.standard_normal(rows)
+    ct, cw = 0.5, 1e3
+    got = ctx.solve_direct(n, bits, w, t, ct, cw)
+    A = dense.astype(np.float64)
+    G = A.T @ (w[:, None] * A) + cw
+    b = A.T @ (w * t) + cw * ct
+    want = np.linalg.solve(G, b)
+    assert np.abs(got - want).max() <= 1e-8 * max(np.abs(want).max(), 1.0)
+
+
+def test_explain_direct_solver_and_dispatch(ctx, ref, port):
+    """explain_node with the direct solver (tcgen05 Gram + device Cholesky):
+    at C1 (n ~ 1K) phi is within the 1e-3 bar of the reference's CGLS
+    explanation with the same top-10; SF_SOLVER_AUTO keeps CGLS there and
+    takes the direct path for a small ball (n <= 256, the measured
+    crossover)."""
+    from paper_2506_22668_b200 import workloads as Wl
+    from paper_2506_22668_b200.api import ExplainOptions
+
+    d = Wl.build("C1")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+    base = dict(samples=cfg.samples, seed=cfg.explain_seed, fidelity=False)
+    auto = ctx.explain_node(g, m, d["target"], ExplainOptions(**base))
+    direct = ctx.explain_node(g, m, d["target"], ExplainOptions(solver_mode=2, **base))
+    cgls = ctx.explain_node(g, m, d["target"], ExplainOptions(solver_mode=0, **base))
+    assert direct.iterations == 0 and cgls.iterations > 0 and auto.iterations == cgls.iterations
+    # CGLS stops at tol 1e-6 on the gradient ratio; the direct solve is exact
+    assert np.linalg.norm(direct.phi - cgls.phi) <= 1e-3 * np.linalg.norm(cgls.phi)
+    rg = ref.graph_build(cfg.nodes, d["edges"], d["features"])
+    rm = ref.model_random(cfg.feature_dim, list(cfg.hidden), cfg.classes, cfg.model_seed)
+    rx = ref.explain_node(rg, rm, d["target"], samples=cfg.samples, seed=cfg.explain_seed, world=8)
+    assert np.linalg.norm(direct.phi - rx["phi"]) <= 1e-3 * np.linalg.norm(rx["phi"])
+    # a small ball: AUTO takes the direct path; same answer as forcing it
+    small = next(v for v in g.select_nodes("degree-range:[2,3]:200") if 20 <= g.extract(int(v), 2).n <= 256)
+    a = ctx.explain_node(g, m, int(small), ExplainOptions(**base))
+    b = ctx.explain_node(g, m, int(small), ExplainOptions(solver_mode=2, **base))
+    c = ctx.explain_node(g, m, int(small), ExplainOptions(solver_mode=0, **base))
+    assert a.iterations == 0 and np.array_equal(a.phi, b.phi)
+    assert np.linalg.norm(a.phi - c.phi) <= 1e-3 * np.linalg.norm(c.phi)
+
+
+@pytest.mark.parametrize("n", [40, 700])
+def test_fixed_order_is_layout_independent(ctx, port, n):
+    """CglsOptions::fixed_order (solver.hpp:62-65): with exact level sums the
+    solution must not depend on how pairs are laid out. Permuting the pair
+    order (same pairs, different tiles, splits and list/nibble split points)
+    gives bitwise the same phi; and it agrees with the default mode."""
+    k = 60 * n
+    p = sf.plan_sizes(n, k, False)
+    bits, ros = ctx.generate_masks(p, 300 + n)
+    vals = toy_game_values(bits, port)
+    w = sf.assemble_weights(n, bits, ros)
+    t, ct = vals - 0.25, 0.5
+    a = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=2, max_iter=4 * n)
+    perm = np.random.default_rng(n).permutation(bits.shape[0] // 2)
+    rows = np.stack([2 * perm, 2 * perm + 1], 1).reshape(-1)
+    b = ctx.solve_cgls(n, bits[rows], w[rows], t[rows], ct, 1e6, mode=2, max_iter=4 * n)
+    assert a["iterations"] == b["iterations"]
+    assert np.array_equal(a["phi"], b["phi"])
+    ref0 = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=0, max_iter=4 * n)
+    assert np.linalg.norm(a["phi"] - ref0["phi"]) <= 1e-8 * np.linalg.norm(ref0["phi"])
