@@ -35,7 +35,8 @@ WORKLOAD_DESC = {
     "C2": "C2: 3-layer GCN (602-128-128-41), Reddit-shaped power-law graph, target with a 49,648-edge "
           "computational subgraph, 500K coalitions",
     "C3": "C3: 3-layer GCN (100-128-128-47), products-shaped power-law graph, ~200K-edge subgraph, 2M coalitions",
-    "C4": "C4: 3-layer GCN (100-128-128-47), ~1M-edge subgraph, 10M coalitions",
+    "C4": "C4: 3-layer GCN (100-128-128-47), products-shaped power-law graph, 999,667-edge subgraph, "
+          "10M coalitions",
 }
 
 
@@ -124,7 +125,17 @@ def build_problem(name, sf):
     return d, cfg, g, m, sg
 
 
-def cpu_baseline(d, cfg, bounded_rows_per_thread=1, k_sample=20_000):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def cpu_baseline(d, cfg, bounded_rows_per_thread=4, k_sample=20_000):
     """Reference CPU path (oracle/_ref) on a bounded sample, all host threads."""
     from oracle.pyoracle import Ref
 
@@ -149,7 +160,7 @@ def cpu_baseline(d, cfg, bounded_rows_per_thread=1, k_sample=20_000):
         "kind": "reference",
         "sample": (f"reference generate_masks for a {t['rows_sampled']}-coalition plan of the same target "
                    f"({t['sampling_ms']:.0f} ms) + predict_batched on {t['rows_predicted']} of those coalitions "
-                   f"({t['prediction_ms']:.0f} ms), {cores} threads, extrapolated per coalition"),
+                   f"({t['prediction_ms']:.0f} ms), {cores} threads of {cpu_model()}, extrapolated per coalition"),
     }
 
 
@@ -173,7 +184,7 @@ def run_reference(args):
     cls = int(np.argmax(ref.predict_probs(rm, rsg, full)))
     seed = ref.node_sampling_seed(cfg.explain_seed, d["target"])
     ksamp = min(cfg.samples, 20_000)
-    rows_per_thread = 1 if cfg.name != "C1" else 8
+    rows_per_thread = 4 if cfg.name != "C1" else 16
     rates, secs = [], []
     for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -185,7 +196,8 @@ def run_reference(args):
             secs.append(dt)
     value = float(np.median(rates))
     sample = (f"per step: reference generate_masks for a {t['rows_sampled']}-coalition plan + predict_batched on "
-              f"{t['rows_predicted']} coalitions, {cores} threads (run_on_thread_workers), extrapolated per coalition")
+              f"{t['rows_predicted']} coalitions, {cores} threads of {cpu_model()} (run_on_thread_workers), "
+              "extrapolated per coalition")
     line = {
         "metric": "coalitions/s (sample + masked inference)", "value": value, "unit": "coalitions/s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -358,11 +370,12 @@ def run_ours(args):
             "dtype": "f32",
             "data": "synthetic",
             "config": {
-                "workload": WORKLOAD_DESC.get(cfg.name, cfg.name),
+                "workload": WORKLOAD_DESC.get(cfg.name, cfg.name) + ("" if k == cfg.samples else
+                                                                     f" (run with k = {k:,} coalitions)"),
                 "coalitions": k, "players": int(sg.n), "subgraph_nodes": int(sg.V),
                 "ball_sizes": sg.ball_sizes(cfg.hops), "parallelism": f"coalition pairs g mod {world}",
-                "l2": "inputs larger than L2 (masks regenerated each step: "
-                      f"{2 * ((k // 2 + world - 1) // world) * max(sg.words, 1) * 8 / 1e9:.2f} GB per rank)",
+                "l2": "inputs larger than L2 (kept-set mask rows regenerated each step: "
+                      f"{((k // 2 + world - 1) // world) * max(sg.words, 1) * 8 / 1e9:.2f} GB per rank)",
                 "accuracy_mode": ("tcgen05 3xTF32 (FP32-equivalent products, FP32 accumulate)"
                                   if kernel_used == "tc" else "FP32 SIMT (CUDA cores)") + ", FP64 solver",
             },
@@ -383,7 +396,7 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = cpu_baseline(d, cfg, 8 if cfg.name == "C1" else 1)
+                line["cpu_baseline"] = cpu_baseline(d, cfg, 16 if cfg.name == "C1" else 4)
             except Exception as exc:  # the oracle is test infrastructure; report why it is absent
                 line["cpu_baseline"] = {"value": None, "unavailable": str(exc)}
         print(json.dumps(line), flush=True)

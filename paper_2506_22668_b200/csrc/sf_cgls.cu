@@ -80,27 +80,32 @@ __global__ void reduce_stage2(const double* __restrict__ part, int count,
 // weights, list sizes) and is_comp[j] = (row 2j+1 == ~row 2j, tail cleared)
 // (solver.cpp:188-198)
 __global__ void pair_scan_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint32_t n, uint64_t pairs,
-                                 uint32_t* __restrict__ pop, uint8_t* __restrict__ is_comp) {
+                                 uint32_t* __restrict__ pop, uint8_t* __restrict__ is_comp, int kept_only) {
   const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= pairs) return;
   const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
-  const uint64_t* e = rows + 2 * j * W;
+  const uint64_t* e = rows + (kept_only ? j : 2 * j) * W;
   const uint64_t* o = e + W;
   uint32_t pe = 0, po = 0;
   bool ok = true;
   for (uint32_t w = lane; w < W; w += 32) {
-    const uint64_t x = e[w], y = o[w];
+    const uint64_t x = e[w];
     pe += __popcll(x);
-    po += __popcll(y);
-    ok &= (y == ((w == W - 1) ? (~x & tail) : ~x));
+    if (!kept_only) {
+      const uint64_t y = o[w];
+      po += __popcll(y);
+      ok &= (y == ((w == W - 1) ? (~x & tail) : ~x));
+    }
   }
+
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     pe += __shfl_xor_sync(kFull, pe, d);
     po += __shfl_xor_sync(kFull, po, d);
   }
   ok = __all_sync(kFull, ok);
+  if (kept_only) po = n - pe;
   if (lane == 0) {
     pop[2 * j] = pe;
     pop[2 * j + 1] = po;
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kFwdThreads)
                    const uint8_t* __restrict__ is_comp, const double* __restrict__ u,
                    uint32_t n, const double* __restrict__ sw,
                    const double* __restrict__ sum_u, double* __restrict__ v,
-                   double* __restrict__ dsq_part) {
+                   double* __restrict__ dsq_part, int kept_only) {
   extern __shared__ double su[];  // min(n, kFwdChunk) doubles
   __shared__ double rowsum[kFwdRows];
   __shared__ double red[kFwdThreads / 32];
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(kFwdThreads)
       const uint32_t rl = nr - 1 - f;
       const uint64_t row = r0 + rl;
       if ((row & 1) && is_comp[row >> 1]) continue;
-      const uint64_t* rp = rows + row * W;
+      const uint64_t* rp = rows + (kept_only ? (row >> 1) : row) * W;
       double acc0 = 0.0, acc1 = 0.0;
       // all of this lane's words of the chunk are loaded before any is used
       uint64_t xs[kFwdWordsPerLane];
@@ -310,15 +315,15 @@ __global__ void __launch_bounds__(256)
 // zero rows to a whole number of 256-pair blocks), so the forward pass reads
 // one coalesced 8-byte word per lane. Built once per solve.
 __global__ void __launch_bounds__(256)
-    rows_word_major_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t pd, uint64_t pairs,
-                           uint64_t pstride, uint64_t* __restrict__ rT) {
+    rows_word_major_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t row_step, uint64_t pd,
+                           uint64_t pairs, uint64_t pstride, uint64_t* __restrict__ rT) {
   __shared__ uint64_t t[32][33];
   const uint32_t w0 = blockIdx.x * 32;
   const uint64_t jl0 = blockIdx.y * 32ull;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int r = ty; r < 32; r += 8) {  // r: pair within the tile, tx: word
     const uint64_t j = pd + jl0 + r;
-    t[r][tx] = (j < pairs && w0 + tx < W) ? rows[2 * j * W + w0 + tx] : 0ull;
+    t[r][tx] = (j < pairs && w0 + tx < W) ? rows[j * row_step + w0 + tx] : 0ull;
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8)  // r: word, tx: pair
@@ -412,12 +417,12 @@ __global__ void even_pop_kernel(const uint32_t* __restrict__ pop, uint64_t pd, u
 }
 
 // warp per pair: the even row's set bits in ascending order
-__global__ void row_list_fill_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t pd,
-                                     const uint64_t* __restrict__ off, uint32_t* __restrict__ idx) {
+__global__ void row_list_fill_kernel(const uint64_t* __restrict__ rows, uint32_t W, uint64_t row_step,
+                                     uint64_t pd, const uint64_t* __restrict__ off, uint32_t* __restrict__ idx) {
   const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= pd) return;
-  const uint64_t* rp = rows + 2 * j * W;
+  const uint64_t* rp = rows + j * row_step;
   uint64_t base = off[j];
   for (uint32_t wb = 0; wb < W; wb += 32) {
     const uint32_t w = wb + lane;
@@ -533,6 +538,37 @@ __global__ void axpy_kernel(double* __restrict__ y, const double* __restrict__ x
   if (i >= n) return;
   const double a = sign * (*alpha_num / *alpha_den);
   y[i] += a * x[i];
+}
+
+// One CGLS step's scalars on the device (solver.cpp:282-296): delta =
+// ||v||^2 (all-reduced, scal[1]) + v_c^2 with v_c = sqrt(cw) sum_u
+// (scal[0]); stop flag scal[12] = 2 non-finite, 1 delta <= 0; theta =
+// gamma / delta applied through scal[8] / scal[9]; r_c (scal[7]) -= theta v_c.
+__global__ void step_kernel(double* __restrict__ scal, double scw, int gslot) {
+  const double v_c = scw * scal[0];
+  const double delta = scal[1] + v_c * v_c;
+  const double stop = !isfinite(delta) ? 2.0 : (delta <= 0.0 ? 1.0 : 0.0);
+  scal[9] = delta;
+  scal[12] = stop;
+  if (stop == 0.0) {
+    const double gamma = scal[gslot];
+    scal[8] = gamma;
+    scal[7] -= (gamma / delta) * v_c;
+  }
+}
+
+// y += sign (num / den) x unless *stop is set
+__global__ void axpy_stop_kernel(double* __restrict__ y, const double* __restrict__ x,
+                                 const double* __restrict__ scal, double sign, uint64_t n) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n || scal[12] != 0.0) return;
+  y[i] += sign * (scal[8] / scal[9]) * x[i];
+}
+
+// s += sqrt(cw) r_c (the pin row), r_c on the device
+__global__ void add_pin_kernel(double* __restrict__ s, double scw, const double* __restrict__ r_c, uint32_t n) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) s[e] += scw * (*r_c);
 }
 
 // u = s + beta u, beta = gamma_next / gamma (solver.cpp:357-358)
@@ -766,20 +802,23 @@ __global__ void assemble_pairs_kernel(const uint64_t* __restrict__ rows, uint64_
                                       const float* __restrict__ values, double base,
                                       double* __restrict__ sw, double* __restrict__ tgt,
                                       int* __restrict__ bad, uint32_t* __restrict__ pop,
-                                      uint8_t* __restrict__ is_comp) {
+                                      uint8_t* __restrict__ is_comp, int kept_only) {
   const uint64_t j = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= pairs) return;
   const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
-  const uint64_t* e = rows + 2 * j * W;
+  const uint64_t* e = rows + (kept_only ? j : 2 * j) * W;
   const uint64_t* o = e + W;
   uint32_t pe = 0, po = 0;
   bool ok = true;
   for (uint32_t w = lane; w < W; w += 32) {
-    const uint64_t x = e[w], y = o[w];
+    const uint64_t x = e[w];
     pe += __popcll(x);
-    po += __popcll(y);
-    ok &= (y == ((w == W - 1) ? (~x & tail) : ~x));
+    if (!kept_only) {
+      const uint64_t y = o[w];
+      po += __popcll(y);
+      ok &= (y == ((w == W - 1) ? (~x & tail) : ~x));
+    }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
@@ -787,6 +826,7 @@ __global__ void assemble_pairs_kernel(const uint64_t* __restrict__ rows, uint64_
     po += __shfl_xor_sync(kFull, po, d);
   }
   ok = __all_sync(kFull, ok);
+  if (kept_only) po = n - pe;  // the complement row
   if (lane < 2) {
     const uint64_t row = 2 * j + lane;
     const uint32_t cnt = lane ? po : pe;
@@ -846,12 +886,13 @@ void launch_assemble(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
 
 void launch_assemble_pairs(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows, uint32_t W, uint32_t n,
                            const double* dev_wsize, const float* dev_values, double base, double* dev_sw,
-                           double* dev_targets, int* dev_bad_row, uint32_t* dev_pop, uint8_t* dev_is_comp) {
+                           double* dev_targets, int* dev_bad_row, uint32_t* dev_pop, uint8_t* dev_is_comp,
+                           bool kept_only) {
   if (rows == 0) return;
   if (rows % 2) throw DataError("assemble_pairs needs adjacent row pairs");
   assemble_pairs_kernel<<<blocks_for(rows / 2 * 32), 256, 0, ctx.stream>>>(
       dev_rows, rows / 2, W, n, dev_wsize, dev_values, base, dev_sw, dev_targets, dev_bad_row, dev_pop,
-      dev_is_comp);
+      dev_is_comp, kept_only ? 1 : 0);
   SF_LAUNCHED(ctx);
 }
 
@@ -883,7 +924,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t bytes = 2 * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
                          (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
-                         uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 16 * 256;
+                         uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 32 * 8 + 16 * 256;
   const bool repro = in.fixed_order;
   if (repro && mode != 0) throw DataError("fixed-order summation runs the reference protocol (solver mode 0)");
   constexpr int kBins = 2201;  // frexp exponents -1100..1100
@@ -928,7 +969,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* red = sc.take<double>(kRedBlocks);
   // device scalars: 0 sum_u, 1 delta, 2 gamma, 3 gamma_next, 4 kconst,
   // 5 sse, 6 data0
-  double* scal = sc.take<double>(16);
+  double* scal = sc.take<double>(32);
 
   cudaStream_t st = ctx.stream;
   auto reduce = [&](const double* x, uint64_t count, int md, double c, double* out) {
@@ -937,7 +978,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     reduce_stage2<<<1, kRedBlocks, 0, st>>>(red, kRedBlocks, out);
     SF_LAUNCHED(ctx);
   };
-  ctx.solver_host.reserve(16);
+  ctx.solver_host.reserve(32);
   double* host = ctx.solver_host.p;
   auto fetch = [&](int idx, int count) {
     ctx.d2h_bytes += uint64_t(count) * sizeof(double);
@@ -947,10 +988,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   };
 
   DebugTimer dt("cgls");
-  launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, 2ull * W);
+  const uint64_t pair_step = in.kept_only ? uint64_t(W) : 2ull * W;  // words between even rows
+  launch_transpose_tiles(ctx, in.dev_rows, pairs, W, ptiles, mte, pair_step);
   if (pairs) {
     if (!in.dev_pop || !in.dev_is_comp) {
-      pair_scan_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, pop, is_comp);
+      pair_scan_kernel<<<blocks_for(pairs * 32), 256, 0, st>>>(in.dev_rows, W, n, pairs, pop, is_comp,
+                                                                in.kept_only ? 1 : 0);
       SF_LAUNCHED(ctx);
     }
     init_r_kernel<<<blocks_for(rows), 256, 0, st>>>(in.dev_sw, in.dev_targets, rows, r);
@@ -968,6 +1011,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   auto needed = [&](uint64_t row) { return !((row & 1) && h_comp[row >> 1]); };
   bool any_noncomp = false;
   for (uint64_t j = 0; j < pairs; ++j) any_noncomp |= !h_comp[j];
+  if (any_noncomp && in.kept_only) throw std::logic_error("kept-only rows are complement pairs");
   if (any_noncomp) launch_transpose_tiles(ctx, in.dev_rows + W, pairs, W, ptiles, mto, 2ull * W);
 
   // Dense tiles (pairs from pd on) take the nibble-table passes, sparse
@@ -1050,7 +1094,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
         SF_CUDA(cudaStreamSynchronize(st));
         dt.lap("lists: scans");
       }
-      row_list_fill_kernel<<<blocks_for(pd * 32), 256, 0, st>>>(in.dev_rows, W, pd, r_off, r_idx);
+      row_list_fill_kernel<<<blocks_for(pd * 32), 256, 0, st>>>(in.dev_rows, W, pair_step, pd, r_off, r_idx);
       SF_LAUNCHED(ctx);
       player_list_fill_kernel<<<dim3(blocks_for(n), lsegs), 256, 0, st>>>(mte, Wp, n, tiles_b, lsegs, p_off,
                                                                          p_idx);
@@ -1126,7 +1170,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   if (pairs_n) {
     ctx.solver_dense.reserve(uint64_t(W) * pstride);
     rT = ctx.solver_dense.p;
-    rows_word_major_kernel<<<dim3((W + 31) / 32, unsigned(pstride / 32)), 256, 0, st>>>(in.dev_rows, W, pd, pairs,
+    rows_word_major_kernel<<<dim3((W + 31) / 32, unsigned(pstride / 32)), 256, 0, st>>>(in.dev_rows, W, pair_step, pd, pairs,
                                                                                       pstride, rT);
     SF_LAUNCHED(ctx);
   }
@@ -1236,7 +1280,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     }
     if (fblocks) {
       forward_kernel<<<unsigned(fblocks), kFwdThreads, size_t(std::min<uint32_t>(n, kFwdChunk)) * 8, st>>>(
-          in.dev_rows, W, row_start, is_comp, x, n, swp, sum_u, vout, dsq);
+          in.dev_rows, W, row_start, is_comp, x, n, swp, sum_u, vout, dsq, in.kept_only ? 1 : 0);
       SF_LAUNCHED(ctx);
     }
     if (nb_rowblocks) {
@@ -1437,6 +1481,58 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     return res;
   }
   DebugTimer di("cgls iteration");
+  if (!trace && !repro) {
+    // One host round trip per iteration: delta, theta, r_c and beta stay on
+    // the device; the host reads (delta, stop flag, gamma_next) once after
+    // the transpose and applies the reference's stop rule and error
+    // semantics. A stopped step (delta <= 0 or non-finite) leaves phi and
+    // r untouched, like the reference's break before the update.
+    host[7] = r_c;
+    SF_CUDA(cudaMemcpyAsync(scal + 7, host + 7, sizeof(double), cudaMemcpyHostToDevice, st));
+    int g = 2;  // gamma slot (scal[2] from the init reduce); gamma_next goes to 5 - g
+    while (res.iterations < maxit) {
+      reduce(u, n, 0, 0.0, scal + 0);  // sum_u
+      if (rows) forward_v(u, in.dev_sw, scal + 0, v);
+      reduce(dsq, rows ? fwd_blocks : 0, 0, 0.0, scal + 1);
+      comm_allreduce_sum(ctx, scal + 1, 1);
+      step_kernel<<<1, 1, 0, st>>>(scal, scw, g);
+      SF_LAUNCHED(ctx);
+      axpy_stop_kernel<<<blocks_for(n), 256, 0, st>>>(phi, u, scal, 1.0, n);
+      SF_LAUNCHED(ctx);
+      if (rows) {
+        axpy_stop_kernel<<<blocks_for(rows), 256, 0, st>>>(r, v, scal, -1.0, rows);
+        SF_LAUNCHED(ctx);
+      }
+      transpose_local(r, s);
+      comm_allreduce_sum(ctx, s, n);
+      add_pin_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw, scal + 7, n);
+      SF_LAUNCHED(ctx);
+      reduce(s, n, 1, 0.0, scal + (5 - g));  // gamma_next
+      direction_kernel<<<blocks_for(n), 256, 0, st>>>(u, s, scal + (5 - g), scal + g, n);
+      SF_LAUNCHED(ctx);
+      ctx.d2h_bytes += 16 * sizeof(double);
+      SF_CUDA(cudaMemcpyAsync(host, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      comm_sync(ctx);
+      if (host[12] == 2.0)
+        throw NumericalError("iterative solve diverged at iteration " + std::to_string(res.iterations) +
+                             ": non-finite step norm");
+      if (host[12] == 1.0) break;
+      const double gamma_next = host[5 - g];
+      ++res.iterations;
+      res.relative_residual = std::sqrt(gamma_next / reference);
+      if (!std::isfinite(gamma_next) || res.relative_residual > blowup)
+        throw NumericalError("iterative solve diverged at iteration " + std::to_string(res.iterations) +
+                             ": residual exploded");
+      if (res.relative_residual <= tol) {
+        res.converged = true;
+        break;
+      }
+      g = 5 - g;
+      di.lap("");
+    }
+    download_phi();
+    return res;
+  }
   while (res.iterations < maxit) {
     di.lap("");
     double delta = 0.0, v_c = 0.0;

@@ -1062,7 +1062,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
 
 void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                     uint32_t cls, float* dev_out, float* dev_allprobs,
-                    float* dominant_ms) {
+                    float* dominant_ms, bool kept_only) {
   (void)dominant_ms;
   Engine& e = ctx.engine;
   if (rows == 0) return;
@@ -1120,7 +1120,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
     const uint64_t row0 = t0 * kTile;
     const uint64_t nrows = std::min<uint64_t>(rows - row0, nt * kTile);
     const uint64_t ntp = wide ? (nt + 1) & ~uint64_t(1) : nt;  // tiles the fused kernel covers
-    launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, ntp, maskt);
+    if (kept_only)  // row0 is a multiple of 64: pairs from row0 / 2
+      launch_transpose_pairs(ctx, dev_rows + (row0 / 2) * e.W, (nrows + 1) / 2, e.W, uint32_t(e.n), ntp, maskt);
+    else
+      launch_transpose_tiles(ctx, dev_rows + row0 * e.W, nrows, e.W, ntp, maskt);
     {
       // small-node warps: split the tiles when there are too few nodes to
       // fill 148 SMs x 64 warps (chunks of a multiple of 32 tiles)

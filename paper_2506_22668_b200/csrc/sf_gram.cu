@@ -522,7 +522,10 @@ std::vector<double> gram_solve(Ctx& ctx, const CglsInput& in, const std::vector<
     dt.lap(what);
   };
   ctx.gram_maskt.reserve(std::max<uint64_t>(tiles * Wp, 1));
-  launch_transpose_tiles(ctx, in.dev_rows, rows, W, tiles, ctx.gram_maskt.p);
+  if (in.kept_only)
+    launch_transpose_pairs(ctx, in.dev_rows, rows / 2, W, n, tiles, ctx.gram_maskt.p);
+  else
+    launch_transpose_tiles(ctx, in.dev_rows, rows, W, tiles, ctx.gram_maskt.p);
   const uint64_t rhs_parts = std::max<uint64_t>(1, (tiles + 255) / 256);
   const uint64_t wbytes = ent.size() * sizeof(GramEntry) + (splits + 1) * 4 + run_w.size() * 8 +
                           rows * 4 + (tiles * 64 + 1) * 8 + rhs_parts * n * 8 + 16 * 256;

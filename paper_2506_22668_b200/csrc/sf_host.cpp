@@ -673,8 +673,10 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     sdt.lap("plan");
     const uint64_t pairs = local_pair_count(plan.total_pairs(), ctx.rank, ctx.world);
     const uint64_t rows = 2 * pairs;
-    ctx.masks.reserve(std::max<uint64_t>(rows * W, 1));
-    launch_generate_masks(ctx, plan, seed, ctx.rank, ctx.world, ctx.masks.p);
+    // kept-set rows only (the complement of every pair is derived where it
+    // is read): half the mask bytes in HBM and half the sampler writes
+    ctx.masks.reserve(std::max<uint64_t>(pairs * W, 1));
+    launch_generate_masks(ctx, plan, seed, ctx.rank, ctx.world, ctx.masks.p, /*kept_only=*/true);
     sdt.lap("launch");
     comm_barrier(ctx);
     sdt.lap("masks");
@@ -685,7 +687,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     t_stage = Clock::now();
     engine_prepare(ctx, sg, m);
     ctx.preds.reserve(std::max<uint64_t>(rows, 1));
-    engine_predict(ctx, ctx.masks.p, rows, out->predicted_class, ctx.preds.p, nullptr, nullptr);
+    engine_predict(ctx, ctx.masks.p, rows, out->predicted_class, ctx.preds.p, nullptr, nullptr, /*kept_only=*/true);
     comm_barrier(ctx);
     out->prediction_ms = ms_since(t_stage);
     if (ctx.keep_stages) {
@@ -708,7 +710,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     ctx.pop_dev.reserve(std::max<uint64_t>(rows, 1));
     ctx.comp_dev.reserve(std::max<uint64_t>(rows / 2, 1));
     launch_assemble_pairs(ctx, ctx.masks.p, rows, W, n, d_wsize.p, ctx.preds.p, out->base_score, d_sw.p,
-                          d_tgt.p, d_bad.p, ctx.pop_dev.p, ctx.comp_dev.p);
+                          d_tgt.p, d_bad.p, ctx.pop_dev.p, ctx.comp_dev.p, /*kept_only=*/true);
     ctx.h2d_bytes += wsize.size() * 8 + 4;
     ctx.d2h_bytes += 4;
     int bad = big;
@@ -728,6 +730,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     in.global_pair_count = plan.total_pairs();
     in.dev_pop = ctx.pop_dev.p;
     in.dev_is_comp = ctx.comp_dev.p;
+    in.kept_only = true;
     DebugTimer("explain").lap("assemble done");
     // Solver dispatch: the direct (tcgen05 Gram + device Cholesky) path
     // for small player counts on one worker, CGLS otherwise. Crossover
@@ -1789,7 +1792,7 @@ int sf_sample_and_predict(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
     const SizePlan plan = plan_sizes(n, k, allow_exhaustive != 0);
     const uint64_t rows = 2 * local_pair_count(plan.total_pairs(), c.rank, c.world);
     const uint32_t W = std::max<uint32_t>(1, (n + 63) / 64);
-    c.masks.reserve(std::max<uint64_t>(rows * W, 1));
+    c.masks.reserve(std::max<uint64_t>(rows / 2 * W, 1));  // kept-set rows only
     c.preds.reserve(std::max<uint64_t>(rows, 1));
     engine_prepare(c, sg->s, m->m);
     cudaEvent_t e0, e1, e2;
@@ -1797,10 +1800,10 @@ int sf_sample_and_predict(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
     SF_CUDA(cudaEventCreate(&e1));
     SF_CUDA(cudaEventCreate(&e2));
     SF_CUDA(cudaEventRecord(e0, c.stream));
-    launch_generate_masks(c, plan, seed, c.rank, c.world, c.masks.p);
+    launch_generate_masks(c, plan, seed, c.rank, c.world, c.masks.p, /*kept_only=*/true);
     SF_CUDA(cudaEventRecord(e1, c.stream));
     float dom = 0.f;
-    engine_predict(c, c.masks.p, rows, cls, c.preds.p, nullptr, stage_ms ? &dom : nullptr);
+    engine_predict(c, c.masks.p, rows, cls, c.preds.p, nullptr, stage_ms ? &dom : nullptr, /*kept_only=*/true);
     SF_CUDA(cudaEventRecord(e2, c.stream));
     SF_CUDA(cudaEventSynchronize(e2));
     float a = 0.f, b = 0.f;

@@ -322,8 +322,14 @@ void launch_philox_stream(Ctx& ctx, uint64_t seed, uint64_t stream,
 // Generates this rank's rows (row-major, 2 rows per local pair) into
 // dev_rows; also writes the tile-transposed kept-set layout when dev_maskt
 // is non-null.
+// kept_only: row j holds local pair j's kept-set only (W words per pair;
+// the complement row is derived by every consumer) — half the mask bytes
 void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
-                           int rank, int world, uint64_t* dev_rows);
+                           int rank, int world, uint64_t* dev_rows, bool kept_only = false);
+// kept-only pair rows -> tile layout with the complement rows interleaved
+// (bit 2i = pair i kept, bit 2i+1 = its complement, players < n)
+void launch_transpose_pairs(Ctx& ctx, const uint64_t* dev_kept, uint64_t pairs, uint32_t W, uint32_t n,
+                            uint64_t tiles, uint64_t* dev_maskt);
 // Independent Floyd draws (fidelity baselines, fidelity.cpp:25-33): row j
 // is the size-sizes[j] subset drawn from Philox(seed, streams[j]), or the
 // full row minus that subset when invert[j] != 0.
@@ -343,7 +349,7 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m);
 // `cls`) and, when dev_allprobs is non-null, every class probability.
 void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                     uint32_t cls, float* dev_out, float* dev_allprobs,
-                    float* dominant_ms);
+                    float* dominant_ms, bool kept_only = false);
 
 // sf_fused_tc.cu
 bool tc_width(uint64_t d);
@@ -381,6 +387,9 @@ struct CglsInput {
   // fixed-order mode (CglsOptions::fixed_order, solver.hpp:62-65): every
   // cross-row sum exact, so phi is bitwise identical for any worker layout
   bool fixed_order = false;
+  // dev_rows holds kept-set rows only (one per pair, W words each; every
+  // pair a complement pair)
+  bool kept_only = false;
 };
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
@@ -408,6 +417,6 @@ void launch_assemble_pairs(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
                            uint32_t W, uint32_t n, const double* dev_wsize,
                            const float* dev_values, double base, double* dev_sw,
                            double* dev_targets, int* dev_bad_row, uint32_t* dev_pop,
-                           uint8_t* dev_is_comp);
+                           uint8_t* dev_is_comp, bool kept_only = false);
 
 }  // namespace sfb

@@ -154,7 +154,7 @@ __device__ uint64_t unrank(uint64_t idx, uint32_t m, uint32_t t,
 
 __global__ void exhaustive_kernel(ClassTable ct, uint32_t n, int rank,
                                   int world, uint64_t local_pairs,
-                                  uint64_t* rows) {
+                                  uint64_t* rows, int kept_only) {
   const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (j >= local_pairs) return;
   const uint64_t g = rank + j * uint64_t(world);
@@ -167,6 +167,10 @@ __global__ void exhaustive_kernel(ClassTable ct, uint32_t n, int rank,
   else
     sub = unrank(idx, n, s, 0);
   const uint64_t tail = (n % 64) ? ((1ull << (n % 64)) - 1) : ~0ull;
+  if (kept_only) {
+    rows[j] = sub;
+    return;
+  }
   rows[2 * j] = sub;
   rows[2 * j + 1] = ~sub & tail;
 }
@@ -174,7 +178,7 @@ __global__ void exhaustive_kernel(ClassTable ct, uint32_t n, int rank,
 template <bool kSmem>
 __global__ void __launch_bounds__(kSamplerWarps * 32)
     floyd_kernel(ClassTable ct, uint32_t n, uint32_t W, uint64_t seed,
-                 int rank, int world, uint64_t local_pairs, uint64_t* rows) {
+                 int rank, int world, uint64_t local_pairs, uint64_t* rows, int kept_only) {
   extern __shared__ uint64_t smem_sets[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -185,7 +189,9 @@ __global__ void __launch_bounds__(kSamplerWarps * 32)
     const uint64_t g = rank + j * uint64_t(world);
     const uint32_t ci = find_class(ct, g);
     const uint32_t s = ct.size[ci];
-    uint64_t* even = rows + (2 * j) * W;
+    // kept-only layout: row j = the kept-set of local pair j (the odd row is
+    // its complement, derived by the consumers); full layout: rows 2j, 2j+1
+    uint64_t* even = rows + (kept_only ? j : 2 * j) * W;
     uint64_t* odd = even + W;
     uint64_t* bits = kSmem ? smem_sets + size_t(warp) * W : even;
     for (uint32_t w = lane; w < W; w += 32) bits[w] = 0;
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(kSamplerWarps * 32)
     for (uint32_t w = lane; w < W; w += 32) {
       const uint64_t v = kSmem ? bits[w] : __ldcg(&bits[w]);
       if (kSmem) even[w] = v;
-      odd[w] = (w == W - 1) ? (~v & tail) : ~v;
+      if (!kept_only) odd[w] = (w == W - 1) ? (~v & tail) : ~v;
     }
     __syncwarp();
   }
@@ -291,6 +297,61 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Kept-only rows -> tile layout: tile t covers local pairs 32t..32t+31;
+// out[t][e] bit 2i = bit e of pair (32t+i)'s kept-set row, bit 2i+1 = its
+// complement (players e < n only; rows past `pairs` are zero). One CTA per
+// (tile, kTWords-word chunk): 32 rows x kTWords words staged in shared
+// memory; per word two 32 x 32 butterfly transposes give, for each player,
+// the 32 pair bits, which are spread to the even bit positions and their
+// complement to the odd ones.
+__device__ __forceinline__ uint64_t spread_even(uint32_t x) {
+  uint64_t v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+    transpose_pairs_kernel(const uint64_t* __restrict__ in, uint64_t pairs, uint32_t W, uint32_t n,
+                           uint64_t* __restrict__ out) {
+  __shared__ uint64_t sm[32][kTWords + 1];
+  const uint64_t t = blockIdx.y;
+  const uint32_t w0 = blockIdx.x * kTWords;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 32 * kTWords; i += 256) {
+    const int r = i / kTWords, w = i % kTWords;
+    const uint64_t j = t * 32 + r;
+    sm[r][w] = (j < pairs && w0 + w < W) ? in[j * W + w0 + w] : 0ull;
+  }
+  __syncthreads();
+  const uint64_t Wp = uint64_t(W) * 64;
+  const uint64_t left = pairs > t * 32 ? pairs - t * 32 : 0;
+  const uint32_t npairs = left > 32 ? 32u : uint32_t(left);
+  const uint32_t valid = npairs == 32 ? 0xFFFFFFFFu : ((1u << npairs) - 1u);
+#pragma unroll 1
+  for (int w = warp * (kTWords / 8); w < (warp + 1) * (kTWords / 8); ++w) {
+    if (w0 + w >= W) break;
+    const uint64_t r0 = sm[lane][w];
+    uint32_t a = uint32_t(r0), b = uint32_t(r0 >> 32);
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                       : s == 2 ? 0x33333333u : 0x55555555u;
+      const uint32_t keep = (lane & s) ? ~m : m, amt = (lane & s) ? 32 - s : s;
+      a = bfly_step(a, s, keep, amt);
+      b = bfly_step(b, s, keep, amt);
+    }
+    const uint32_t ea = (w0 + w) * 64 + lane, eb = ea + 32;
+    const uint32_t ca = ea < n ? (~a & valid) : 0u, cb = eb < n ? (~b & valid) : 0u;
+    uint64_t* o = out + t * Wp + uint64_t(w0 + w) * 64;
+    o[lane] = spread_even(a) | (spread_even(ca) << 1);
+    o[lane + 32] = spread_even(b) | (spread_even(cb) << 1);
+  }
+}
+
 }  // namespace
 
 void launch_philox_stream(Ctx& ctx, uint64_t seed, uint64_t stream,
@@ -303,7 +364,7 @@ void launch_philox_stream(Ctx& ctx, uint64_t seed, uint64_t stream,
 }
 
 void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
-                           int rank, int world, uint64_t* dev_rows) {
+                           int rank, int world, uint64_t* dev_rows, bool kept_only) {
   const uint64_t pairs = local_pair_count(plan.total_pairs(), rank, world);
   if (pairs == 0) return;
   const uint32_t n = plan.n;
@@ -336,7 +397,7 @@ void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
   ClassTable ct{ctx.plan_dev32.p, ctx.plan_dev64.p, ctx.plan_dev64.p + C, static_cast<uint32_t>(C)};
   if (plan.exhaustive) {
     exhaustive_kernel<<<unsigned((pairs + 127) / 128), 128, 0, ctx.stream>>>(
-        ct, n, rank, world, pairs, dev_rows);
+        ct, n, rank, world, pairs, dev_rows, kept_only ? 1 : 0);
     SF_LAUNCHED(ctx);
   } else {
     int sms = 148;
@@ -351,11 +412,11 @@ void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
       SF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSamplerWarps * 32, smem));
       const uint64_t grid = std::min<uint64_t>(want, uint64_t(sms) * std::max(per_sm, 1) * 4);
       k<<<unsigned(grid), kSamplerWarps * 32, smem, ctx.stream>>>(
-          ct, n, W, seed, rank, world, pairs, dev_rows);
+          ct, n, W, seed, rank, world, pairs, dev_rows, kept_only ? 1 : 0);
     } else {
       const uint64_t grid = std::min<uint64_t>(want, uint64_t(sms) * 16);
       floyd_kernel<false><<<unsigned(grid), kSamplerWarps * 32, 0, ctx.stream>>>(
-          ct, n, W, seed, rank, world, pairs, dev_rows);
+          ct, n, W, seed, rank, world, pairs, dev_rows, kept_only ? 1 : 0);
     }
     SF_LAUNCHED(ctx);
   }
@@ -382,6 +443,14 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
     floyd_jobs_kernel<false><<<grid, kSamplerWarps * 32, 0, ctx.stream>>>(n, W, seed, dev_streams, dev_sizes,
                                                                           dev_invert, jobs, dev_rows);
   }
+  SF_LAUNCHED(ctx);
+}
+
+void launch_transpose_pairs(Ctx& ctx, const uint64_t* dev_kept, uint64_t pairs, uint32_t W, uint32_t n,
+                            uint64_t tiles, uint64_t* dev_maskt) {
+  if (tiles == 0) return;
+  dim3 grid((W + kTWords - 1) / kTWords, unsigned(tiles));
+  transpose_pairs_kernel<<<grid, 256, 0, ctx.stream>>>(dev_kept, pairs, W, n, dev_maskt);
   SF_LAUNCHED(ctx);
 }
 

@@ -89,3 +89,43 @@ def test_c5_widths_vs_reference(ctx, ref):
         want = ref.predict_batched(rm, rg, target, bits, classes - 1, sg=sgr)
         assert rel_err(got, want) <= RTOL
         ref.cg_free(sgr)
+
+
+@pytest.fixture(scope="module")
+def c4(ref):
+    d = W.build("C4")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    rg = ref.graph_build(cfg.nodes, d["edges"], d["features"])
+    m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+    rm = ref.model_random(cfg.feature_dim, list(cfg.hidden), cfg.classes, cfg.model_seed)
+    sg = g.extract(d["target"], cfg.hops)
+    sgr = ref.extract(rg, d["target"], cfg.hops, keep_handle=True)
+    yield dict(d=d, cfg=cfg, g=g, rg=rg, m=m, rm=rm, sg=sg, sgr=sgr)
+    ref.cg_free(sgr)
+
+
+@pytest.mark.slow
+def test_c4_rank_block_and_predictions(ctx, ref, c4):
+    """C4 (3-layer, 1M-edge computational subgraph, n = 999,667 players):
+    rank 5 of 8's mask block bit-exact with the reference sampler (the
+    global-memory Floyd path: sets of up to n/2 = 500K players do not fit in
+    shared memory), and predictions on a spread of its rows within 1e-5 of
+    the reference's predict_batched."""
+    sg, cfg = c4["sg"], c4["cfg"]
+    assert sg.n == c4["sgr"].n and sg.n > 990_000
+    k, seed, rank, world = 16_000, 99, 5, 8
+    p = sf.plan_sizes(sg.n, k, True)
+    bits, ros = ctx.generate_masks(p, seed, rank, world)
+    want, want_ros = ref.generate_masks(sg.n, k, seed, rank, world)
+    assert np.array_equal(bits, want)
+    assert np.array_equal(np.asarray(ros, np.uint64), np.asarray(want_ros, np.uint64))
+    got = ctx.predict_batched(c4["m"], sg, bits, 11)
+    pick = np.r_[0:4, bits.shape[0] // 2:bits.shape[0] // 2 + 4, bits.shape[0] - 4:bits.shape[0]]
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(len(pick)) as ex:
+        outs = list(ex.map(lambda r: ref.predict_batched(c4["rm"], c4["rg"], c4["d"]["target"], bits[r:r + 1], 11,
+                                                         sg=c4["sgr"]), pick))
+    assert rel_err(got[pick], np.concatenate(outs)) <= RTOL
