@@ -353,6 +353,8 @@ def run_ours(args):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / max(e2e_steps, 1))
     h2d1, d2h1 = C.c_uint64(), C.c_uint64()
     sf.lib.sf_ctx_io_bytes(ctx.h, C.byref(h2d1), C.byref(d2h1))
+    used_b, total_b = C.c_uint64(), C.c_uint64()
+    sf.lib.sf_ctx_device_memory(ctx.h, C.byref(used_b), C.byref(total_b))
 
     line = None
     if rank == 0:
@@ -391,6 +393,8 @@ def run_ours(args):
                         "stays on the device after the first call of a context (uploaded once per graph)",
                 "wall_ms_per_call": [round(t["wall_ms"], 2) for t in e2e_timings]},
             "gpu_launches": int(launches),
+            "device_memory_gb": {"used": used_b.value / 1e9, "total": total_b.value / 1e9,
+                                 "mask_rows_per_rank": ((k // 2 + world - 1) // world) * max(sg.words, 1) * 8 / 1e9},
             "roofline": roof,
             "clocks": clk,
         }
@@ -440,8 +444,12 @@ def run_batch(args):
         if dist is not None:
             dist.barrier()
 
+    workers = max(1, args.workers)
+    ctx.set_workers(workers)
     ctx.explain_nodes(g, m, mine, opts)  # warm-up pass over the batch (buffers grow to the largest target)
     times, players = [], 0
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.steps):
         barrier()
         t0 = time.perf_counter()
@@ -449,6 +457,7 @@ def run_batch(args):
         barrier()
         times.append(time.perf_counter() - t0)
         players = sum(len(e.phi) for e in ex)
+    clk = clocks.stop()
     if rank == 0:
         print("c5 step seconds", [round(x, 3) for x in times], file=sys.stderr, flush=True)
     dt = float(np.median(times))
@@ -466,8 +475,9 @@ def run_batch(args):
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {len(targets)} targets (degree 4-12), "
                                    f"{len(cfg.hidden) + 1}-layer GCN, d0={cfg.feature_dim}, {k} coalitions each",
-                       "parallelism": f"node-parallel replicas x{world}", "targets_rank0": len(mine),
-                       "players_rank0_total": int(players)},
+                       "parallelism": f"node-parallel replicas x{world}, {workers} concurrent targets per GPU",
+                       "targets_rank0": len(mine), "players_rank0_total": int(players)},
+            "clocks": clk,
             "coalitions_per_s": len(targets) * k / dt, "s_per_node": dt / max(len(targets), 1) * world,
         }), flush=True)
     return 0
@@ -484,6 +494,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the explain_node e2e leg (profiling runs)")
     ap.add_argument("--samples", type=int, default=0, help="override k (profiling runs only)")
     ap.add_argument("--targets", type=int, default=0, help="C5: number of target nodes (default 1024)")
+    ap.add_argument("--workers", type=int, default=4, help="C5: concurrent targets per GPU (sf_ctx_set_workers)")
     ap.add_argument("--explain-only", action="store_true", help="profiling: run explain_node twice and exit")
     args = ap.parse_args()
     if args.warmup < 3:

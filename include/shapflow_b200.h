@@ -334,6 +334,20 @@ int sf_explain_nodes(sf_ctx* ctx, const sf_graph* g, const sf_model* m,
                      const uint32_t* nodes, uint64_t count,
                      const sf_explain_options* opts, sf_explanation* out);
 
+/* Device memory in use on the context's GPU (all allocations of the
+ * process, cudaMemGetInfo) and its capacity, in bytes. */
+int sf_ctx_device_memory(const sf_ctx* ctx, uint64_t* used, uint64_t* total);
+
+/* Concurrent targets for sf_explain_nodes on a one-worker context (no
+ * reference counterpart; the reference loops over nodes, explain.cpp:145-181):
+ * `workers` contexts on this device (own stream and buffers, created on
+ * first use) each take the next target from a shared counter, so one
+ * target's CGLS overlaps another's sampling and inference. Results per
+ * target are unchanged; errors report the lowest failing node. 1..16,
+ * default 1. Ignored for multi-rank contexts (every rank must run the same
+ * collective sequence). */
+int sf_ctx_set_workers(sf_ctx* ctx, int workers);
+
 /* explain.hpp:59-64 select_nodes: "degree-range:[lo,hi]:count" (first
  * `count` ids in ascending order with degree in [lo, hi]) or a comma
  * separated id list. Writes up to `cap` ids, *count = number selected. */

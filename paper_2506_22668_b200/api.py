@@ -465,6 +465,13 @@ class Context:
 
     FUSED_KERNELS = {"auto": 0, "simt": 1, "tc": 2, "tc16": 3}
 
+    def set_workers(self, workers):
+        """Concurrent targets for explain_nodes on this device (sf_ctx_set_workers)."""
+        _chk(lib.sf_ctx_set_workers(self.h, C.c_int(workers)))
+
+    def set_comm_timeout(self, timeout_ms):
+        _chk(lib.sf_ctx_set_comm_timeout(self.h, C.c_int(timeout_ms)))
+
     def keep_stages(self, enable=True):
         _chk(lib.sf_ctx_keep_stages(self.h, C.c_int(int(enable))))
 

@@ -921,7 +921,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2 + (pairs + 255) / 256 + 1;
   // nibble forward: the player axis in parts so the grid covers the SMs
   const uint32_t nb_parts_max = uint32_t((n + kNbChunk - 1) / kNbChunk);
-  const uint64_t bytes = 2 * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
+  const uint64_t bytes = (in.kept_only ? 1 : 2) * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
                          (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
                          uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 32 * 8 + 16 * 256;
@@ -935,7 +935,8 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   ctx.solver_work.reserve(bytes + repro_bytes);
   Scratch sc{ctx.solver_work.p, 0};
   uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
-  uint64_t* mto = sc.take<uint64_t>(ptiles * Wp);  // odd rows (non-complement pairs only)
+  // odd rows (non-complement pairs only; kept-only rows are all complement pairs)
+  uint64_t* mto = in.kept_only ? nullptr : sc.take<uint64_t>(ptiles * Wp);
   uint8_t* is_comp = in.dev_is_comp ? const_cast<uint8_t*>(in.dev_is_comp) : sc.take<uint8_t>(pairs);
   double* r = sc.take<double>(rows);
   double* v = sc.take<double>(rows);
@@ -1175,8 +1176,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     SF_LAUNCHED(ctx);
   }
   if (pairs_n) {
-    SF_CUDA(cudaFuncSetAttribute(nib_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kNbChunk / 4 * 16 * 8)));
+    set_max_dynamic_smem(nib_forward_kernel, int(kNbChunk / 4 * 16 * 8));
   }
   const uint32_t* row_start = d_bounds;
   const uint32_t* split_start = d_bounds + bounds.size();
@@ -1292,7 +1292,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       SF_LAUNCHED(ctx);
     }
   };
-  SF_CUDA(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdChunk * 8)));
+  set_max_dynamic_smem(forward_kernel, int(kFwdChunk * 8));
   // v = sqrt(W) M u; delta = ||v||^2 all-reduced + v_c^2 (solver.cpp:252-287)
   auto forward_product = [&](double& delta, double& v_c) {
     if (repro) {

@@ -1243,8 +1243,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       const uint32_t cpb = 8;  // coalitions per CTA
       const size_t smem = size_t(cpb) * (Din + C) * 4;
       if (smem > 48 * 1024)
-        SF_CUDA(cudaFuncSetAttribute(last_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(std::min<size_t>(smem, 227 * 1024))));
+        set_max_dynamic_smem(last_kernel, 227 * 1024);
       dim3 grid(unsigned(nt), kTile / cpb);
       last_kernel<<<grid, 256, smem, ctx.stream>>>(
           maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, shared_x ? 1 : 0,

@@ -12,6 +12,10 @@
 #include <fstream>
 #include <numeric>
 #include <sstream>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <thread>
 
 #include "../../include/shapflow_b200.h"
 #include "sf_internal.hpp"
@@ -815,6 +819,10 @@ using namespace sfb;
 
 struct sf_ctx {
   Ctx c;
+  // explain_nodes on one device: extra contexts (own stream and buffers)
+  // run other targets concurrently from worker threads (sf_ctx_set_workers)
+  int workers = 1;
+  std::vector<std::unique_ptr<sf_ctx>> helpers;
 };
 struct sf_graph {
   Graph g;
@@ -1096,6 +1104,25 @@ int sf_ctx_allreduce_host(sf_ctx* ctx, double* buf, uint64_t count) {
     comm_allreduce_sum(ctx->c, d.p, count);
     SF_CUDA(cudaMemcpyAsync(buf, d.p, count * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
     comm_sync(ctx->c);
+  });
+}
+
+int sf_ctx_device_memory(const sf_ctx* ctx, uint64_t* used, uint64_t* total) {
+  return guard([&] {
+    need(ctx, "context");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    size_t f = 0, t = 0;
+    SF_CUDA(cudaMemGetInfo(&f, &t));
+    if (used) *used = t - f;
+    if (total) *total = t;
+  });
+}
+
+int sf_ctx_set_workers(sf_ctx* ctx, int workers) {
+  return guard([&] {
+    need(ctx, "context");
+    if (workers < 1 || workers > 16) throw DataError("workers must be in [1, 16]");
+    ctx->workers = workers;
   });
 }
 
@@ -1673,6 +1700,63 @@ int sf_explain_nodes(sf_ctx* ctx, const sf_graph* g, const sf_model* m, const ui
     else
       sf_explain_options_default(&o);
     SF_CUDA(cudaSetDevice(ctx->c.device));
+    const int workers = ctx->c.world == 1 ? int(std::min<uint64_t>(uint64_t(ctx->workers), count)) : 1;
+    if (workers > 1) {
+      // Targets are independent on one worker: pull them from a shared
+      // counter on `workers` contexts of this device (one host thread each),
+      // so one target's solve overlaps another's sampling and inference.
+      // Each target's result is what explain_node gives on its own.
+      while (int(ctx->helpers.size()) < workers - 1) {
+        sf_ctx* h = nullptr;
+        const int rc = sf_ctx_create(ctx->c.device, &h);
+        if (rc != SF_OK) throw CudaError(std::string("helper context: ") + sf_last_error());
+        h->c.fused_kind = ctx->c.fused_kind;
+        ctx->helpers.emplace_back(h);
+      }
+      std::atomic<uint64_t> next{0};
+      std::mutex mu;
+      uint64_t bad = count;
+      std::exception_ptr err;
+      std::vector<char> filled(count, 0);
+      auto run = [&](Ctx& c) {
+        cudaSetDevice(c.device);
+        for (;;) {
+          const uint64_t i = next++;
+          if (i >= count) return;
+          {
+            std::lock_guard<std::mutex> g(mu);
+            if (bad < i) return;  // an earlier target failed: stop
+          }
+          try {
+            explain_node(c, g->g, m->m, nodes[i], o, &out[i]);
+            filled[i] = 1;
+          } catch (...) {
+            std::lock_guard<std::mutex> g(mu);
+            if (i < bad) {
+              bad = i;
+              err = std::current_exception();
+            }
+          }
+        }
+      };
+      std::vector<std::thread> pool;
+      for (int w = 1; w < workers; ++w) pool.emplace_back(run, std::ref(ctx->helpers[w - 1]->c));
+      run(ctx->c);
+      for (auto& t : pool) t.join();
+      if (err) {
+        for (uint64_t i = 0; i < count; ++i)
+          if (filled[i]) sf_explanation_free(&out[i]);
+        const uint32_t node = nodes[bad];
+        try {
+          std::rethrow_exception(err);
+        } catch (const DataError& e) {  // explain.cpp:171-175
+          throw DataError("node " + std::to_string(node) + ": " + e.what());
+        } catch (const NumericalError& e) {
+          throw NumericalError("node " + std::to_string(node) + ": " + e.what());
+        }
+      }
+      return;
+    }
     uint64_t done = 0;
     try {
       for (; done < count; ++done) {

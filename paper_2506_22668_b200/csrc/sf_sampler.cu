@@ -406,8 +406,9 @@ void launch_generate_masks(Ctx& ctx, const SizePlan& plan, uint64_t seed,
     const uint64_t want = (pairs + kSamplerWarps - 1) / kSamplerWarps;
     if (smem <= 200 * 1024) {
       auto k = floyd_kernel<true>;
-      SF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
+      // a fixed ceiling, set once per device: launches on several streams
+      // (explain_nodes workers) must not race on a per-call value
+      set_max_dynamic_smem(k, 200 * 1024);
       int per_sm = 1;
       SF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSamplerWarps * 32, smem));
       const uint64_t grid = std::min<uint64_t>(want, uint64_t(sms) * std::max(per_sm, 1) * 4);
@@ -436,7 +437,7 @@ void launch_floyd_jobs(Ctx& ctx, uint32_t n, uint64_t seed,
   const size_t smem = size_t(kSamplerWarps) * W * 8;
   if (smem <= 200 * 1024) {  // the set in shared memory (one row per warp)
     auto k = floyd_jobs_kernel<true>;
-    SF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    set_max_dynamic_smem(k, 200 * 1024);
     k<<<grid, kSamplerWarps * 32, smem, ctx.stream>>>(n, W, seed, dev_streams, dev_sizes, dev_invert, jobs,
                                                       dev_rows);
   } else {

@@ -143,3 +143,27 @@ def test_fused_solver_mode_matches_reference_protocol(ctx, port, n):
     st = res[1][1]
     assert st["vector_allreduce"] == e1.iterations + 1
     assert st["scalar_allreduce"] == 0
+
+
+def test_explain_nodes_workers_match_sequential(ctx):
+    """sf_ctx_set_workers: targets spread over several contexts of the device
+    give bitwise the explanations of the sequential loop (explain.cpp:145-181),
+    in node order; an error names the lowest failing node."""
+    d = W.build("C5")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+    nodes = g.select_nodes("degree-range:[4,12]:24")
+    opts = ExplainOptions(samples=20_000, seed=5, baseline_trials=2)
+    seq = ctx.explain_nodes(g, m, nodes, opts)
+    ctx.set_workers(3)
+    try:
+        par = ctx.explain_nodes(g, m, nodes, opts)
+        assert [e.node for e in par] == [e.node for e in seq]
+        for a, b in zip(seq, par):
+            assert np.array_equal(a.phi, b.phi) and a.top == b.top
+            assert np.array_equal(a.fidelity["plus"], b.fidelity["plus"])
+        with pytest.raises(sf.DataError, match=f"^node {cfg.nodes + 5}: "):
+            ctx.explain_nodes(g, m, list(nodes[:5]) + [cfg.nodes + 5, cfg.nodes + 9], opts)
+    finally:
+        ctx.set_workers(1)

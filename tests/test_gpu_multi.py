@@ -224,3 +224,53 @@ def test_two_gpu_shard_predictions_match_single(tmp_path, ctx):
         bad = np.nonzero(rp != pred[rows])[0]
         assert bad.size == 0, f"rank {r}: {bad.size} predictions differ, first rows {bad[:8]}, " \
                               f"max rel {np.max(np.abs(rp - pred[rows]) / np.abs(pred[rows])):.3g}"
+
+
+TIMEOUT_WORKER = r"""
+import json, os, sys, time
+sys.path.insert(0, os.environ["SF_ROOT"])
+import torch.distributed as dist
+import paper_2506_22668_b200 as sf
+rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+ctx = sf.Context(local)
+obj = [sf.Context.nccl_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(obj, src=0)
+ctx.join(obj[0], rank, world)
+ctx.barrier()  # both ranks: a normal collective first
+dist.barrier()
+out = {"rank": rank}
+if rank == 0:
+    ctx.set_comm_timeout(3000)
+    t0 = time.time()
+    try:
+        ctx.barrier()  # rank 1 never joins this one
+        out["error"] = None
+    except sf.ProtocolError as e:
+        out["error"] = str(e)
+    out["waited_s"] = time.time() - t0
+else:
+    time.sleep(6)
+with open(os.path.join(os.environ["SF_OUT"], f"timeout{rank}.json"), "w") as f:
+    json.dump(out, f)
+dist.barrier()
+os._exit(0)  # the aborted communicator is not torn down again
+"""
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs (gpurun --gpus 2)")
+def test_collective_timeout_raises_protocol_error(tmp_path):
+    """A rank that never enters a collective: the waiting rank aborts its
+    NCCL communicator after the configured timeout and raises ProtocolError
+    (the reference Communicator's kDefaultCommTimeout behaviour,
+    comm.hpp:54) instead of hanging."""
+    world = 2
+    script = tmp_path / "timeout_worker.py"
+    script.write_text(TIMEOUT_WORKER)
+    env = dict(os.environ, SF_ROOT=ROOT, SF_OUT=str(tmp_path))
+    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                    "--master-addr", "127.0.0.1", "--master-port", "29537", str(script)],
+                   check=True, env=env, timeout=300)
+    r0 = json.load(open(tmp_path / "timeout0.json"))
+    assert r0["error"] and "timed out" in r0["error"]
+    assert 2.5 <= r0["waited_s"] <= 30
