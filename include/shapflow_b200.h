@@ -187,6 +187,12 @@ int sf_model_layer(const sf_model* m, int l, float* weight, float* bias);
  * discovery order, players sorted, symmetric local CSR with edge_player) */
 int sf_extract(const sf_graph* g, uint32_t target, int hops,
                sf_subgraph** out);
+/* graph.hpp:69-70 extract_computational_graph on the device (level-
+ * synchronous BFS with the reference's discovery order, segmented sorts for
+ * the local CSR): byte-identical to sf_extract; explain_node uses it for
+ * graphs with >= 2^20 CSR entries (env SF_EXTRACT=host|device|auto). */
+int sf_extract_device(sf_ctx* ctx, const sf_graph* g, uint32_t target,
+                      int hops, sf_subgraph** out);
 int sf_subgraph_free(sf_subgraph* sg);
 /* A ComputationalGraph built by the caller (graph.hpp:36-53 layout: local
  * ids BFS order, players_uv 2n local endpoints u < v sorted, symmetric CSR

@@ -197,6 +197,12 @@ class Graph:
         _chk(lib.sf_extract(self.h, C.c_uint32(target), C.c_int(hops), C.byref(h)))
         return Subgraph(h)
 
+    def extract_device(self, ctx, target, hops):
+        """extract_computational_graph on the GPU of `ctx` (sf_extract_device)."""
+        h = C.c_void_p()
+        _chk(lib.sf_extract_device(ctx.h, self.h, C.c_uint32(target), C.c_int(hops), C.byref(h)))
+        return Subgraph(h)
+
     def __del__(self):
         try:
             if self.h:

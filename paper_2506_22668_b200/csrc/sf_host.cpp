@@ -250,6 +250,10 @@ static void save_sfg(const Graph& g, const std::string& path) {
   if (!out) throw DataError("write failed: " + path);
 }
 
+// graphs with at least this many CSR entries are extracted on the device
+// (SF_EXTRACT=host|device|auto)
+constexpr uint64_t kDeviceExtractNnz = 1u << 20;
+
 static Subgraph extract(const Graph& g, uint32_t target, int hops, bool with_features = true) {
   // graph.cpp:195-261: BFS ball (discovery order = local ids, target 0),
   // induced undirected edges sorted lexicographically, symmetric local CSR
@@ -618,7 +622,11 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     throw DataError("model expects " + std::to_string(m.layers.front().in) +
                     " input features but the graph has " + std::to_string(g.feature_dim));
   DebugTimer("explain").lap("start");
-  const Subgraph sg = extract(g, node, m.depth(), false);
+  // large graphs: the BFS ball and local CSR on the device (byte-identical)
+  static const char* ex_env = std::getenv("SF_EXTRACT");
+  static const std::string ex_mode = ex_env ? ex_env : "auto";
+  const bool on_device = ex_mode == "device" || (ex_mode == "auto" && g.col.size() >= kDeviceExtractNnz);
+  const Subgraph sg = on_device ? extract_device(ctx, g, node, int(m.depth())) : extract(g, node, m.depth(), false);
   out->extract_ms = ms_since(t_start);
   DebugTimer("explain").lap("extracted");
   const uint64_t n_raw = sg.num_players();
@@ -1409,6 +1417,23 @@ int sf_subgraph_create(uint32_t target_global, uint32_t V, uint64_t n, const uin
     for (uint64_t i = 0; i < nnz; ++i)
       if (sg.col[i] >= V || sg.edge_player[i] >= n) throw DataError("subgraph CSR entry out of range");
     sg.features.assign(features, features + uint64_t(V) * dim);
+    *out = new sf_subgraph{std::move(sg)};
+  });
+}
+
+int sf_extract_device(sf_ctx* ctx, const sf_graph* g, uint32_t target, int hops, sf_subgraph** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(g, "graph");
+    need(out, "output");
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    Subgraph sg = extract_device(ctx->c, g->g, target, hops);
+    sg.source = nullptr;  // a standalone subgraph carries its feature slice
+    const uint64_t d = g->g.feature_dim;
+    sg.features.resize(uint64_t(sg.num_nodes()) * d);
+    for (uint32_t lu = 0; lu < sg.num_nodes(); ++lu)
+      std::memcpy(sg.features.data() + uint64_t(lu) * d, g->g.features.data() + uint64_t(sg.local_to_global[lu]) * d,
+                  d * 4);
     *out = new sf_subgraph{std::move(sg)};
   });
 }

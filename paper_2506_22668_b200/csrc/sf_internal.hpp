@@ -226,6 +226,15 @@ struct HostComm {
   int (*barrier)(void* user) = nullptr;
 };
 
+// device extraction state (sf_extract.cu): the graph CSR once per graph and
+// scratch reused across targets
+struct ExtractState {
+  uint64_t graph_id = 0;
+  DevBuf<uint64_t> rp, off, deg, lrp, cnt, ufirst, pstart, first;
+  DevBuf<uint32_t> col, local_of, l2g, flag, pos, lcol_raw, lcol, ep, players;
+  DevBuf<unsigned char> tmp;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -275,6 +284,7 @@ struct Ctx {
   DevBuf<uint64_t> fid_streams, fid_rows;  // fidelity random-baseline jobs
   DevBuf<uint32_t> fid_sizes;
   DevBuf<uint8_t> fid_inv;
+  ExtractState extract;             // device extraction (large balls)
   DevBuf<uint64_t> gram_maskt;      // direct solve: tile-transposed rows
   DevBuf<unsigned char> gram_work;  // direct solve: plan, run weights, targets
   DevBuf<double> gram_g;            // direct solve: Gram partials, factor, copy, rhs
@@ -393,6 +403,9 @@ struct CglsInput {
 };
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
+// extract_computational_graph (graph.cpp:195-261) on the device, byte-
+// identical to the host version; features are not copied (sg.source = &g)
+Subgraph extract_device(Ctx& ctx, const Graph& g, uint32_t target, int hops);
 // Runs of rows with one weight (explain_node: a size class; solve_direct:
 // equal caller weights), rows [begin, end)
 struct GramRun {

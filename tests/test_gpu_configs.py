@@ -129,3 +129,37 @@ def test_c4_rank_block_and_predictions(ctx, ref, c4):
         outs = list(ex.map(lambda r: ref.predict_batched(c4["rm"], c4["rg"], c4["d"]["target"], bits[r:r + 1], 11,
                                                          sg=c4["sgr"]), pick))
     assert rel_err(got[pick], np.concatenate(outs)) <= RTOL
+
+
+def _sub_arrays(sg):
+    a = sg.arrays()
+    return {k: np.asarray(v) for k, v in a.items()}
+
+
+@pytest.mark.parametrize("name,hops", [("C1", 2), ("C2", 3), ("C5", 2), ("C2", 1), ("C2", 0)])
+def test_device_extraction_byte_identical(ctx, name, hops):
+    """extract_computational_graph on the device (graph.cpp:195-261):
+    local ids (BFS discovery order), players (lexicographic), local CSR and
+    edge_player byte-identical to the host extraction (itself byte-identical
+    to the reference, tests/test_host.py), for several targets."""
+    d = W.build(name)
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    rp, _ = g.csr()
+    deg = np.diff(rp)
+    targets = [int(d["target"] or 0), int(np.argmax(deg)), int(np.argmin(deg)), 3]
+    for t in targets:
+        a = _sub_arrays(g.extract(t, hops))
+        b = _sub_arrays(g.extract_device(ctx, t, hops))
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (name, t, k)
+
+
+@pytest.mark.slow
+def test_device_extraction_c4(ctx, c4):
+    """C4's 1M-player ball (the graph explain_node extracts on the device)."""
+    g, t = c4["g"], c4["d"]["target"]
+    a = _sub_arrays(c4["sg"])
+    b = _sub_arrays(g.extract_device(ctx, t, c4["cfg"].hops))
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
