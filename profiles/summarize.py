@@ -28,6 +28,16 @@ KEYS = [
     ("dram__bytes_write.sum", "DRAM write (MB)"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("lts__t_bytes.sum", "L2 traffic (MB)"),
+    ("lts__t_sectors.sum", "L2 sectors (x32 B)"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active % (elapsed)"),
+    ("sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+     "tcgen05 tf32 MMA ops % of peak"),
+    ("sm__ops_path_tensor_op_utchmma_src_fp16_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+     "tcgen05 f16 MMA ops % of peak"),
+    ("sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active", "TMEM pipe inst % (active)"),
+    ("sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active", "legacy HMMA pipe % (active)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem LSU wavefronts % of peak"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
@@ -61,10 +71,15 @@ def report(path, regex=None):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     h, units = r[0], r[1]
+    seen = set()
     for v in r[2:]:
         name = v[h.index("Kernel Name")]
         if regex and not re.search(regex, name):
             continue
+        short = re.sub(r"[(].*", "", name)
+        if short in seen:  # one launch per kernel
+            continue
+        seen.add(short)
         print(f"### `{re.sub(r'[(].*', '', name)}`\n")
         print("| metric | value |")
         print("|---|---:|")
@@ -83,6 +98,17 @@ def report(path, regex=None):
             except ValueError:
                 pass
             print(f"| {label} | {x} |")
+        try:  # achieved DRAM bandwidth of the launch (cold-cache replay)
+            def mb(key):
+                f = float(v[h.index(key)].replace(",", ""))
+                return f * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(units[h.index(key)], 1.0)
+            dur = float(v[h.index("gpu__time_duration.sum")].replace(",", "")) * {
+                "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(
+                units[h.index("gpu__time_duration.sum")], 1e-9)
+            print(f"| DRAM GB/s achieved (read+write / duration) | "
+                  f"{(mb('dram__bytes_read.sum') + mb('dram__bytes_write.sum')) * 1e6 / dur / 1e9:.0f} |")
+        except (ValueError, KeyError):
+            pass
         st = [(n, v[i]) for i, n in enumerate(h)
               if n.startswith("smsp__average_warps_issue_stalled") and n.endswith("per_issue_active.ratio")]
         st = sorted(st, key=lambda a: -float(a[1] or 0))[:6]
