@@ -55,7 +55,9 @@ int sf_ctx_join_nccl(sf_ctx* ctx, const void* unique_id_128, int rank,
  * Communicator behind the ABI: thread or socket workers, comm.hpp:28-52).
  * all_reduce sums `count` doubles in place across ranks, barrier waits for
  * every rank; both return 0 on success. The library stages device buffers
- * through pinned host memory for each call. Replaces any NCCL communicator. */
+ * through pinned host memory for each call. Replaces any NCCL communicator.
+ * With world == 1 the hooks are still called (buf == NULL for all_reduce:
+ * the sum is the identity) so the caller's collective accounting matches. */
 int sf_ctx_set_host_comm(sf_ctx* ctx, int rank, int world, void* user,
                          int (*all_reduce)(void* user, double* buf,
                                            uint64_t count),

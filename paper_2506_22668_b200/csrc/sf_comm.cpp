@@ -149,6 +149,13 @@ void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count) {
   else
     ++ctx.stats.vector_allreduce;
   ctx.stats.doubles_reduced += count;
+  if (ctx.world == 1 && ctx.host_comm.all_reduce) {
+    // one worker: the sum is the identity; the caller's Communicator still
+    // sees (and counts) the collective, like the reference's LocalComm
+    if (ctx.host_comm.all_reduce(ctx.host_comm.user, nullptr, count) != 0)
+      throw ProtocolError("host communicator all_reduce_sum failed");
+    return;
+  }
   if (ctx.world == 1 || count == 0) return;
   if (ctx.host_comm.all_reduce) {
     ctx.comm_stage.reserve(count);
@@ -171,7 +178,7 @@ void comm_allreduce_sum(Ctx& ctx, double* dev_buf, size_t count) {
 
 void comm_barrier(Ctx& ctx) {
   ++ctx.stats.barriers;
-  if (ctx.world > 1 && ctx.host_comm.barrier) {
+  if (ctx.host_comm.barrier) {
     SF_CUDA(cudaStreamSynchronize(ctx.stream));
     if (ctx.host_comm.barrier(ctx.host_comm.user) != 0) throw ProtocolError("host communicator barrier failed");
     return;

@@ -56,4 +56,22 @@ __device__ __forceinline__ float inv_sqrt_deg(uint32_t deg) {
   return __fdiv_rn(1.0f, __fsqrt_rn(static_cast<float>(deg)));
 }
 
+// float softmax of one row in place (max subtraction, gcn.cpp:143-152), one warp
+__device__ __forceinline__ void softmax_row_warp(float* zi, uint32_t C, int lane) {
+  float mx = -INFINITY;
+  for (uint32_t c = lane; c < C; c += 32) mx = fmaxf(mx, zi[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+  for (uint32_t c = lane; c < C; c += 32) {
+    const float e = expf(zi[c] - mx);
+    zi[c] = e;
+    sum += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  for (uint32_t c = lane; c < C; c += 32) zi[c] = zi[c] / sum;
+  __syncwarp();
+}
+
 }  // namespace sfb

@@ -413,22 +413,6 @@ __device__ __forceinline__ void softmax_row(float* zi, uint32_t C) {
 // The same float softmax with the warp's lanes over the classes: max and
 // sum by butterfly reductions (sum order differs from the sequential
 // reference loop by float rounding only), exp and divide per lane.
-__device__ __forceinline__ void softmax_row_warp(float* zi, uint32_t C, int lane) {
-  float mx = -INFINITY;
-  for (uint32_t c = lane; c < C; c += 32) mx = fmaxf(mx, zi[c]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.f;
-  for (uint32_t c = lane; c < C; c += 32) {
-    const float e = expf(zi[c] - mx);
-    zi[c] = e;
-    sum += e;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  for (uint32_t c = lane; c < C; c += 32) zi[c] = zi[c] / sum;
-  __syncwarp();
-}
 
 // A[t][u][i][:] = isd_i(u) * sum over the items of u of Apart[t][item][i][:]
 // (fixed item order, deterministic), one float4 per thread.
@@ -1054,6 +1038,13 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   if (e.tc) build_tc_plan(ctx, e, sg);
   if (e.tc16 && !e.tc) e.tc16 = false;  // the plan may have rejected the tensor-core path
   if (e.tc16) prepare_tc16(ctx, e);
+  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: the mma.sync tail)
+  static const bool use_tail_tc = [] {
+    const char* v = std::getenv("SF_TAIL_TC");
+    return v == nullptr || std::strcmp(v, "0") != 0;
+  }();
+  e.tail_tc = use_tail_tc && tail_tc_supported(e);
+  if (e.tail_tc) build_tail_tc(ctx, e);
   dt.lap("tc plan");
   e.sg_id = sg.id;
   e.model_id = m.id;
@@ -1169,6 +1160,10 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       if (!ok) throw std::logic_error("fused width not instantiated");
       if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
+      if (e.tail_tc) {  // tcgen05 tail (sf_tail_tc.cu)
+        launch_tail_tc(ctx, e, pbuf, maskt, Wp, isd, ntp, cls, row0, rows, dev_out, dev_allprobs);
+        continue;
+      }
       if (L <= 3) {  // fused tail: reduce + layer 1 + last layer + softmax in one kernel
         // coalitions per CTA: 16 when the tile fits (the weights are staged
         // once per CTA; 16 measured 49.1 vs 50.5 ms/step for 4 at C2); the

@@ -1093,7 +1093,9 @@ int sf_ctx_set_host_comm(sf_ctx* ctx, int rank, int world, void* user,
     need(ctx, "context");
     if (world < 1 || rank < 0 || rank >= world)
       throw DataError("invalid worker rank " + std::to_string(rank) + " of " + std::to_string(world));
-    if (world > 1 && (!all_reduce || !barrier)) throw DataError("host communicator needs all_reduce and barrier");
+    if ((all_reduce == nullptr) != (barrier == nullptr))
+      throw DataError("host communicator needs both all_reduce and barrier");
+    if (world > 1 && !all_reduce) throw DataError("host communicator needs all_reduce and barrier");
     comm_drop_nccl(ctx->c);
     ctx->c.rank = rank;
     ctx->c.world = world;

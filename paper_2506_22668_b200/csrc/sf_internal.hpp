@@ -191,6 +191,9 @@ struct Engine {
   DevBuf<float> p16_scale;  // [0] P0 scale (power of two), [1] its inverse
   DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items, tc_const;
   DevBuf<uint8_t> tc_kflags;
+  // tensor-core tail (sf_tail_tc.cu): 3-layer, hidden 128/128
+  bool tail_tc = false;
+  DevBuf<float> tail_w1img;  // W1 as a K-major tf32 hi | lo image
 };
 
 // SF_TIMING=1: host-side stage timings to stderr (debug aid, off by default)
@@ -403,6 +406,12 @@ struct CglsInput {
 };
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
+// tensor-core tail (sf_tail_tc.cu)
+bool tail_tc_supported(const Engine& e);
+void build_tail_tc(Ctx& ctx, Engine& e);
+void launch_tail_tc(Ctx& ctx, const Engine& e, const float* apart, const uint64_t* maskt, uint64_t Wp,
+                    const float* isd, uint64_t ntp, uint32_t cls, uint64_t row0, uint64_t rows, float* out,
+                    float* allprobs);
 // extract_computational_graph (graph.cpp:195-261) on the device, byte-
 // identical to the host version; features are not copied (sg.source = &g)
 Subgraph extract_device(Ctx& ctx, const Graph& g, uint32_t target, int hops);

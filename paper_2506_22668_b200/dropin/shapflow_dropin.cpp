@@ -95,13 +95,16 @@ class Binding {
       return;
     }
     ctx_ = thread_context();
-    if (comm.world_size() > 1)
-      check(sf_ctx_set_host_comm(ctx_, comm.rank(), comm.world_size(), this, &Binding::all_reduce, &Binding::barrier));
-    else
-      check(sf_ctx_set_host_comm(ctx_, 0, 1, nullptr, nullptr, nullptr));
+    // every collective goes through `comm` (for one worker the sums are
+    // identities, but its CollectiveStats still count them)
+    check(sf_ctx_set_host_comm(ctx_, comm.rank(), comm.world_size(), this, &Binding::all_reduce, &Binding::barrier));
   }
   ~Binding() {
-    if (nccl_) nccl_->absorb_device_stats();
+    if (nccl_) {
+      nccl_->absorb_device_stats();
+    } else {  // no hooks outlive this call (they point at *this)
+      sf_ctx_set_host_comm(ctx_, 0, 1, nullptr, nullptr, nullptr);
+    }
   }
   sf_ctx* ctx() const { return ctx_; }
   // a failure inside the Communicator (e.g. a ProtocolError) is rethrown as is
@@ -118,6 +121,12 @@ class Binding {
   static int all_reduce(void* user, double* buf, std::uint64_t count) {
     auto* self = static_cast<Binding*>(user);
     try {
+      if (buf == nullptr) {  // one worker: count the call, the sum is the identity
+        thread_local std::vector<double> scratch;
+        scratch.assign(count, 0.0);
+        self->comm_.all_reduce_sum(std::span<double>(scratch.data(), count));
+        return 0;
+      }
       self->comm_.all_reduce_sum(std::span<double>(buf, count));
       return 0;
     } catch (...) {
