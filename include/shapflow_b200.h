@@ -34,6 +34,7 @@ typedef struct sf_ctx sf_ctx;           /* one rank = one GPU + stream + comm */
 typedef struct sf_graph sf_graph;       /* graph.hpp:16-31  Graph */
 typedef struct sf_model sf_model;       /* gcn.hpp:13-30    GcnModel */
 typedef struct sf_subgraph sf_subgraph; /* graph.hpp:36-53  ComputationalGraph */
+typedef struct sf_dmasks sf_dmasks;     /* sampler.hpp:55-78 MaskBlock, in HBM */
 
 const char* sf_last_error(void);
 const char* sf_version(void);
@@ -152,6 +153,36 @@ int sf_generate_masks(sf_ctx* ctx, uint32_t n, const uint32_t* sizes,
                       uint64_t cap_words, uint64_t* rows,
                       uint64_t* rows_of_size);
 
+/* Device-resident stages (the reference's explain.cpp:91-114 sequence
+ * generate_masks -> predict_batched -> assemble_problem -> solve_cgls without
+ * moving the mask block across PCIe). sf_masks_device samples this rank's
+ * pairs into HBM, one kept-set row per pair (the complement rows are derived
+ * by every consumer); sf_dmasks_download expands them into the reference's
+ * MaskBlock.bits layout (rows 2j, 2j+1) on the host. */
+int sf_masks_device(sf_ctx* ctx, uint32_t n, const uint32_t* sizes,
+                    const uint64_t* pairs, const uint64_t* first_pair,
+                    uint64_t nclasses, int exhaustive, uint64_t seed, int rank,
+                    int world, sf_dmasks** out);
+/* rows (2 per local pair), player count, global rows per size (n+1, may be NULL) */
+int sf_dmasks_info(const sf_dmasks* m, uint64_t* rows, uint32_t* num_players,
+                   uint64_t* rows_of_size);
+int sf_dmasks_download(sf_ctx* ctx, const sf_dmasks* m, uint64_t* out_host,
+                       uint64_t cap_words);
+int sf_dmasks_free(sf_dmasks* m);
+/* gcn.hpp:60-62 predict_batched over device masks: p[class] per row to the host */
+int sf_predict_dmasks(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg,
+                      const sf_dmasks* masks, uint32_t class_index,
+                      uint64_t batch_size, float* out);
+/* solver.hpp:46-49 assemble_problem + 94-95 solve_cgls over device masks:
+ * values[row] the model outputs (float, as predict_batched returns them),
+ * base / full the empty / full outputs; mode as sf_solve_cgls. Collective
+ * over the context's ranks. */
+int sf_solve_dmasks(sf_ctx* ctx, const sf_dmasks* masks, const float* values,
+                    double base, double full, double constraint_scale,
+                    double tol, uint64_t max_iter, int mode, double* phi,
+                    uint64_t* iterations, double* relative_residual,
+                    int* converged);
+
 /* ------------------------------------------------------------ graph + model */
 /* graph.hpp:57-60 build_graph: symmetrize, dedupe, drop self-loops.
  * edges_uv: num_edges (u, v) pairs; labels may be NULL (kNoLabel). */
@@ -244,6 +275,18 @@ int sf_solve_cgls(sf_ctx* ctx, uint32_t n, const uint64_t* bits,
                   double* relative_residual, int* converged,
                   double* trace, double* row_residual_trace,
                   uint64_t trace_cap);
+/* sf_solve_cgls for one rank's slice of a multi-rank system: the global
+ * pair count (WlsProblem::global_pair_count, solver.hpp:17-18) sizes the
+ * fixed-order tree identically on every rank (mode 2). sf_solve_cgls
+ * assumes the rows are the whole system. */
+int sf_solve_cgls_ex(sf_ctx* ctx, uint32_t n, const uint64_t* bits,
+                     uint64_t rows, uint64_t words, const double* weights,
+                     const double* targets, double constraint_target,
+                     double constraint_weight, double tol, uint64_t max_iter,
+                     int mode, uint64_t global_pair_count, double* phi,
+                     uint64_t* iterations, double* relative_residual,
+                     int* converged, double* trace, double* row_residual_trace,
+                     uint64_t trace_cap);
 /* solver.hpp:46-49 assemble_problem weights: per-row normalized weight
  * from the global per-size row counts (solver.cpp:125-138). */
 int sf_assemble_weights(uint32_t n, const uint64_t* bits, uint64_t rows,

@@ -417,6 +417,52 @@ class ExplainOptions:
                          sp, len(self.sparsities), int(self.fixed_order))
 
 
+class DeviceMasks:
+    """A device-resident MaskBlock (sf_dmasks): kept-set rows in HBM."""
+
+    def __init__(self, ctx, handle):
+        self.ctx, self.h = ctx, handle
+
+    def info(self):
+        rows, n = C.c_uint64(), C.c_uint32()
+        _chk(lib.sf_dmasks_info(self.h, C.byref(rows), C.byref(n), None))
+        ros = np.zeros(n.value + 1, np.uint64)
+        _chk(lib.sf_dmasks_info(self.h, C.byref(rows), C.byref(n), _p(ros)))
+        return rows.value, n.value, ros
+
+    def download(self):
+        rows, n, _ = self.info()
+        W = max(1, (n + 63) // 64)
+        out = np.zeros((rows, W), np.uint64)
+        _chk(lib.sf_dmasks_download(self.ctx.h, self.h, _p(out), _u64(out.size)))
+        return out
+
+    def predict(self, model, sg, class_index, batch_size=50):
+        rows, _, _ = self.info()
+        out = np.zeros(max(rows, 1), np.float32)
+        _chk(lib.sf_predict_dmasks(self.ctx.h, model.h, sg.h, self.h, C.c_uint32(class_index), _u64(batch_size),
+                                   _p(out)))
+        return out[:rows]
+
+    def solve(self, values, base, full, constraint_scale=1e6, tol=1e-6, max_iter=0, mode=0):
+        rows, n, _ = self.info()
+        v = np.ascontiguousarray(values, np.float32)
+        phi = np.zeros(max(n, 1), np.float64)
+        it, rel, conv = C.c_uint64(), C.c_double(), C.c_int()
+        _chk(lib.sf_solve_dmasks(self.ctx.h, self.h, _p(v), C.c_double(base), C.c_double(full),
+                                 C.c_double(constraint_scale), C.c_double(tol), _u64(max_iter), C.c_int(mode),
+                                 _p(phi), C.byref(it), C.byref(rel), C.byref(conv)))
+        return dict(phi=phi[:n], iterations=it.value, relative_residual=rel.value, converged=bool(conv.value))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.sf_dmasks_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Context:
     """One rank: a B200, its stream and (for world > 1) an NCCL communicator."""
 
@@ -519,6 +565,14 @@ class Context:
         return out, ros
 
     # ---- inference
+    def masks_device(self, plan, seed, rank=0, world=1):
+        """sampler.hpp:84-85 generate_masks into HBM (sf_masks_device)."""
+        h = C.c_void_p()
+        _chk(lib.sf_masks_device(self.h, C.c_uint32(plan["n"]), _p(plan["sizes"]), _p(plan["pairs"]),
+                                 _p(plan["first"]), _u64(len(plan["sizes"])), C.c_int(int(plan["exhaustive"])),
+                                 _u64(seed), C.c_int(rank), C.c_int(world), C.byref(h)))
+        return DeviceMasks(self, h)
+
     def predict_batched(self, model, sg, bits, class_index, batch_size=50):
         bits = np.ascontiguousarray(bits, np.uint64)
         if bits.ndim == 1:

@@ -758,6 +758,73 @@ __global__ void sq_parts_kernel(const double* __restrict__ r, uint64_t rows, con
   parts[2 * rows + i] = c;
 }
 
+// ---------------------------------------------------------------- fixed order, small systems
+// The reference's own order (PairwiseFolder, solver.cpp:31-61, 227-237,
+// 270-279): leaves are pushed in bit-reversed local pair order and folded
+// in a binary tree; with the Communicator folding ranks by halves this is
+// one tree over the global pairs, the same for every worker count. Used when
+// padded pairs x players is small (the leaves are dense n-vectors).
+__device__ __forceinline__ uint64_t bitrev_n(uint64_t x, int bits) {
+  return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
+}
+
+// thread per player: s_local[e] = folded leaves, leaf_j[e] = c_o + (c_e - c_o)
+// bit (complement pair, solver.cpp:209-217) or c_e bit_e + c_o bit_o
+__global__ void __launch_bounds__(128) tree_transpose_kernel(const uint64_t* __restrict__ mte,
+                                                             const uint64_t* __restrict__ mto, uint64_t Wp,
+                                                             uint32_t n, uint64_t pairs, const uint8_t* __restrict__ is_comp,
+                                                             const double* __restrict__ sw, const double* __restrict__ r,
+                                                             uint64_t padded, int log_local, double* __restrict__ out) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double slot[40];
+  double carry = 0.0;
+  for (uint64_t t = 0; t < padded; ++t) {
+    const uint64_t j = bitrev_n(t, log_local);
+    double leaf = 0.0;
+    if (j < pairs) {
+      const double ce = sw[2 * j] * r[2 * j], co = sw[2 * j + 1] * r[2 * j + 1];
+      const double be = double((mte[(j >> 6) * Wp + e] >> (j & 63)) & 1ull);
+      if (is_comp[j]) {
+        leaf = co + (ce - co) * be;
+      } else {
+        const double bo = double((mto[(j >> 6) * Wp + e] >> (j & 63)) & 1ull);
+        leaf = ce * be + co * bo;
+      }
+    }
+    carry = leaf;
+    int level = 0;
+    for (uint64_t c = t; c & 1; c >>= 1, ++level) carry = slot[level] + carry;
+    slot[level] = carry;
+  }
+  int top = 0;
+  while (!((padded >> top) & 1)) ++top;
+  out[e] = slot[top];
+}
+
+// x[0] = fold by halves of x[0, padded) (x[j] += x[j + h], h = padded/2 ... 1):
+// the same tree as pushing x in bit-reversed order through the folder
+__global__ void fold_level_kernel(double* __restrict__ x, uint64_t h) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (j < h) x[j] = x[j] + x[j + h];
+}
+__global__ void __launch_bounds__(1024) fold_small_kernel(double* __restrict__ x, uint64_t padded, double* out) {
+  __shared__ double sm[2048];
+  for (uint64_t j = threadIdx.x; j < padded; j += blockDim.x) sm[j] = x[j];
+  __syncthreads();
+  for (uint64_t h = padded / 2; h >= 1; h /= 2) {
+    for (uint64_t j = threadIdx.x; j < h; j += blockDim.x) sm[j] = sm[j] + sm[j + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+// leaves of the scalar sums: d_j = a[2j]^2 + a[2j+1]^2 for j < pairs, 0 up to padded
+__global__ void pair_sq_kernel(const double* __restrict__ a, uint64_t pairs, uint64_t padded, double* __restrict__ d) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (j >= padded) return;
+  d[j] = j < pairs ? a[2 * j] * a[2 * j] + a[2 * j + 1] * a[2 * j + 1] : 0.0;
+}
+
 __global__ void fill_kernel(double* __restrict__ x, double value, uint64_t count) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (i < count) x[i] = value;
@@ -925,14 +992,30 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
                          (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
                          uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 32 * 8 + 16 * 256;
-  const bool repro = in.fixed_order;
+  const bool repro_req = in.fixed_order;
+  // fixed order: the reference's folder tree when the dense leaves are small
+  // (and the cross-rank sum is the caller's fold-by-halves or a 2-rank sum),
+  // exact level sums otherwise
+  auto ceil2 = [](uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+  };
+  const uint64_t tree_global = ceil2(std::max<uint64_t>(in.global_pair_count, 64));
+  const uint64_t tree_local = ceil2(std::max<uint64_t>({tree_global / uint64_t(ctx.world), pairs, 1}));
+  int tree_log = 0;
+  while ((uint64_t(1) << tree_log) < tree_local) ++tree_log;
+  const bool tree = repro_req && tree_local * uint64_t(n) <= (uint64_t(1) << 27) &&
+                    (ctx.world <= 2 || ctx.host_comm.all_reduce != nullptr);
+  const bool repro = repro_req && !tree;
   if (repro && mode != 0) throw DataError("fixed-order summation runs the reference protocol (solver mode 0)");
   constexpr int kBins = 2201;  // frexp exponents -1100..1100
   const uint64_t repro_bytes =
       repro ? (3ull * n + 8 + 3 * rows * 2 + 3 * ptiles * 64 * 2 + 3 * std::max<uint64_t>(pairs, 1) + rows +
                (2ull * kBins + 8) + 64) * 8 + 16 * 256
             : 0;
-  ctx.solver_work.reserve(bytes + repro_bytes);
+  const uint64_t tree_bytes = tree ? (tree_local + 2) * 8 + 256 : 0;
+  ctx.solver_work.reserve(bytes + repro_bytes + tree_bytes);
   Scratch sc{ctx.solver_work.p, 0};
   uint64_t* mte = sc.take<uint64_t>(ptiles * Wp);  // even rows, 64 pairs per tile
   // odd rows (non-complement pairs only; kept-only rows are all complement pairs)
@@ -952,6 +1035,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* tv = sc.take<double>(n + 1);  // fused mode: [A^T v ; ||v||^2]
   double* u = sc.take<double>(n);
   double* phi = sc.take<double>(n);
+  double* tleaf = tree ? sc.take<double>(tree_local + 2) : nullptr;  // scalar tree leaves
   // fixed-order mode buffers
   double *lev = nullptr, *ul = nullptr, *vl = nullptr, *dparts = nullptr, *cel = nullptr, *col = nullptr,
          *kcl = nullptr, *ones = nullptr, *flags = nullptr, *grids = nullptr;
@@ -1022,7 +1106,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   // SF_CGLS_NIBBLE=0 keeps every tile on the set-bit loops.
   uint64_t pd = pairs;
   {
-    bool nibble = pairs > 0 && !any_noncomp;
+    bool nibble = pairs > 0 && !any_noncomp && !tree;
     if (const char* env = std::getenv("SF_CGLS_NIBBLE")) nibble = nibble && std::atoi(env) != 0;
     double density = 1.0 / 64;
     if (const char* env = std::getenv("SF_CGLS_NIB_DENSITY")) density = std::atof(env);
@@ -1040,7 +1124,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   }
   const uint64_t tiles_b = (pd + 63) / 64, pairs_n = pairs - pd;
   // the sparse pairs as kept-set lists (SF_CGLS_LISTS=0: set-bit loops)
-  bool lists = pd > 0 && pd < pairs + 1 && !any_noncomp;
+  bool lists = pd > 0 && pd < pairs + 1 && !any_noncomp && !tree;
   if (const char* env = std::getenv("SF_CGLS_LISTS")) lists = lists && std::atoi(env) != 0;
   const uint32_t lsegs = uint32_t(std::max<uint64_t>(1, (tiles_b + kListTiles - 1) / kListTiles));
   const uint64_t* row_off = nullptr;
@@ -1256,7 +1340,29 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     }
   };
   // s = M^T (sw r) all-reduced, then the pin row (solver.cpp:226-248)
+  // scalar fold over pair leaves d_j = x[2j]^2 + x[2j+1]^2 into *out
+  auto tree_scalar = [&](const double* x, double* out) {
+    pair_sq_kernel<<<blocks_for(tree_local), 256, 0, st>>>(x, pairs, tree_local, tleaf);
+    SF_LAUNCHED(ctx);
+    uint64_t h = tree_local;
+    while (h > 2048) {
+      h /= 2;
+      fold_level_kernel<<<blocks_for(h), 256, 0, st>>>(tleaf, h);
+      SF_LAUNCHED(ctx);
+    }
+    fold_small_kernel<<<1, 1024, 0, st>>>(tleaf, h, out);
+    SF_LAUNCHED(ctx);
+  };
   auto transpose_product = [&]() {
+    if (tree) {
+      tree_transpose_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(mte, mto, Wp, n, pairs, is_comp, in.dev_sw, r,
+                                                                       tree_local, tree_log, s);
+      SF_LAUNCHED(ctx);
+      comm_allreduce_sum(ctx, s, n);
+      add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw * r_c, n);
+      SF_LAUNCHED(ctx);
+      return;
+    }
     if (repro) {
       transpose_levels(r);
       comm_allreduce_sum(ctx, lev, 3ull * n + 3);
@@ -1295,6 +1401,17 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   set_max_dynamic_smem(forward_kernel, int(kFwdChunk * 8));
   // v = sqrt(W) M u; delta = ||v||^2 all-reduced + v_c^2 (solver.cpp:252-287)
   auto forward_product = [&](double& delta, double& v_c) {
+    if (tree) {
+      reduce(u, n, 0, 0.0, scal + 0);  // sum_u
+      if (rows) forward_v(u, in.dev_sw, scal + 0, v);
+      tree_scalar(v, scal + 1);
+      comm_allreduce_sum(ctx, scal + 1, 1);
+      fetch(0, 2);
+      delta = host[1];
+      v_c = scw * host[0];
+      delta += v_c * v_c;
+      return;
+    }
     if (repro) {
       // parts of u on a grid from max|u| (u is replicated: same grid on
       // every rank), exact per-level row dots, v = sw ((V0 + V1) + V2),
@@ -1481,7 +1598,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     return res;
   }
   DebugTimer di("cgls iteration");
-  if (!trace && !repro) {
+  if (!trace && !repro && !tree) {
     // One host round trip per iteration: delta, theta, r_c and beta stay on
     // the device; the host reads (delta, stop flag, gamma_next) once after
     // the transpose and applies the reference's stop rule and error
@@ -1553,7 +1670,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       SF_LAUNCHED(ctx);
     }
     r_c -= theta * v_c;
-    if (trace && repro) {
+    if (trace && tree) {
+      tree_scalar(r, scal + 5);
+      comm_allreduce_sum(ctx, scal + 5, 1);
+      fetch(5, 1);
+      res.row_residual_trace.push_back(std::sqrt(host[5] + r_c * r_c));
+    } else if (trace && repro) {
       sq_parts_kernel<<<blocks_for(std::max<uint64_t>(rows, 1)), 256, 0, st>>>(r, rows, grids + 24, dparts);
       SF_LAUNCHED(ctx);
       for (int k = 0; k < 3; ++k) reduce(dparts + k * rows, rows, 0, 0.0, grids + 48 + k);

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint2* __restrict__ seg, const uint32_t* __restrict__ item_ent,
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
                     uint32_t items, const uint64_t* __restrict__ const_words, float* __restrict__ Apart,
-                    unsigned long long* __restrict__ prof, int exp) {
+                    unsigned long long* __restrict__ prof) {
   using Cfg = TcCfg<D>;
   uint64_t pw[3] = {0, 0, 0};
   const long long t_begin = PROF ? clock64() : 0;
@@ -186,8 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       // trip counts are warp-uniform (J0 steps by whole warps), so every lane
       // takes part in the shuffles
-      if (!PROF || !(exp & 1))
-        for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
+      for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
           const int J = J0 + lane, k = min(J >> 5, 31), q = (J >> 4) & 1, ug = J & 15;
           const uint32_t x = __shfl_sync(kFull, rec.x, k);
           if (J < cnt * 2 * 16)
@@ -223,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // entries [16 (sw / 4), +16).
       {
         const int sw = warp - kEpiWarps, q = sw & 3, k0 = (sw >> 2) * 16;
-        if (k0 < cnt && !(PROF && (exp & 8))) {
+        if (k0 < cnt) {
           const int m = q * 32 + lane, tq = m >> 6, i = m & 63;
           uint32_t hv[16], lv[16];
 #pragma unroll
@@ -363,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TC_WAIT(0, &hfull[b], (sg >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < ((PROF && (exp & 16)) ? 0 : NCH); ++cc) {
+      for (int cc = 0; cc < NCH; ++cc) {
         const uint32_t hcol = tmem + lane_base + b * D + hb + cc * CW;
         const uint32_t acol = tmem + lane_base + acc_col + cc * CW;
         if constexpr (CW == 32) {
@@ -436,13 +435,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// SF_TC_EXP (PROF only, results invalid): bit 0 skips the isd-row gathers,
-// bit 1 the P-row gathers, bit 2 the B transposition, bit 3 the A stores to
-// TMEM, bit 4 the epilogue's TMEM loads/stores and math
-int exp_flags() {
-  static const int f = std::getenv("SF_TC_EXP") ? std::atoi(std::getenv("SF_TC_EXP")) : 0;
-  return f;
-}
 
 // B bank: for every chunk of every item, the K-major tf32 hi | lo B tile of
 // the chunk's P0 rows (entries past the chunk end are zero). One CTA per
@@ -485,8 +477,7 @@ void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t W
   fused_tc_kernel<D, PROF><<<grid, kThreads, smem, ctx.stream>>>(
       maskt, Wp, isd, e.V, e.tc_bbank.p, e.tc_item_chunk.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
       e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
-      e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof,
-      PROF ? exp_flags() : 0);
+      e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof);
   SF_LAUNCHED(ctx);
 }
 

@@ -841,6 +841,15 @@ struct sf_model {
 struct sf_subgraph {
   Subgraph s;
 };
+// device-resident MaskBlock (sampler.hpp:55-78): kept-set rows only
+struct sf_dmasks {
+  int device = 0;
+  SizePlan plan;
+  int rank = 0, world = 1;
+  uint64_t pairs = 0;  // local pairs
+  uint32_t W = 1;
+  DevBuf<uint64_t> rows;
+};
 
 namespace {
 thread_local std::string g_last_error;
@@ -1244,6 +1253,152 @@ int sf_generate_masks(sf_ctx* ctx, uint32_t n, const uint32_t* sizes, const uint
   });
 }
 
+int sf_masks_device(sf_ctx* ctx, uint32_t n, const uint32_t* sizes, const uint64_t* pairs,
+                    const uint64_t* first, uint64_t nclasses, int exhaustive, uint64_t seed, int rank,
+                    int world, sf_dmasks** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "output");
+    if (world < 1 || rank < 0 || rank >= world)
+      throw DataError("invalid worker rank " + std::to_string(rank) + " of " + std::to_string(world));
+    SF_CUDA(cudaSetDevice(ctx->c.device));
+    auto d = std::make_unique<sf_dmasks>();
+    d->device = ctx->c.device;
+    d->plan = plan_from_arrays(n, sizes, pairs, first, nclasses, exhaustive);
+    d->rank = rank;
+    d->world = world;
+    d->pairs = local_pair_count(d->plan.total_pairs(), rank, world);
+    d->W = std::max<uint32_t>(1, (n + 63) / 64);
+    d->rows.reserve(std::max<uint64_t>(d->pairs * d->W, 1));
+    launch_generate_masks(ctx->c, d->plan, seed, rank, world, d->rows.p, /*kept_only=*/true);
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = d.release();
+  });
+}
+
+int sf_dmasks_info(const sf_dmasks* m, uint64_t* rows, uint32_t* num_players, uint64_t* rows_of_size) {
+  return guard([&] {
+    need(m, "masks");
+    if (rows) *rows = 2 * m->pairs;
+    if (num_players) *num_players = m->plan.n;
+    if (rows_of_size) {
+      const auto c = global_rows_of_size(m->plan);
+      std::memcpy(rows_of_size, c.data(), c.size() * 8);
+    }
+  });
+}
+
+int sf_dmasks_download(sf_ctx* ctx, const sf_dmasks* m, uint64_t* out, uint64_t cap_words) {
+  return guard([&] {
+    need(ctx, "context");
+    need(m, "masks");
+    const uint64_t W = m->W, total = 2 * m->pairs * W;
+    if (total == 0) return;
+    need(out, "output");
+    if (cap_words < total) throw DataError("mask output buffer too small");
+    SF_CUDA(cudaSetDevice(m->device));
+    std::vector<uint64_t> kept(m->pairs * W);
+    SF_CUDA(cudaMemcpyAsync(kept.data(), m->rows.p, kept.size() * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    SF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    ctx->c.d2h_bytes += kept.size() * 8;
+    const uint32_t n = m->plan.n;
+    const uint64_t tail = (n % 64) ? ((uint64_t{1} << (n % 64)) - 1) : ~uint64_t{0};
+    for (uint64_t j = 0; j < m->pairs; ++j) {  // rows 2j (kept), 2j+1 (complement, sampler.cpp:205-207)
+      std::memcpy(out + 2 * j * W, kept.data() + j * W, W * 8);
+      for (uint64_t w = 0; w < W; ++w) out[(2 * j + 1) * W + w] = (w + 1 == W) ? (~kept[j * W + w] & tail) : ~kept[j * W + w];
+      if (n == 0) out[(2 * j + 1) * W] = 0;
+    }
+  });
+}
+
+int sf_dmasks_free(sf_dmasks* m) {
+  delete m;
+  return SF_OK;
+}
+
+int sf_predict_dmasks(sf_ctx* ctx, const sf_model* m, const sf_subgraph* sg, const sf_dmasks* masks,
+                      uint32_t class_index, uint64_t batch_size, float* out) {
+  return guard([&] {  // gcn.cpp:259-270 on device-resident rows
+    need(ctx, "context");
+    need(m, "model");
+    need(sg, "subgraph");
+    need(masks, "masks");
+    if (batch_size == 0) throw DataError("batch_size must be positive");
+    if (class_index >= m->m.layers.back().out) throw DataError("class index out of range");
+    if (masks->device != ctx->c.device) throw DataError("masks live on another device");
+    if (masks->plan.n != sg->s.num_players()) throw DataError("masks do not match the subgraph's player count");
+    const uint64_t rows = 2 * masks->pairs;
+    if (rows == 0) return;
+    need(out, "output");
+    Ctx& c = ctx->c;
+    SF_CUDA(cudaSetDevice(c.device));
+    engine_prepare(c, sg->s, m->m);
+    c.preds.reserve(rows);
+    engine_predict(c, masks->rows.p, rows, class_index, c.preds.p, nullptr, nullptr, /*kept_only=*/true);
+    SF_CUDA(cudaMemcpyAsync(out, c.preds.p, rows * 4, cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    c.d2h_bytes += rows * 4;
+  });
+}
+
+int sf_solve_dmasks(sf_ctx* ctx, const sf_dmasks* masks, const float* values, double base, double full,
+                    double constraint_scale, double tol, uint64_t max_iter, int mode, double* phi,
+                    uint64_t* iterations, double* rel, int* converged) {
+  return guard([&] {  // assemble_problem (solver.cpp:95-156) + solve_cgls (158-362) on device rows
+    need(ctx, "context");
+    need(masks, "masks");
+    const uint32_t n = masks->plan.n;
+    if (iterations) *iterations = 0;
+    if (rel) *rel = 0.0;
+    if (converged) *converged = 1;
+    if (n == 0) return;
+    need(phi, "output");
+    if (masks->rank != ctx->c.rank || masks->world != ctx->c.world)
+      throw DataError("system slice does not match the communicator layout");
+    if (mode < 0 || mode > 2) throw DataError("solver mode must be 0, 1 or 2");
+    const uint64_t rows = 2 * masks->pairs;
+    if (rows) need(values, "values");
+    Ctx& c = ctx->c;
+    SF_CUDA(cudaSetDevice(c.device));
+    const std::vector<double> wsize = weight_of_size(n, global_rows_of_size(masks->plan));
+    c.wsize_dev.upload(wsize.data(), wsize.size(), c.stream);
+    c.preds.reserve(std::max<uint64_t>(rows, 1));
+    if (rows) SF_CUDA(cudaMemcpyAsync(c.preds.p, values, rows * 4, cudaMemcpyHostToDevice, c.stream));
+    c.sw_dev.reserve(std::max<uint64_t>(rows, 1));
+    c.tgt_dev.reserve(std::max<uint64_t>(rows, 1));
+    c.pop_dev.reserve(std::max<uint64_t>(rows, 1));
+    c.comp_dev.reserve(std::max<uint64_t>(rows / 2, 1));
+    const int big = 0x7fffffff;
+    c.bad_dev.upload(&big, 1, c.stream);
+    c.h2d_bytes += wsize.size() * 8 + rows * 4 + 4;
+    launch_assemble_pairs(c, masks->rows.p, rows, masks->W, n, c.wsize_dev.p, c.preds.p, base, c.sw_dev.p, c.tgt_dev.p,
+                          c.bad_dev.p, c.pop_dev.p, c.comp_dev.p, /*kept_only=*/true);
+    int bad = big;
+    SF_CUDA(cudaMemcpyAsync(&bad, c.bad_dev.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    if (bad != big) throw DataError("coalition row " + std::to_string(bad) + " keeps all or no players");
+    CglsInput in;
+    in.n = n;
+    in.rows = rows;
+    in.W = masks->W;
+    in.dev_rows = masks->rows.p;
+    in.dev_sw = c.sw_dev.p;
+    in.dev_targets = c.tgt_dev.p;
+    in.constraint_target = full - base;
+    in.constraint_weight = constraint_scale;
+    in.global_pair_count = masks->plan.total_pairs();
+    in.dev_pop = c.pop_dev.p;
+    in.dev_is_comp = c.comp_dev.p;
+    in.kept_only = true;
+    in.fixed_order = mode == 2;
+    const CglsResult r = cgls_solve(c, in, tol, max_iter, mode == 1 ? 1 : 0, false);
+    std::memcpy(phi, r.phi.data(), uint64_t(n) * 8);
+    if (iterations) *iterations = r.iterations;
+    if (rel) *rel = r.relative_residual;
+    if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
 int sf_graph_build(uint32_t num_nodes, const uint64_t* edges, uint64_t num_edges,
                    const float* features, uint64_t dim, const uint32_t* labels, sf_graph** out) {
   return guard([&] {
@@ -1583,35 +1738,54 @@ static void solve_common(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t
   in.dev_targets = d_tgt.p;
 }
 
+static void solve_cgls_impl(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
+                            const double* weights, const double* targets, double ct, double cw, double tol,
+                            uint64_t max_iter, int mode, uint64_t global_pairs, double* phi, uint64_t* iterations,
+                            double* rel, int* converged, double* trace, double* row_trace, uint64_t trace_cap) {
+  // solver.cpp:158-362
+  if (n == 0) {
+    if (iterations) *iterations = 0;
+    if (converged) *converged = 1;
+    if (rel) *rel = 0.0;
+    return;
+  }
+  need(phi, "output");
+  DevBuf<double> d_sw, d_tgt;
+  CglsInput in;
+  solve_common(ctx, n, bits, rows, words, weights, targets, d_sw, d_tgt, in);
+  in.constraint_target = ct;
+  in.constraint_weight = cw;
+  in.global_pair_count = global_pairs;
+  if (mode < 0 || mode > 2) throw DataError("solver mode must be 0 (reference protocol), 1 (fused) or 2 (fixed order)");
+  in.fixed_order = mode == 2;
+  CglsResult r = cgls_solve(ctx->c, in, tol, max_iter, mode == 2 ? 0 : mode, trace || row_trace);
+  std::memcpy(phi, r.phi.data(), uint64_t(n) * 8);
+  if (iterations) *iterations = r.iterations;
+  if (rel) *rel = r.relative_residual;
+  if (converged) *converged = r.converged ? 1 : 0;
+  for (uint64_t i = 0; i < trace_cap; ++i) {
+    if (trace && i < r.trace.size()) trace[i] = r.trace[i];
+    if (row_trace && i < r.row_residual_trace.size()) row_trace[i] = r.row_residual_trace[i];
+  }
+}
+
 int sf_solve_cgls(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
                   const double* weights, const double* targets, double ct, double cw, double tol,
                   uint64_t max_iter, int mode, double* phi, uint64_t* iterations, double* rel,
                   int* converged, double* trace, double* row_trace, uint64_t trace_cap) {
-  return guard([&] {  // solver.cpp:158-362
-    if (n == 0) {
-      if (iterations) *iterations = 0;
-      if (converged) *converged = 1;
-      if (rel) *rel = 0.0;
-      return;
-    }
-    need(phi, "output");
-    DevBuf<double> d_sw, d_tgt;
-    CglsInput in;
-    solve_common(ctx, n, bits, rows, words, weights, targets, d_sw, d_tgt, in);
-    in.constraint_target = ct;
-    in.constraint_weight = cw;
-    in.global_pair_count = rows / 2;
-    if (mode < 0 || mode > 2) throw DataError("solver mode must be 0 (reference protocol), 1 (fused) or 2 (fixed order)");
-    in.fixed_order = mode == 2;
-    CglsResult r = cgls_solve(ctx->c, in, tol, max_iter, mode == 2 ? 0 : mode, trace || row_trace);
-    std::memcpy(phi, r.phi.data(), uint64_t(n) * 8);
-    if (iterations) *iterations = r.iterations;
-    if (rel) *rel = r.relative_residual;
-    if (converged) *converged = r.converged ? 1 : 0;
-    for (uint64_t i = 0; i < trace_cap; ++i) {
-      if (trace && i < r.trace.size()) trace[i] = r.trace[i];
-      if (row_trace && i < r.row_residual_trace.size()) row_trace[i] = r.row_residual_trace[i];
-    }
+  return guard([&] {
+    solve_cgls_impl(ctx, n, bits, rows, words, weights, targets, ct, cw, tol, max_iter, mode, rows / 2, phi,
+                    iterations, rel, converged, trace, row_trace, trace_cap);
+  });
+}
+
+int sf_solve_cgls_ex(sf_ctx* ctx, uint32_t n, const uint64_t* bits, uint64_t rows, uint64_t words,
+                     const double* weights, const double* targets, double ct, double cw, double tol,
+                     uint64_t max_iter, int mode, uint64_t global_pair_count, double* phi, uint64_t* iterations,
+                     double* rel, int* converged, double* trace, double* row_trace, uint64_t trace_cap) {
+  return guard([&] {
+    solve_cgls_impl(ctx, n, bits, rows, words, weights, targets, ct, cw, tol, max_iter, mode, global_pair_count,
+                    phi, iterations, rel, converged, trace, row_trace, trace_cap);
   });
 }
 

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const uint32_t* __restrict__ col, const uint32_t* __restrict__ ep, const float* __restrict__ isd,
                    uint32_t V, const float* __restrict__ w1img, const float* __restrict__ b1,
                    const float* __restrict__ W2, const float* __restrict__ b2, uint32_t C, uint32_t cls,
-                   uint64_t row0, uint64_t rows, float* __restrict__ out, float* __restrict__ allprobs) {
+                   uint64_t row0, uint64_t rows, float* __restrict__ out, float* __restrict__ allprobs,
+                   float* __restrict__ apart_out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   float* sW2 = reinterpret_cast<float*>(smem + kOffW2);
   float* sA = sW2 + kD * C;  // a[m][:] after the u loop
@@ -117,12 +118,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kD >> 3) << 17) | (uint32_t(kM >> 4) << 24);
   const uint64_t K4 = kD / 4;
 
-  for (uint32_t u = 0; u < U; ++u) {
-    const uint32_t b = u & 1u;
+  // u range of this CTA: gridDim.y CTAs split B_1 (their partial a's are
+  // summed in CTA order by tail_finish_kernel)
+  const uint32_t S = gridDim.y, ub = U * blockIdx.y / S, ue = U * (blockIdx.y + 1) / S;
+  for (uint32_t u = ub; u < ue; ++u) {
+    const uint32_t b = (u - ub) & 1u, ul = u - ub;
     // (1) A_u: this thread's coalition, columns [c0, c0 + 64): partial sums
     // in item order, isd(u) scale, tf32 hi/lo into TMEM
-    if (u >= 1) {  // the previous u's MMAs read the A region: wait for them
-      mbar_wait(&h_full[(u - 1) & 1u], ((u - 1) >> 1) & 1u);
+    if (ul >= 1) {  // the previous u's MMAs read the A region: wait for them
+      mbar_wait(&h_full[(ul - 1) & 1u], ((ul - 1) >> 1) & 1u);
       tc_fence_after();
     }
     const float su = __ldg(&isd_t[uint64_t(u) * kTile + i]);
@@ -133,17 +137,36 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < 8; ++j) s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       const float4* src = Apart + ((tile * items) * kTile + i) * K4 + (c0 + 32 * cc) / 4;
-      for (uint32_t it = ib; it < ie; ++it) {
+      uint32_t it = ib;
+      for (; it + 2 <= ie; it += 2) {  // two items' loads in flight, summed in item order
         const float4* p = src + uint64_t(it) * kTile * K4;
-        float4 v[8];
+        float4 v[8], w[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(p + j);
+        for (int j = 0; j < 8; ++j) {
+          v[j] = __ldg(p + j);
+          w[j] = __ldg(p + uint64_t(kTile) * K4 + j);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           s[j].x += v[j].x;
           s[j].y += v[j].y;
           s[j].z += v[j].z;
           s[j].w += v[j].w;
+          s[j].x += w[j].x;
+          s[j].y += w[j].y;
+          s[j].z += w[j].z;
+          s[j].w += w[j].w;
+        }
+      }
+      if (it < ie) {
+        const float4* p = src + uint64_t(it) * kTile * K4;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = __ldg(p + j);
+          s[j].x += v.x;
+          s[j].y += v.y;
+          s[j].z += v.z;
+          s[j].w += v.w;
         }
       }
       uint32_t hv[32], lv[32];
@@ -167,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     // (2) MMAs: H_u[b] = A_u W1, 3xTF32, 16 k-steps
     if (tid == 0) {
-      if (u == 0) mbar_wait(w_full, 0);
+      if (ul == 0) mbar_wait(w_full, 0);
       const uint32_t sw = su32(smem + kOffW);
       const uint32_t d = tmem + b * kD;
 #pragma unroll 1
@@ -182,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_commit(&h_full[b]);
     }
     // (3) epilogue of u: relu(H + b1) scaled by the target-row coefficient
-    mbar_wait(&h_full[b], (u >> 1) & 1u);
+    mbar_wait(&h_full[b], (ul >> 1) & 1u);
     tc_fence_after();
     float coef;
     if (u == 0) {
@@ -208,6 +231,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     tc_fence_before();
+  }
+  if (S > 1) {  // partial a of this u range -> [tp][s][m][k]
+    float* o = apart_out + ((tp * S + blockIdx.y) * kM + m) * uint64_t(kD) + c0;
+#pragma unroll
+    for (int j = 0; j < kD / 2; j += 4)
+      *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+    return;
   }
   // (4) a -> shared memory, z = b2 + a W2, softmax, p[cls]
   __syncthreads();
@@ -243,6 +279,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// a = sum of the u-range partials (CTA order), z = b2 + a W2, softmax, p[cls]
+__global__ void __launch_bounds__(kThreads)
+    tail_finish_kernel(const float* __restrict__ apart, uint32_t S, const float* __restrict__ W2,
+                       const float* __restrict__ b2, uint32_t C, uint32_t cls, uint64_t row0, uint64_t rows,
+                       float* __restrict__ out, float* __restrict__ allprobs) {
+  extern __shared__ float fsm[];
+  float* sW2 = fsm;                 // [kD][C]
+  float* sA = sW2 + kD * C;         // [32][kD + 1]: 32 coalitions per CTA
+  float* sZ = sA + 32 * (kD + 1);   // [32][C]
+  const uint64_t tp = blockIdx.x;
+  const uint32_t m0 = blockIdx.y * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (uint32_t idx = tid; idx < kD * C; idx += kThreads) sW2[idx] = __ldg(&W2[idx]);
+  for (uint32_t idx = tid; idx < 32 * kD; idx += kThreads) {
+    const uint32_t ml = idx / kD, k = idx % kD;
+    float a = 0.f;
+    for (uint32_t sidx = 0; sidx < S; ++sidx) a += apart[((tp * S + sidx) * kM + m0 + ml) * uint64_t(kD) + k];
+    sA[ml * (kD + 1) + k] = a;
+  }
+  __syncthreads();
+  for (uint32_t idx = tid; idx < 32 * C; idx += kThreads) {
+    const uint32_t ml = idx / C, c = idx % C;
+    float v0 = b2[c], v1 = 0.f;
+    const float* a = sA + ml * (kD + 1);
+#pragma unroll 4
+    for (int k = 0; k < kD; k += 2) {
+      v0 = fmaf(a[k], sW2[k * C + c], v0);
+      v1 = fmaf(a[k + 1], sW2[(k + 1) * C + c], v1);
+    }
+    sZ[idx] = v0 + v1;
+  }
+  __syncthreads();
+  for (uint32_t ml = warp; ml < 32; ml += kThreads / 32) {
+    const uint64_t row = row0 + 2 * tp * kTile + m0 + ml;
+    if (row >= rows) continue;
+    softmax_row_warp(sZ + ml * C, C, lane);
+    if (lane == 0) out[row] = sZ[ml * C + cls];
+    __syncwarp();
+    if (allprobs)
+      for (uint32_t c = lane; c < C; c += 32) allprobs[row * C + c] = sZ[ml * C + c];
+  }
+}
+
 }  // namespace
 
 size_t tail_tc_smem(uint32_t C) {
@@ -266,10 +345,30 @@ void launch_tail_tc(Ctx& ctx, const Engine& e, const float* apart, const uint64_
   const uint32_t C = uint32_t(e.dims[3]);
   const size_t smem = tail_tc_smem(C);
   set_max_dynamic_smem(tail_tc_kernel, int(227 * 1024));
-  tail_tc_kernel<<<unsigned(ntp / 2), kThreads, smem, ctx.stream>>>(
+  // split B_1 over S CTAs per tile pair when the tile pairs alone do not
+  // fill the SMs (one CTA per SM: 512 TMEM columns, ~218 KB smem)
+  int sms = 148;
+  SF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
+  const uint64_t tps = ntp / 2;
+  uint32_t S = 1;
+  while (S < e.U && tps * S < uint64_t(sms)) ++S;
+  float* apart_out = nullptr;
+  if (S > 1) {
+    ctx.tail_part.reserve(tps * S * kM * kD);
+    apart_out = ctx.tail_part.p;
+  }
+  tail_tc_kernel<<<dim3(unsigned(tps), S), kThreads, smem, ctx.stream>>>(
       reinterpret_cast<const float4*>(apart), e.tc_items, e.tc_u_items.p, e.U, maskt, Wp, e.row_ptr.p, e.col.p,
-      e.edge_player.p, isd, e.V, e.tail_w1img.p, e.b[1]->p, e.w[2]->p, e.b[2]->p, C, cls, row0, rows, out, allprobs);
+      e.edge_player.p, isd, e.V, e.tail_w1img.p, e.b[1]->p, e.w[2]->p, e.b[2]->p, C, cls, row0, rows, out, allprobs,
+      apart_out);
   SF_LAUNCHED(ctx);
+  if (S > 1) {
+    const size_t fsmem = (size_t(kD) * C + 32 * (kD + 1) + 32 * size_t(C)) * 4;
+    set_max_dynamic_smem(tail_finish_kernel, int(fsmem));
+    tail_finish_kernel<<<dim3(unsigned(tps), kM / 32), kThreads, fsmem, ctx.stream>>>(
+        ctx.tail_part.p, S, e.w[2]->p, e.b[2]->p, C, cls, row0, rows, out, allprobs);
+    SF_LAUNCHED(ctx);
+  }
 }
 
 }  // namespace sfb

@@ -403,10 +403,11 @@ CglsResult solve_cgls(const WlsProblem& p, Communicator& comm, const CglsOptions
   std::uint64_t it = 0;
   double rel = 0.0;
   int conv = 0;
-  bind.check_call(sf_solve_cgls(bind.ctx(), p.num_players, bits.data(), p.num_rows, W, p.weights.data(),
-                                p.targets.data(), p.constraint_target, p.constraint_weight, opts.tol, opts.max_iter,
-                                /*mode=*/opts.fixed_order ? 2 : 0, res.phi.data(), &it, &rel, &conv,
-                                opts.trace ? trace.data() : nullptr,
+  bind.check_call(sf_solve_cgls_ex(bind.ctx(), p.num_players, bits.data(), p.num_rows, W, p.weights.data(),
+                                   p.targets.data(), p.constraint_target, p.constraint_weight, opts.tol,
+                                   opts.max_iter, /*mode=*/opts.fixed_order ? 2 : 0,
+                                   std::max<std::uint64_t>(p.global_pair_count, p.num_rows / 2), res.phi.data(), &it,
+                                   &rel, &conv, opts.trace ? trace.data() : nullptr,
                                 opts.trace ? row_trace.data() : nullptr, cap));
   res.iterations = it;
   res.relative_residual = rel;

@@ -261,23 +261,65 @@ def test_explain_direct_solver_and_dispatch(ctx, ref, port):
     assert np.linalg.norm(a.phi - c.phi) <= 1e-3 * np.linalg.norm(c.phi)
 
 
-@pytest.mark.parametrize("n", [40, 700])
-def test_fixed_order_is_layout_independent(ctx, port, n):
-    """CglsOptions::fixed_order (solver.hpp:62-65): with exact level sums the
-    solution must not depend on how pairs are laid out. Permuting the pair
-    order (same pairs, different tiles, splits and list/nibble split points)
-    gives bitwise the same phi; and it agrees with the default mode."""
-    k = 60 * n
-    p = sf.plan_sizes(n, k, False)
-    bits, ros = ctx.generate_masks(p, 300 + n)
-    vals = toy_game_values(bits, port)
+def test_fixed_order_modes(ctx, port):
+    """CglsOptions::fixed_order (solver.hpp:62-65), both device schemes.
+    Small systems follow the reference's folder tree (leaves in bit-reversed
+    pair order, one scalar + one vector all-reduce per iteration); large ones
+    use exact level sums, which make phi independent of the pair layout
+    altogether: permuting the pairs (different tiles, splits, list/nibble
+    split points) gives bitwise the same phi. Both agree with the default
+    mode to rounding."""
+    for n, k in ((40, 2400), (2100, 150_000)):
+        p = sf.plan_sizes(n, k, False)
+        bits, ros = ctx.generate_masks(p, 300 + n)
+        vals = toy_game_values(bits, port)
+        w = sf.assemble_weights(n, bits, ros)
+        t, ct = vals - 0.25, 0.5
+        s0 = ctx.stats()
+        a = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=2, max_iter=4 * n)
+        s1 = ctx.stats()
+        again = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=2, max_iter=4 * n)
+        assert np.array_equal(a["phi"], again["phi"])
+        ref0 = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=0, max_iter=4 * n)
+        assert np.linalg.norm(a["phi"] - ref0["phi"]) <= 1e-8 * np.linalg.norm(ref0["phi"])
+        if n == 40:  # the reference protocol: 1 scalar + 1 vector per iteration, +1 vector at init
+            assert s1["scalar_allreduce"] - s0["scalar_allreduce"] == a["iterations"]
+            assert s1["vector_allreduce"] - s0["vector_allreduce"] == a["iterations"] + 1
+        else:
+            perm = np.random.default_rng(n).permutation(bits.shape[0] // 2)
+            rows = np.stack([2 * perm, 2 * perm + 1], 1).reshape(-1)
+            b = ctx.solve_cgls(n, bits[rows], w[rows], t[rows], ct, 1e6, mode=2, max_iter=4 * n)
+            assert a["iterations"] == b["iterations"]
+            assert np.array_equal(a["phi"], b["phi"])
+
+
+def test_device_resident_stages_match_host_stages(ctx, ref, port):
+    """sf_masks_device -> sf_predict_dmasks -> sf_solve_dmasks (explain.cpp:
+    91-114 without moving the mask block over PCIe): the downloaded block is
+    the reference's MaskBlock bit for bit, the predictions equal the host-row
+    path, and phi equals solve_cgls on the host-assembled system."""
+    from paper_2506_22668_b200 import workloads as Wl
+
+    d = Wl.build("C1")
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+    sg = g.extract(d["target"], cfg.hops)
+    n = sg.n
+    p = sf.plan_sizes(n, 4000, True)
+    seed = sf.node_sampling_seed(1, d["target"])
+    dm = ctx.masks_device(p, seed)
+    rows, nn, ros = dm.info()
+    bits = dm.download()
+    want, want_ros = ref.generate_masks(n, 4000, seed)
+    assert nn == n and rows == bits.shape[0] and np.array_equal(bits, want)
+    assert np.array_equal(ros, np.asarray(want_ros, np.uint64))
+    pd = dm.predict(m, sg, 2)
+    ph = ctx.predict_batched(m, sg, bits, 2)
+    assert np.array_equal(pd, ph)
+    base, full = 0.25, 0.75
+    a = dm.solve(pd, base, full)
     w = sf.assemble_weights(n, bits, ros)
-    t, ct = vals - 0.25, 0.5
-    a = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=2, max_iter=4 * n)
-    perm = np.random.default_rng(n).permutation(bits.shape[0] // 2)
-    rows = np.stack([2 * perm, 2 * perm + 1], 1).reshape(-1)
-    b = ctx.solve_cgls(n, bits[rows], w[rows], t[rows], ct, 1e6, mode=2, max_iter=4 * n)
+    b = ctx.solve_cgls(n, bits, w, pd.astype(np.float64) - base, full - base, 1e6)
     assert a["iterations"] == b["iterations"]
-    assert np.array_equal(a["phi"], b["phi"])
-    ref0 = ctx.solve_cgls(n, bits, w, t, ct, 1e6, mode=0, max_iter=4 * n)
-    assert np.linalg.norm(a["phi"] - ref0["phi"]) <= 1e-8 * np.linalg.norm(ref0["phi"])
+    assert np.linalg.norm(a["phi"] - b["phi"]) <= 1e-10 * np.linalg.norm(b["phi"])
