@@ -825,6 +825,12 @@ __global__ void pair_sq_kernel(const double* __restrict__ a, uint64_t pairs, uin
   d[j] = j < pairs ? a[2 * j] * a[2 * j] + a[2 * j + 1] * a[2 * j + 1] : 0.0;
 }
 
+// x <- r - x (exact row residual sqrt(W) t - sqrt(W) M phi for the fused protocol)
+__global__ void residual_kernel(const double* __restrict__ r, double* __restrict__ x, uint64_t rows) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < rows) x[i] = r[i] - x[i];
+}
+
 __global__ void fill_kernel(double* __restrict__ x, double value, uint64_t count) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (i < count) x[i] = value;
@@ -991,7 +997,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t bytes = (in.kept_only ? 1 : 2) * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
                          (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
-                         uint64_t(n) * 8 * 5 + 8 + kRedBlocks * 8 + 64 * 8 + 32 * 8 + 16 * 256;
+                         uint64_t(n) * 8 * 6 + 16 + rows * 8 + kRedBlocks * 8 + 64 * 8 + 32 * 8 + 18 * 256;
   const bool repro_req = in.fixed_order;
   // fixed order: the reference's folder tree when the dense leaves are small
   // (and the cross-rank sum is the caller's fold-by-halves or a 2-rank sum),
@@ -1011,7 +1017,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   if (repro && mode != 0) throw DataError("fixed-order summation runs the reference protocol (solver mode 0)");
   constexpr int kBins = 2201;  // frexp exponents -1100..1100
   const uint64_t repro_bytes =
-      repro ? (3ull * n + 8 + 3 * rows * 2 + 3 * ptiles * 64 * 2 + 3 * std::max<uint64_t>(pairs, 1) + rows +
+      repro ? (2 * (3ull * n + 3) + 3 * rows * 2 + 3 * ptiles * 64 * 2 + 3 * std::max<uint64_t>(pairs, 1) + rows +
                (2ull * kBins + 8) + 64) * 8 + 16 * 256
             : 0;
   const uint64_t tree_bytes = tree ? (tree_local + 2) * 8 + 256 : 0;
@@ -1032,7 +1038,8 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   double* s_part = sc.take<double>((max_splits + max_nsplits + 1) * n);
   double* vpart = sc.take<double>(std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs);
   double* s = sc.take<double>(n);
-  double* tv = sc.take<double>(n + 1);  // fused mode: [A^T v ; ||v||^2]
+  double* tv = sc.take<double>(2ull * n + 2);  // fused mode: [A^T v ; ||v||^2 ; A^T r_exact]
+  double* vphi = mode == 1 ? sc.take<double>(std::max<uint64_t>(rows, 1)) : nullptr;  // fused: sw M phi
   double* u = sc.take<double>(n);
   double* phi = sc.take<double>(n);
   double* tleaf = tree ? sc.take<double>(tree_local + 2) : nullptr;  // scalar tree leaves
@@ -1542,7 +1549,25 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     // all-reduce of [A^T v ; ||v||^2]; s follows the recurrence
     // s <- s - theta A^T A u instead of s = A^T r (same math, different
     // rounding; r is not formed). Stop rule and error semantics unchanged.
+    // Residual replacement every `every` iterations: the exact gradient
+    // A^T r(phi) (r = sqrt(W)(t - M phi), pin row sqrt(cw)(ct - sum phi))
+    // rides in the same all-reduce, so the recurrence's drift stays
+    // bounded and the collective count stays one per iteration.
+    static const uint64_t every =
+        std::getenv("SF_CGLS_RECOMPUTE") ? std::strtoull(std::getenv("SF_CGLS_RECOMPUTE"), nullptr, 10) : 10;
     while (res.iterations < maxit) {
+      const bool exact = every && res.iterations > 0 && res.iterations % every == 0;
+      if (exact) {
+        reduce(phi, n, 0, 0.0, scal + 13);  // sum phi
+        if (rows) {
+          forward_v(phi, in.dev_sw, scal + 13, vphi);
+          residual_kernel<<<blocks_for(rows), 256, 0, st>>>(r, vphi, rows);  // vphi <- sw t - sw M phi
+          SF_LAUNCHED(ctx);
+          transpose_local(vphi, tv + n + 1);
+        } else {
+          SF_CUDA(cudaMemsetAsync(tv + n + 1, 0, uint64_t(n) * 8, st));
+        }
+      }
       reduce(u, n, 0, 0.0, scal + 0);  // sum_u (pin row: v_c = scw sum_u)
       if (rows) {
         forward_v(u, in.dev_sw, scal + 0, v);
@@ -1551,7 +1576,16 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
         SF_CUDA(cudaMemsetAsync(tv, 0, uint64_t(n) * 8, st));
       }
       reduce(dsq, rows ? fwd_blocks : 0, 0, 0.0, tv + n);
-      comm_allreduce_sum(ctx, tv, uint64_t(n) + 1);
+      comm_allreduce_sum(ctx, tv, exact ? 2ull * n + 1 : uint64_t(n) + 1);
+      if (exact) {
+        fetch(13, 1);
+        r_c = scw * in.constraint_target - scw * host[13];
+        // s <- exact gradient at phi (+ the pin row); the step below then
+        // applies -theta (A^T v + scw v_c) as usual
+        SF_CUDA(cudaMemcpyAsync(s, tv + n + 1, uint64_t(n) * 8, cudaMemcpyDeviceToDevice, st));
+        add_scalar_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw * r_c, n);
+        SF_LAUNCHED(ctx);
+      }
       fetch(0, 1);
       SF_CUDA(cudaMemcpyAsync(host + 1, tv + n, sizeof(double), cudaMemcpyDeviceToHost, st));
       comm_sync(ctx);

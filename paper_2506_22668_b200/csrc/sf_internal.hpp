@@ -289,6 +289,7 @@ struct Ctx {
   DevBuf<uint8_t> fid_inv;
   ExtractState extract;             // device extraction (large balls)
   DevBuf<float> tail_part;          // tcgen05 tail: per-u-range partial layer-2 aggregations
+  DevBuf<uint32_t> tail_count;      // tcgen05 tail: arrivals per tile pair (last CTA finishes)
   DevBuf<uint64_t> gram_maskt;      // direct solve: tile-transposed rows
   DevBuf<unsigned char> gram_work;  // direct solve: plan, run weights, targets
   DevBuf<double> gram_g;            // direct solve: Gram partials, factor, copy, rhs

@@ -14,6 +14,8 @@
 // quarter, 64 columns each).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "sf_device.cuh"
 #include "sf_internal.hpp"
 #include "sf_tcgen05.cuh"
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    uint32_t V, const float* __restrict__ w1img, const float* __restrict__ b1,
                    const float* __restrict__ W2, const float* __restrict__ b2, uint32_t C, uint32_t cls,
                    uint64_t row0, uint64_t rows, float* __restrict__ out, float* __restrict__ allprobs,
-                   float* __restrict__ apart_out) {
+                   float* __restrict__ apart_out, uint32_t* __restrict__ counters) {
   extern __shared__ __align__(1024) unsigned char smem[];
   float* sW2 = reinterpret_cast<float*>(smem + kOffW2);
   float* sA = sW2 + kD * C;  // a[m][:] after the u loop
@@ -232,23 +234,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
   }
-  if (S > 1) {  // partial a of this u range -> [tp][s][m][k]
+  if (S > 1) {
+    // partial a of this u range -> [tp][s][m][k]; the last of the S CTAs of
+    // the tile pair sums the partials in s order (deterministic) and finishes
     float* o = apart_out + ((tp * S + blockIdx.y) * kM + m) * uint64_t(kD) + c0;
 #pragma unroll
     for (int j = 0; j < kD / 2; j += 4)
       *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-    tc_fence_before();
+    __threadfence();
     __syncthreads();
-    if (warp == 0) {
-      tc_fence_after();
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    uint32_t* flag = reinterpret_cast<uint32_t*>(tmem_slot + 1);
+    if (counters == nullptr) {  // tail_finish_kernel sums the partials
+      tc_fence_before();
+      if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+      }
+      return;
     }
-    return;
-  }
-  // (4) a -> shared memory, z = b2 + a W2, softmax, p[cls]
-  __syncthreads();
+    if (tid == 0) {
+      const uint32_t prev = atomicAdd(&counters[tp], 1u);
+      *flag = prev == S - 1 ? 1u : 0u;
+      if (prev == S - 1) counters[tp] = 0u;  // ready for the next launch
+    }
+    __syncthreads();
+    if (*flag == 0u) {
+      tc_fence_before();
+      if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+      }
+      return;
+    }
+    __threadfence();
+    for (uint32_t idx = tid; idx < kM * kD; idx += kThreads) {
+      const uint32_t mm = idx / kD, k = idx % kD;
+      float a = 0.f;
+      for (uint32_t sidx = 0; sidx < S; ++sidx) a += __ldcg(&apart_out[((tp * S + sidx) * kM + mm) * uint64_t(kD) + k]);
+      sA[mm * (kD + 1) + k] = a;
+    }
+  } else {
+    // (4) a -> shared memory, z = b2 + a W2, softmax, p[cls]
+    __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kD / 2; ++j) sA[m * (kD + 1) + c0 + j] = acc[j];
+    for (int j = 0; j < kD / 2; ++j) sA[m * (kD + 1) + c0 + j] = acc[j];
+  }
   __syncthreads();
   for (uint32_t idx = tid; idx < kM * C; idx += kThreads) {
     const uint32_t mm = idx / C, c = idx % C;
@@ -353,16 +383,27 @@ void launch_tail_tc(Ctx& ctx, const Engine& e, const float* apart, const uint64_
   uint32_t S = 1;
   while (S < e.U && tps * S < uint64_t(sms)) ++S;
   float* apart_out = nullptr;
+  uint32_t* counters = nullptr;
   if (S > 1) {
     ctx.tail_part.reserve(tps * S * kM * kD);
     apart_out = ctx.tail_part.p;
+    // the last CTA of a tile pair finishes (SF_TAIL_LAST=1) or a second
+    // kernel does (default)
+    static const bool last = std::getenv("SF_TAIL_LAST") && std::atoi(std::getenv("SF_TAIL_LAST")) != 0;
+    if (last) {
+      if (ctx.tail_count.n < tps) {  // zeroed once; the finishing CTA resets its counter
+        ctx.tail_count.reserve(tps);
+        SF_CUDA(cudaMemsetAsync(ctx.tail_count.p, 0, tps * 4, ctx.stream));
+      }
+      counters = ctx.tail_count.p;
+    }
   }
   tail_tc_kernel<<<dim3(unsigned(tps), S), kThreads, smem, ctx.stream>>>(
       reinterpret_cast<const float4*>(apart), e.tc_items, e.tc_u_items.p, e.U, maskt, Wp, e.row_ptr.p, e.col.p,
       e.edge_player.p, isd, e.V, e.tail_w1img.p, e.b[1]->p, e.w[2]->p, e.b[2]->p, C, cls, row0, rows, out, allprobs,
-      apart_out);
+      apart_out, counters);
   SF_LAUNCHED(ctx);
-  if (S > 1) {
+  if (S > 1 && counters == nullptr) {
     const size_t fsmem = (size_t(kD) * C + 32 * (kD + 1) + 32 * size_t(C)) * 4;
     set_max_dynamic_smem(tail_finish_kernel, int(fsmem));
     tail_finish_kernel<<<dim3(unsigned(tps), kM / 32), kThreads, fsmem, ctx.stream>>>(
