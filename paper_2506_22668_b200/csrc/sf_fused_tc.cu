@@ -53,7 +53,9 @@ constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + 
 constexpr int kBLoadWarp = kMmaWarp + 1;  // one warp, one lane: B tiles from the B bank
 constexpr int kThreads = (kBLoadWarp + 1) * 32;
 
-template <int D>
+constexpr int kTabCap = 8192;  // 1/sqrt table entries in shared memory (u16-degree variant)
+
+template <int D, bool DEG = false>
 struct TcCfg {
   // smem stage: B (gathered P rows, K-major) hi | lo; A lives in TMEM
   static constexpr int B_LBO = (D / 8) * 128;          // k-unit stride (n-groups of 8 rows)
@@ -63,14 +65,17 @@ struct TcCfg {
   static constexpr int STAGE = ((2 * B_BYTES + 1023) / 1024) * 1024;
   // raw stage: isd rows (2 tiles) | mask words (2 tiles); B tiles come
   // pre-transposed from the B bank straight into the stage
+  // isd rows are f32 (4 B) or u16 degrees (2 B, DEG) per coalition
+  static constexpr int ISD_ELEM = DEG ? 2 : 4;
   static constexpr int RAW_ISD = 0;
-  static constexpr int RAW_W = RAW_ISD + kKC * kM * 4;
+  static constexpr int RAW_W = RAW_ISD + kKC * kM * ISD_ELEM;
   static constexpr int RAW = ((RAW_W + kKC * 2 * 8 + 127) / 128) * 128;
   static constexpr int OFF_RAW = kCanStages * STAGE;
   static constexpr int OFF_KFL = OFF_RAW + kRawStages * RAW;  // the item's k-step flags
   static constexpr int OFF_BIAS = OFF_KFL + kMaxKsteps;      // b0 (D floats)
   static constexpr int OFF_BARS = OFF_BIAS + D * 4;
-  static constexpr int SMEM = OFF_BARS + 8 * (2 * kRawStages + 3 * kCanStages + 4) + 16;
+  static constexpr int OFF_TAB = ((OFF_BARS + 8 * (2 * kRawStages + 3 * kCanStages + 4) + 16 + 15) / 16) * 16;
+  static constexpr int SMEM = OFF_TAB + (DEG ? kTabCap * 4 : 0);
   // TMEM columns: H buffers [0, 2D), accumulator [2D, 3D), A stages (hi 32 | lo 32) from 3D
   static constexpr uint32_t A_COL = 3 * D;
   static constexpr uint32_t TMEM_COLS = 3 * D + kCanStages * 2 * kKC <= 256 ? 256 : 512;
@@ -102,9 +107,10 @@ constexpr int kProfSites = 16;
     }                                                  \
   } while (0)
 
-template <int D, bool PROF>
+template <int D, bool PROF, bool DEG>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_tc_kernel(const uint64_t* __restrict__ maskt, uint64_t Wp, const float* __restrict__ isd,
+                    const uint16_t* __restrict__ deg16, const float* __restrict__ tab, uint32_t tab_n,
                     uint32_t V, const float* __restrict__ bbank, const uint32_t* __restrict__ item_chunk,
                     const float* __restrict__ bias,
                     const uint2* __restrict__ ent, const uint8_t* __restrict__ kflags,
@@ -112,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t* __restrict__ item_seg, const uint32_t* __restrict__ item_order,
                     uint32_t items, const uint64_t* __restrict__ const_words, float* __restrict__ Apart,
                     unsigned long long* __restrict__ prof) {
-  using Cfg = TcCfg<D>;
+  using Cfg = TcCfg<D, DEG>;
   uint64_t pw[3] = {0, 0, 0};
   const long long t_begin = PROF ? clock64() : 0;
   auto prof_flush = [&](int base, int n) {
@@ -156,6 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < D; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_BIAS)[j] = bias[j];
+  if constexpr (DEG)
+    for (uint32_t j = tid; j < tab_n; j += kThreads) reinterpret_cast<float*>(smem + Cfg::OFF_TAB)[j] = tab[j];
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "r"(Cfg::TMEM_COLS));
@@ -186,13 +194,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       // trip counts are warp-uniform (J0 steps by whole warps), so every lane
       // takes part in the shuffles
-      for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
+      if constexpr (DEG) {
+        for (int J0 = pw_base; J0 < cnt * 2 * 8; J0 += kProdWarps * 32) {  // u16 degree rows, 2 tiles
+          const int J = J0 + lane, k = min(J >> 4, 31), q = (J >> 3) & 1, ug = J & 7;
+          const uint32_t x = __shfl_sync(kFull, rec.x, k);
+          if (J < cnt * 2 * 8)
+            cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 8) * 2,
+                       deg16 + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 8);
+        }
+      } else {
+        for (int J0 = pw_base; J0 < cnt * 2 * 16; J0 += kProdWarps * 32) {  // isd rows, 2 tiles
           const int J = J0 + lane, k = min(J >> 5, 31), q = (J >> 4) & 1, ug = J & 15;
           const uint32_t x = __shfl_sync(kFull, rec.x, k);
           if (J < cnt * 2 * 16)
             cp_async16(rw + Cfg::RAW_ISD + (k * kM + q * kTile + ug * 4) * 4,
                        isd + ((t0 + q) * uint64_t(V) + x) * kTile + ug * 4);
         }
+      }
       {  // mask words, one u64 per (entry, tile); self -> all ones, pad -> zero
         const int k = pt >> 1, q = pt & 1;
         const uint32_t y = __shfl_sync(kFull, rec.y, k & 31);
@@ -214,6 +232,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();  // the A stage in TMEM is rewritten after the MMAs that read it
       const unsigned char* rw = smem + Cfg::OFF_RAW + r * Cfg::RAW;
       const float* isds = reinterpret_cast<const float*>(rw + Cfg::RAW_ISD);
+      const uint16_t* degs = reinterpret_cast<const uint16_t*>(rw + Cfg::RAW_ISD);
+      const float* stab = reinterpret_cast<const float*>(smem + Cfg::OFF_TAB);
       const uint64_t* ws = reinterpret_cast<const uint64_t*>(rw + Cfg::RAW_W);
       unsigned char* st = smem + s * Cfg::STAGE;
       const int cnt = int(min(uint32_t(kKC), e1 - (e0 + c * kKC)));  // multiple of 8
@@ -228,7 +248,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int w = 0; w < 16; ++w) {
             const int k = k0 + w;
-            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? isds[k * kM + m] : 0.f;
+            float iv;
+            // entries past the chunk's count hold stale stage data (their
+            // k-steps are not issued): keep the table index in range
+            if constexpr (DEG) iv = stab[degs[k * kM + m] & (kTabCap - 1)];
+            else iv = isds[k * kM + m];
+            const float cf = ((ws[k * 2 + tq] >> i) & 1ull) ? iv : 0.f;
             const float h = tf32_hi(cf);
             hv[w] = __float_as_uint(h);
             lv[w] = __float_as_uint(cf - h);
@@ -333,7 +358,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t tile = t0 + (m >> 6);
     const int i = m & 63;
     const uint64_t* mt = maskt + tile * Wp;
-    const float* isd_t = isd + tile * uint64_t(V) * kTile;
+    const float* isd_t = DEG ? nullptr : isd + tile * uint64_t(V) * kTile;
+    const uint16_t* deg_t = DEG ? deg16 + tile * uint64_t(V) * kTile : nullptr;
+    const float* stab_e = reinterpret_cast<const float*>(smem + Cfg::OFF_TAB);
     const float* sbias = reinterpret_cast<const float*>(smem + Cfg::OFF_BIAS);
     const uint32_t lane_base = uint32_t(q * 32) << 16;
     const uint32_t acc_col = 2 * D + hb;
@@ -349,7 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s0 = item_seg[item], s1 = item_seg[item + 1];
     auto factors = [&](uint32_t k, float& svk, float& dvk) {
       const uint2 se = seg[k];
-      svk = __ldg(&isd_t[uint64_t(se.x) * kTile + i]);
+      if constexpr (DEG) svk = stab_e[__ldg(&deg_t[uint64_t(se.x) * kTile + i])];
+      else svk = __ldg(&isd_t[uint64_t(se.x) * kTile + i]);
       const bool muv = se.y == kSelf || ((__ldg(&mt[se.y]) >> i) & 1ull);
       dvk = muv ? svk : 0.f;
     };
@@ -467,17 +495,18 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <int D, bool PROF>
+template <int D, bool PROF, bool DEG>
 void launch_tc_impl(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, const float* isd,
                     const uint16_t* deg16, uint64_t ntp, float* apart, unsigned long long* prof) {
-  using Cfg = TcCfg<D>;
-  set_max_dynamic_smem(fused_tc_kernel<D, PROF>, int(Cfg::SMEM));
+  using Cfg = TcCfg<D, DEG>;
+  set_max_dynamic_smem(fused_tc_kernel<D, PROF, DEG>, int(Cfg::SMEM));
   const size_t smem = Cfg::SMEM;
   dim3 grid(e.tc_items, unsigned(ntp / 2));
-  fused_tc_kernel<D, PROF><<<grid, kThreads, smem, ctx.stream>>>(
-      maskt, Wp, isd, e.V, e.tc_bbank.p, e.tc_item_chunk.p, e.b[0]->p, reinterpret_cast<const uint2*>(e.tc_ent.p),
-      e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p), e.tc_item_ent.p, e.tc_item_seg.p,
-      e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p), apart, prof);
+  fused_tc_kernel<D, PROF, DEG><<<grid, kThreads, smem, ctx.stream>>>(
+      maskt, Wp, isd, deg16, e.isd_tab.p, e.isd_tab_n, e.V, e.tc_bbank.p, e.tc_item_chunk.p, e.b[0]->p,
+      reinterpret_cast<const uint2*>(e.tc_ent.p), e.tc_kflags.p, reinterpret_cast<const uint2*>(e.tc_seg.p),
+      e.tc_item_ent.p, e.tc_item_seg.p, e.tc_item_order.p, e.tc_items, reinterpret_cast<const uint64_t*>(e.tc_const.p),
+      apart, prof);
   SF_LAUNCHED(ctx);
 }
 
@@ -488,7 +517,8 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
                const uint16_t* deg16, uint64_t ntp, float* apart) {
   static const bool prof_on = std::getenv("SF_TC_PROF") != nullptr;
   if (!prof_on) {
-    launch_tc_impl<D, false>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, nullptr);
+    if (deg16) launch_tc_impl<D, false, true>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, nullptr);
+    else launch_tc_impl<D, false, false>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, nullptr);
     return;
   }
   static unsigned long long* dprof = nullptr;
@@ -497,7 +527,8 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
     SF_CUDA(cudaMalloc(&dprof, kProfSites * sizeof(unsigned long long)));
     SF_CUDA(cudaMemset(dprof, 0, kProfSites * sizeof(unsigned long long)));
   }
-  launch_tc_impl<D, true>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, dprof);
+  if (deg16) launch_tc_impl<D, true, true>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, dprof);
+  else launch_tc_impl<D, true, false>(ctx, e, maskt, Wp, isd, deg16, ntp, apart, dprof);
   if (++nlaunch % 100 == 0) {
     unsigned long long h[kProfSites];
     SF_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
@@ -516,6 +547,7 @@ void launch_tc(Ctx& ctx, const Engine& e, const uint64_t* maskt, uint64_t Wp, co
 }  // namespace
 
 bool tc_width(uint64_t d) { return d == 32 || d == 64 || d == 128; }
+uint32_t tc_deg_table_cap() { return uint32_t(kTabCap); }
 
 // Padded entries / k-step flags / segments / items for the tensor-core path
 // (segments padded to multiples of e.tc_kstep entries).

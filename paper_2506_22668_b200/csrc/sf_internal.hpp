@@ -193,6 +193,9 @@ struct Engine {
   DevBuf<uint8_t> tc_kflags;
   // tensor-core tail (sf_tail_tc.cu): 3-layer, hidden 128/128
   bool tail_tc = false;
+  // degrees as u16 rows + a 1/sqrt table instead of f32 isd rows (tcgen05
+  // path with the tcgen05 tail: every consumer reads degrees)
+  bool deg_only = false;
   DevBuf<float> tail_w1img;  // W1 as a K-major tf32 hi | lo image
 };
 
@@ -410,10 +413,11 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
 // tensor-core tail (sf_tail_tc.cu)
 bool tail_tc_supported(const Engine& e);
+uint32_t tc_deg_table_cap();
 void build_tail_tc(Ctx& ctx, Engine& e);
 void launch_tail_tc(Ctx& ctx, const Engine& e, const float* apart, const uint64_t* maskt, uint64_t Wp,
-                    const float* isd, uint64_t ntp, uint32_t cls, uint64_t row0, uint64_t rows, float* out,
-                    float* allprobs);
+                    const float* isd, const uint16_t* deg16, uint64_t ntp, uint32_t cls, uint64_t row0,
+                    uint64_t rows, float* out, float* allprobs);
 // extract_computational_graph (graph.cpp:195-261) on the device, byte-
 // identical to the host version; features are not copied (sg.source = &g)
 Subgraph extract_device(Ctx& ctx, const Graph& g, uint32_t target, int hops);

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tail_tc_kernel(const float4* __restrict__ Apart, uint32_t items, const uint32_t* __restrict__ u_items,
                    uint32_t U, const uint64_t* __restrict__ maskt, uint64_t Wp, const uint32_t* __restrict__ row_ptr,
                    const uint32_t* __restrict__ col, const uint32_t* __restrict__ ep, const float* __restrict__ isd,
+                   const uint16_t* __restrict__ deg16, const float* __restrict__ tab,
                    uint32_t V, const float* __restrict__ w1img, const float* __restrict__ b1,
                    const float* __restrict__ W2, const float* __restrict__ b2, uint32_t C, uint32_t cls,
                    uint64_t row0, uint64_t rows, float* __restrict__ out, float* __restrict__ allprobs,
@@ -108,11 +109,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m = q * 32 + lane;
   const uint64_t tile = t0 + (m >> 6);
   const int i = m & 63;
-  const float* isd_t = isd + tile * uint64_t(V) * kTile;
+  // isd of node x for this coalition: f32 rows or u16 degrees + table
+  const float* isd_t = isd ? isd + tile * uint64_t(V) * kTile : nullptr;
+  const uint16_t* deg_t = deg16 ? deg16 + tile * uint64_t(V) * kTile : nullptr;
+  auto isd_of = [&](uint32_t x) {
+    return deg_t ? __ldg(&tab[__ldg(&deg_t[uint64_t(x) * kTile + i])]) : __ldg(&isd_t[uint64_t(x) * kTile + i]);
+  };
   const uint64_t* mt = maskt + tile * Wp;
   const uint32_t lane_base = uint32_t(q * 32) << 16;
   const int c0 = half * (kD / 2);
-  const float isd0 = __ldg(&isd_t[i]);
+  const float isd0 = isd_of(0);
   const uint32_t e_beg = row_ptr[0], e_end = row_ptr[1];
   float acc[kD / 2];
 #pragma unroll
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&h_full[(ul - 1) & 1u], ((ul - 1) >> 1) & 1u);
       tc_fence_after();
     }
-    const float su = __ldg(&isd_t[uint64_t(u) * kTile + i]);
+    const float su = isd_of(u);
     const uint32_t ib = u_items[u], ie = u_items[u + 1];
 #pragma unroll 1
     for (int cc = 0; cc < 2; ++cc) {  // 32-column chunks
@@ -370,8 +376,8 @@ void build_tail_tc(Ctx& ctx, Engine& e) {
 }
 
 void launch_tail_tc(Ctx& ctx, const Engine& e, const float* apart, const uint64_t* maskt, uint64_t Wp,
-                    const float* isd, uint64_t ntp, uint32_t cls, uint64_t row0, uint64_t rows, float* out,
-                    float* allprobs) {
+                    const float* isd, const uint16_t* deg16, uint64_t ntp, uint32_t cls, uint64_t row0,
+                    uint64_t rows, float* out, float* allprobs) {
   const uint32_t C = uint32_t(e.dims[3]);
   const size_t smem = tail_tc_smem(C);
   set_max_dynamic_smem(tail_tc_kernel, int(227 * 1024));
@@ -400,7 +406,7 @@ void launch_tail_tc(Ctx& ctx, const Engine& e, const float* apart, const uint64_
   }
   tail_tc_kernel<<<dim3(unsigned(tps), S), kThreads, smem, ctx.stream>>>(
       reinterpret_cast<const float4*>(apart), e.tc_items, e.tc_u_items.p, e.U, maskt, Wp, e.row_ptr.p, e.col.p,
-      e.edge_player.p, isd, e.V, e.tail_w1img.p, e.b[1]->p, e.w[2]->p, e.b[2]->p, C, cls, row0, rows, out, allprobs,
+      e.edge_player.p, isd, deg16, e.isd_tab.p, e.V, e.tail_w1img.p, e.b[1]->p, e.w[2]->p, e.b[2]->p, C, cls, row0, rows, out, allprobs,
       apart_out, counters);
   SF_LAUNCHED(ctx);
   if (S > 1 && counters == nullptr) {
