@@ -990,13 +990,24 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t nib_pblocks = (n + kNbPlayers - 1) / kNbPlayers;
   // nibble kernels run 3 CTAs per SM; ~8 waves keep the tail wave small
   const uint64_t nib_ctas = 24ull * sms;
-  const uint64_t max_nsplits = (nib_ctas + nib_pblocks - 1) / nib_pblocks;
+  // tensor-core (i8) passes: 128 lanes per item, splits of <= 16384 tiles
+  // (2^20 elements: the S32 accumulators stay exact), >= 2 items per SM
+  const bool i8 = cgls_i8_enabled();
+  const uint64_t i8_pb = (n + 127) / 128;
+  const uint64_t i8_max_nsplits = std::max<uint64_t>((2ull * sms + i8_pb - 1) / i8_pb, (ptiles + 16383) / 16384);
+  const uint64_t i8_max_parts = std::min<uint64_t>((W + 3) / 4, std::max<uint64_t>(2ull * sms, (W + 16383) / 16384));
+  const uint64_t max_nsplits =
+      i8 ? i8_max_nsplits : (nib_ctas + nib_pblocks - 1) / nib_pblocks;
   const uint64_t fblocks_max = (rows + 63) / 64 + 8ull * sms + 2 + (pairs + 255) / 256 + 1;
   // nibble forward: the player axis in parts so the grid covers the SMs
-  const uint32_t nb_parts_max = uint32_t((n + kNbChunk - 1) / kNbChunk);
+  const uint32_t nb_parts_max =
+      i8 ? uint32_t(i8_max_parts) : uint32_t(std::min<uint64_t>((n + kNbChunk - 1) / kNbChunk, nib_ctas));
+  const uint64_t i8_bytes =
+      i8 ? cgls_i8_digit_bytes(uint64_t(W) * 64) + cgls_i8_digit_bytes(ptiles * 64) + cgls_i8_scratch_doubles() * 8 + 64
+         : 0;
   const uint64_t bytes = (in.kept_only ? 1 : 2) * ptiles * Wp * 8 + pairs + rows * 8 * 2 + fblocks_max * 8 + rows * 4 +
                          (fblocks_max + max_splits + max_nsplits + 4) * 4 + 2 * ptiles * 64 * 8 + pairs * 8 +
-                         (max_splits + max_nsplits + 1) * n * 8 + std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs * 8 +
+                         (max_splits + max_nsplits + 1) * n * 8 + uint64_t(nb_parts_max) * pairs * 8 + i8_bytes + 5 * 256 +
                          uint64_t(n) * 8 * 6 + 16 + rows * 8 + kRedBlocks * 8 + 64 * 8 + 32 * 8 + 18 * 256;
   const bool repro_req = in.fixed_order;
   // fixed order: the reference's folder tree when the dense leaves are small
@@ -1036,7 +1047,11 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   uint32_t* d_bounds = sc.take<uint32_t>(fblocks_max + max_splits + max_nsplits + 4);
   double* kc = sc.take<double>(pairs);
   double* s_part = sc.take<double>((max_splits + max_nsplits + 1) * n);
-  double* vpart = sc.take<double>(std::min<uint64_t>(nb_parts_max, nib_ctas) * pairs);
+  double* vpart = sc.take<double>(uint64_t(nb_parts_max) * pairs);
+  uint8_t* i8_udig = i8 ? sc.take<uint8_t>(cgls_i8_digit_bytes(uint64_t(W) * 64)) : nullptr;  // digits of u
+  uint8_t* i8_cdig = i8 ? sc.take<uint8_t>(cgls_i8_digit_bytes(ptiles * 64)) : nullptr;      // of the coefficients
+  double* i8_abs = i8 ? sc.take<double>(cgls_i8_scratch_doubles()) : nullptr;
+  int* i8_exp = i8 ? sc.take<int>(2) : nullptr;
   double* s = sc.take<double>(n);
   double* tv = sc.take<double>(2ull * n + 2);  // fused mode: [A^T v ; ||v||^2 ; A^T r_exact]
   double* vphi = mode == 1 ? sc.take<double>(std::max<uint64_t>(rows, 1)) : nullptr;  // fused: sw M phi
@@ -1246,7 +1261,17 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint32_t splits = uint32_t(sbounds.size() - 1);
   // nibble part: uniform tile splits (every dense tile costs the same)
   std::vector<uint32_t> nbounds{uint32_t(tiles_b)};
-  if (ptiles > tiles_b) {
+  if (ptiles > tiles_b && i8) {
+    // i8 passes: split boundaries on whole digit groups (4 tiles)
+    const uint64_t nt = ptiles - tiles_b;
+    uint64_t ns = std::max<uint64_t>((2ull * sms + i8_pb - 1) / i8_pb, (nt + 16383) / 16384);
+    ns = std::max<uint64_t>(1, std::min<uint64_t>({ns, max_nsplits, (nt + 15) / 16}));
+    for (uint64_t k = 1; k < ns; ++k) {
+      const uint64_t b = (tiles_b + nt * k / ns) & ~uint64_t(3);
+      if (b > nbounds.back()) nbounds.push_back(uint32_t(b));
+    }
+    nbounds.push_back(uint32_t(ptiles));
+  } else if (ptiles > tiles_b) {
     const uint64_t nt = ptiles - tiles_b;
     const uint64_t ns = std::max<uint64_t>(1, std::min<uint64_t>(max_nsplits, (nt + kNbTT - 1) / kNbTT));
     for (uint64_t k = 1; k <= ns; ++k) nbounds.push_back(uint32_t(tiles_b + nt * k / ns));
@@ -1257,6 +1282,16 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       1, std::min<uint64_t>({uint64_t(nb_parts_max), nib_ctas,
                              (nib_ctas + nb_rowblocks - 1) / std::max<uint64_t>(nb_rowblocks, 1)})));
   const uint32_t nb_part_players = uint32_t(((uint64_t(n) + nb_parts - 1) / nb_parts + 63) / 64 * 64);
+  // i8 forward: parts of the word axis (whole digit groups, <= 16384 words)
+  // so that >= 2 items per SM
+  uint32_t i8_parts = 1, i8_part_words = ((W + 3) / 4) * 4;
+  if (i8 && pairs_n) {
+    const uint64_t lb = (pairs_n + 127) / 128;
+    uint64_t parts = std::max<uint64_t>((2ull * sms + lb - 1) / lb, (W + 16383) / 16384);
+    parts = std::max<uint64_t>(1, std::min<uint64_t>(parts, nb_parts_max));
+    i8_part_words = uint32_t(((W + parts - 1) / parts + 3) / 4 * 4);
+    i8_parts = uint32_t((W + i8_part_words - 1) / i8_part_words);
+  }
   const uint64_t pstride = nb_rowblocks * 256;
   uint64_t* rT = nullptr;
   if (pairs_n) {
@@ -1309,7 +1344,14 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
           pl_off, pl_idx, n, lsegs, ce, s_part + uint64_t(splits + nsplits) * n);
       SF_LAUNCHED(ctx);
     }
-    if (nsplits) {
+    if (nsplits && i8) {
+      launch_cgls_digits(ce, tiles_b * 64, ptiles * 64, i8_abs, i8_cdig, i8_exp + 1, st);
+      SF_LAUNCHED(ctx);
+      ctx.launches++;
+      launch_bitmat_i8(mte, Wp, n, n, nsplits, nsplit_start, 0, uint32_t(ptiles), i8_cdig, i8_exp + 1,
+                       s_part + uint64_t(splits) * n, n, sms, st);
+      SF_LAUNCHED(ctx);
+    } else if (nsplits) {
       nib_transpose_kernel<<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
           mte, Wp, n, ptiles, nsplit_start, ce, s_part + uint64_t(splits) * n);
       SF_LAUNCHED(ctx);
@@ -1396,7 +1438,17 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
           in.dev_rows, W, row_start, is_comp, x, n, swp, sum_u, vout, dsq, in.kept_only ? 1 : 0);
       SF_LAUNCHED(ctx);
     }
-    if (nb_rowblocks) {
+    if (nb_rowblocks && i8) {
+      launch_cgls_digits(x, 0, n, i8_abs, i8_udig, i8_exp, st);
+      SF_LAUNCHED(ctx);
+      ctx.launches++;
+      launch_bitmat_i8(rT, pstride, pstride, pairs_n, i8_parts, nullptr, i8_part_words, W, i8_udig, i8_exp, vpart,
+                       pairs_n, sms, st);
+      SF_LAUNCHED(ctx);
+      nib_forward_finish<<<unsigned(nb_rowblocks), 256, 0, st>>>(vpart, i8_parts, pd, pairs, swp, sum_u, vout,
+                                                                   dsq + fblocks + lblocks);
+      SF_LAUNCHED(ctx);
+    } else if (nb_rowblocks) {
       nib_forward_kernel<<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 4 * 16 * 8, st>>>(
           rT, pstride, pairs_n, x, n, nb_part_players, vpart);
       SF_LAUNCHED(ctx);

@@ -412,6 +412,20 @@ struct CglsInput {
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);
 // tensor-core tail (sf_tail_tc.cu)
+// Tensor-core (tcgen05 kind::i8, exact integer) passes of the bit-row CGLS
+// over the dense pairs (sf_cgls_i8.cu). SF_CGLS_I8=0 keeps the nibble tables.
+bool cgls_i8_enabled();
+uint64_t cgls_i8_digit_bytes(uint64_t elements);
+uint64_t cgls_i8_scratch_doubles();
+// digit groups of x over [beg, len) (groups aligned down from beg); the grid
+// exponent goes to *exp_slot
+void launch_cgls_digits(const double* x, uint64_t beg, uint64_t len, double* partial, uint8_t* digits, int* exp_slot,
+                        cudaStream_t st);
+// out[p][lane] = sum over the words of part p of the lane's bits x the digit groups
+void launch_bitmat_i8(const uint64_t* words, uint64_t stride, uint64_t lanes, uint64_t out_lanes, uint32_t nparts,
+                      const uint32_t* split_start, uint32_t part_words, uint32_t total_words, const uint8_t* digits,
+                      const int* exp_slot, double* out, uint64_t out_stride, int sms, cudaStream_t st);
+
 bool tail_tc_supported(const Engine& e);
 uint32_t tc_deg_table_cap();
 void build_tail_tc(Ctx& ctx, Engine& e);

@@ -2,6 +2,9 @@
 solve_cgls + solve_direct, solver.cpp:95-428). The reference's own solver tests
 (test_solver.cpp) re-expressed through the C-ABI, plus parity with the
 reference / bit-row restatement at larger sizes."""
+import os
+import pathlib
+
 import numpy as np
 import pytest
 
@@ -185,6 +188,54 @@ def test_cgls_pass_variants_agree(ctx, ref, port, n, k, seed, monkeypatch):
     for name in out:
         d = np.linalg.norm(out[name] - out["bits"]) / np.linalg.norm(out["bits"])
         assert d <= 1e-8, (name, d)
+
+
+I8_WORKER = r"""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.environ["SF_ROOT"])
+import paper_2506_22668_b200 as sf
+n, k, seed = (int(x) for x in sys.argv[1:4])
+ctx = sf.Context(0)
+p = sf.plan_sizes(n, k, False)
+bits, ros = ctx.generate_masks(p, seed)
+vals = np.cos(np.arange(bits.shape[0]) * 0.11) * 0.5 + 0.5
+w = sf.assemble_weights(n, bits, ros)
+r = ctx.solve_cgls(n, bits, w, vals - 0.25, 0.5, 1e6, max_iter=4 * n)
+np.save(sys.argv[4], r["phi"])
+"""
+
+
+@pytest.mark.parametrize("n,k,seed", [(999, 20000, 5), (3001, 40000, 6)])
+def test_cgls_i8_passes_agree(ctx, ref, tmp_path, n, k, seed, monkeypatch):
+    """The tensor-core dense-pair passes (SF_CGLS_I8=1: A operand in TMEM,
+    2: in shared memory; exact integer sums over 16 digits of the vector)
+    solve the same system as the nibble tables, and the two operand paths
+    give bitwise the same phi (the sums do not depend on how the work is
+    staged). SF_CGLS_NIB_DENSITY=0 puts every pair tile on the dense path."""
+    import subprocess
+    import sys as _sys
+
+    script = tmp_path / "i8.py"
+    script.write_text(I8_WORKER)
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    phis = {}
+    for mode in ("0", "1", "2"):
+        env = dict(os.environ, SF_ROOT=root, SF_CGLS_I8=mode, SF_CGLS_NIB_DENSITY="0")
+        out = tmp_path / f"phi{mode}.npy"
+        subprocess.run([_sys.executable, str(script), str(n), str(k), str(seed), str(out)], check=True, env=env,
+                       timeout=600)
+        phis[mode] = np.load(out)
+    p = sf.plan_sizes(n, k, False)
+    bits, ros = ctx.generate_masks(p, seed)
+    vals = np.cos(np.arange(bits.shape[0]) * 0.11) * 0.5 + 0.5
+    phi_ref, _, _, _ = ref.solve_cgls(n, bits, vals, 0.25, 0.75, max_iter=4 * n)
+    assert np.array_equal(phis["1"], phis["2"])
+    for mode in ("1", "2"):
+        d = np.linalg.norm(phis[mode] - phis["0"]) / np.linalg.norm(phis["0"])
+        assert d <= 1e-8, (mode, d)
+        err = np.linalg.norm(phis[mode] - phi_ref) / np.linalg.norm(phi_ref)
+        assert err <= 1e-3, (mode, err)
 
 
 @pytest.mark.parametrize("n", [40, 300, 1000, 2100])
