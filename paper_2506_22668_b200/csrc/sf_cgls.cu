@@ -1329,6 +1329,27 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     }
   };
   // out = sum over pairs of the coefficients on their set bits + *kconst
+  // The sparse-pair list passes run on a side stream beside the dense-pair
+  // passes (they write disjoint partials; SF_CGLS_OVERLAP=0 serialises).
+  static const bool overlap_env = [] {
+    const char* v = std::getenv("SF_CGLS_OVERLAP");
+    return v == nullptr || std::strcmp(v, "0") != 0;
+  }();
+  auto fork = [&]() {
+    SideStream& sd = ctx.side;
+    if (!sd.s) {
+      SF_CUDA(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+      SF_CUDA(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+      SF_CUDA(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
+    }
+    SF_CUDA(cudaEventRecord(sd.fork, st));
+    SF_CUDA(cudaStreamWaitEvent(sd.s, sd.fork, 0));
+    return sd.s;
+  };
+  auto join = [&]() {
+    SF_CUDA(cudaEventRecord(ctx.side.join, ctx.side.s));
+    SF_CUDA(cudaStreamWaitEvent(st, ctx.side.join, 0));
+  };
   auto passes = [&](const double* ce, const double* co, const double* kconst, double* out) {
     if (splits) {
       dim3 grid(unsigned(pblocks), splits);
@@ -1339,8 +1360,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
         SF_LAUNCHED(ctx);
       }
     }
+    const bool ov = overlap_env && lists && nsplits;
     if (lists) {
-      list_transpose_kernel<<<blocks_for(uint64_t(n) * 32), 256, 0, st>>>(
+      cudaStream_t ls = ov ? fork() : st;
+      list_transpose_kernel<<<blocks_for(uint64_t(n) * 32), 256, 0, ls>>>(
           pl_off, pl_idx, n, lsegs, ce, s_part + uint64_t(splits + nsplits) * n);
       SF_LAUNCHED(ctx);
     }
@@ -1356,6 +1379,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
           mte, Wp, n, ptiles, nsplit_start, ce, s_part + uint64_t(splits) * n);
       SF_LAUNCHED(ctx);
     }
+    if (ov) join();
     transpose_finish_kernel<<<blocks_for(n), 256, 0, st>>>(s_part, splits + nsplits + (lists ? 1 : 0), n,
                                                            kconst, out);
     SF_LAUNCHED(ctx);
@@ -1428,8 +1452,10 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   // sums of v^2 in dsq[0, fwd_blocks)
   const uint64_t fwd_blocks = fblocks + lblocks + nb_rowblocks;
   auto forward_v = [&](const double* x, const double* swp, const double* sum_u, double* vout) {
+    const bool ov = overlap_env && lblocks && nb_rowblocks;
     if (lblocks) {
-      list_forward_kernel<<<unsigned(lblocks), 256, 0, st>>>(row_off, row_idx, pd, x, swp, sum_u, vout,
+      cudaStream_t ls = ov ? fork() : st;
+      list_forward_kernel<<<unsigned(lblocks), 256, 0, ls>>>(row_off, row_idx, pd, x, swp, sum_u, vout,
                                                               dsq + fblocks);
       SF_LAUNCHED(ctx);
     }
@@ -1456,6 +1482,7 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                                                                    sum_u, vout, dsq + fblocks + lblocks);
       SF_LAUNCHED(ctx);
     }
+    if (ov) join();
   };
   set_max_dynamic_smem(forward_kernel, int(kFwdChunk * 8));
   // v = sqrt(W) M u; delta = ||v||^2 all-reduced + v_c^2 (solver.cpp:252-287)

@@ -241,9 +241,25 @@ struct ExtractState {
   DevBuf<unsigned char> tmp;
 };
 
+// A second stream on the same device for work that overlaps the main
+// stream's kernels (fork/join through the two events).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  SideStream() = default;
+  SideStream(const SideStream&) = delete;
+  SideStream& operator=(const SideStream&) = delete;
+  ~SideStream() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  SideStream side;  // CGLS: the sparse-pair list passes beside the dense-pair passes
   int rank = 0, world = 1;
   std::unique_ptr<Nccl> nccl;
   HostComm host_comm;
