@@ -330,6 +330,43 @@ __global__ void __launch_bounds__(256)
     if (w0 + r < W) rT[uint64_t(w0 + r) * pstride + jl0 + tx] = t[tx][r];
 }
 
+// The same word-major rows from the tile-transposed layout: per (dense tile
+// t, word w) one warp transposes the 64 x 64 bit block (64 players' pair
+// words -> 64 pairs' player words; a 64 x 64 bit transpose is its own
+// inverse, the butterfly of transpose_tiles_kernel). Tiles past ptiles give
+// the zero pad rows. Lets the rows buffer be overwritten by rT.
+__global__ void __launch_bounds__(256)
+    tiles_word_major_kernel(const uint64_t* __restrict__ mt, uint64_t Wp, uint32_t W, uint64_t tiles_b,
+                            uint64_t ptiles, uint64_t pstride, uint64_t* __restrict__ rT) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t blk = blockIdx.x * 8ull + (threadIdx.x >> 5);
+  const uint64_t nt = pstride / 64;  // tile slots of rT (dense tiles + zero pad)
+  if (blk >= nt * W) return;
+  const uint32_t w = uint32_t(blk / nt);
+  const uint64_t tl = blk % nt, t = tiles_b + tl;
+  uint64_t* o = rT + uint64_t(w) * pstride + tl * 64;
+  if (t >= ptiles) {
+    o[lane] = 0ull;
+    o[lane + 32] = 0ull;
+    return;
+  }
+  const uint64_t* src = mt + t * Wp + uint64_t(w) * 64;
+  const uint64_t r0 = src[lane], r1 = src[lane + 32];
+  uint32_t a = uint32_t(r0), b = uint32_t(r0 >> 32), c = uint32_t(r1), d = uint32_t(r1 >> 32);
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                     : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t keep = (lane & s) ? ~m : m, amt = (lane & s) ? 32 - s : s;
+    a = bfly_step(a, s, keep, amt);
+    b = bfly_step(b, s, keep, amt);
+    c = bfly_step(c, s, keep, amt);
+    d = bfly_step(d, s, keep, amt);
+  }
+  o[lane] = (uint64_t(c) << 32) | a;
+  o[lane + 32] = (uint64_t(d) << 32) | b;
+}
+
 // M u over the dense pairs, lane per pair: CTA = 256 pairs x one part of
 // the player axis, walked in chunks of kNbChunk players whose tables (built
 // from u) fill 64 KB of shared memory. Writes the even-row dots per part.
@@ -1294,7 +1331,18 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   }
   const uint64_t pstride = nb_rowblocks * 256;
   uint64_t* rT = nullptr;
-  if (pairs_n) {
+  // rT in the caller's rows buffer when it may be overwritten and nothing
+  // reads the rows during the iterations (kept-set lists on the sparse
+  // pairs, the row lists already built): saves W x pstride words (C4: the
+  // dense pairs' share of the mask bytes)
+  const bool rt_in_rows = pairs_n && lists && rows_b == 0 && pd % 64 == 0 &&
+                          in.rows_scratch_words >= uint64_t(W) * pstride;
+  if (rt_in_rows) {
+    rT = const_cast<uint64_t*>(in.dev_rows);
+    const uint64_t blocks = (pstride / 64) * W;
+    tiles_word_major_kernel<<<unsigned((blocks + 7) / 8), 256, 0, st>>>(mte, Wp, W, tiles_b, ptiles, pstride, rT);
+    SF_LAUNCHED(ctx);
+  } else if (pairs_n) {
     ctx.solver_dense.reserve(uint64_t(W) * pstride);
     rT = ctx.solver_dense.p;
     rows_word_major_kernel<<<dim3((W + 31) / 32, unsigned(pstride / 32)), 256, 0, st>>>(in.dev_rows, W, pair_step, pd, pairs,

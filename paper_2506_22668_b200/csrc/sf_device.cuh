@@ -74,4 +74,11 @@ __device__ __forceinline__ void softmax_row_warp(float* zi, uint32_t C, int lane
   __syncwarp();
 }
 
+// one 32 x 32 bit-transpose butterfly stage (see Bfly in sf_gcn.cu): send
+// rot(x) & keep to the lane s away, keep x & keep
+__device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t keep, uint32_t amt) {
+  const uint32_t send = __funnelshift_r(x, x, amt) & keep;
+  return (x & keep) | __shfl_xor_sync(0xffffffffu, send, s);
+}
+
 }  // namespace sfb

@@ -1044,12 +1044,21 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   if (e.tc) build_tc_plan(ctx, e, sg);
   if (e.tc16 && !e.tc) e.tc16 = false;  // the plan may have rejected the tensor-core path
   if (e.tc16) prepare_tc16(ctx, e);
-  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: the mma.sync tail)
-  static const bool use_tail_tc = [] {
+  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: the mma.sync tail,
+  // 1: always). By default only for |B_1| <= SF_TAIL_TC_MAXU (512): its
+  // CTAs walk their share of B_1 one u at a time (A_u build -> TMEM -> MMA),
+  // which wins at C2 (|B_1| = 425: 11.20M vs 10.71M coalitions/s) and loses
+  // at C3 (579: 3.12M vs 3.19M) and C4 (1,981: 468K vs 591K), where the
+  // mma.sync tail's many small CTAs hide the partial-sum reads better.
+  static const int use_tail_tc = [] {
     const char* v = std::getenv("SF_TAIL_TC");
-    return v == nullptr || std::strcmp(v, "0") != 0;
+    return v == nullptr ? 2 : std::atoi(v);
   }();
-  e.tail_tc = use_tail_tc && tail_tc_supported(e);
+  static const uint64_t tail_tc_maxu = [] {
+    const char* v = std::getenv("SF_TAIL_TC_MAXU");
+    return v == nullptr ? uint64_t(512) : std::strtoull(v, nullptr, 10);
+  }();
+  e.tail_tc = use_tail_tc != 0 && tail_tc_supported(e) && (use_tail_tc == 1 || e.U <= tail_tc_maxu);
   if (e.tail_tc) build_tail_tc(ctx, e);
   // u16 degree rows (masked degree recomputed from a shared-memory table in
   // the fused kernel's staging, no f32 isd pass): measured +0.3% at C2, and

@@ -743,6 +743,7 @@ static void explain_node(Ctx& ctx, const Graph& g, const Model& m, uint32_t node
     in.dev_pop = ctx.pop_dev.p;
     in.dev_is_comp = ctx.comp_dev.p;
     in.kept_only = true;
+    in.rows_scratch_words = ctx.masks.n;  // the masks are not read after the solve
     DebugTimer("explain").lap("assemble done");
     // Solver dispatch: the direct (tcgen05 Gram + device Cholesky) path
     // for small player counts on one worker, CGLS otherwise. Crossover

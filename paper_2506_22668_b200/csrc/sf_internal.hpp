@@ -424,6 +424,10 @@ struct CglsInput {
   // dev_rows holds kept-set rows only (one per pair, W words each; every
   // pair a complement pair)
   bool kept_only = false;
+  // > 0: dev_rows is the caller's scratch (capacity in words) and may be
+  // overwritten once the solver's own layouts are built — the dense pairs'
+  // word-major rows then live there instead of in a separate buffer
+  uint64_t rows_scratch_words = 0;
 };
 CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                       uint64_t max_iter, int mode, bool trace);

@@ -254,11 +254,7 @@ __global__ void philox_stream_kernel(uint64_t seed, uint64_t stream,
 // 64 x kTWords words coalesced in shared memory; each warp then transposes
 // kTWords/8 words, each a 64 x 64 bit block, as four 32 x 32 butterfly transposes
 // (5 shuffle stages each) and writes 256 contiguous bytes per output half.
-// one butterfly stage (see Bfly in sf_gcn.cu): send rot(x) & keep, keep x & keep
-__device__ __forceinline__ uint32_t bfly_step(uint32_t x, int s, uint32_t keep, uint32_t amt) {
-  const uint32_t send = __funnelshift_r(x, x, amt) & keep;
-  return (x & keep) | __shfl_xor_sync(kFull, send, s);
-}
+// (bfly_step: sf_device.cuh)
 
 constexpr int kTWords = 32;  // words per CTA (a multiple of 8: one or more per warp)
 

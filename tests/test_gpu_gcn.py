@@ -169,3 +169,55 @@ def test_c2_subset_vs_reference(ctx, ref, kernel):
     pick = np.r_[0:16, 5000:5016, 19_980:20_000]
     want = ref.predict_batched(rm, rg, d["target"], bits[pick], 5)
     assert rel_err(got[pick], want) <= RTOL
+
+
+TAIL_WORKER = r"""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.environ["SF_ROOT"])
+import paper_2506_22668_b200 as sf
+from paper_2506_22668_b200 import workloads as W
+name, k, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+ctx = sf.Context(0)
+d = W.build(name)
+cfg = d["cfg"]
+g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+m = sf.Model.random(cfg.feature_dim, cfg.hidden, cfg.classes, cfg.model_seed)
+sg = g.extract(d["target"], cfg.hops)
+bits, _ = ctx.generate_masks(sf.plan_sizes(sg.n, k, True), 99)
+np.save(out, ctx.predict_batched(m, sg, bits, 5))
+"""
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_tail_variants_agree(ctx, ref, tmp_path, name):
+    """The tcgen05 tail (SF_TAIL_TC=1) and the mma.sync tail (0) give the same
+    predictions within 1e-6 at C2 (|B_1| = 425, tcgen05 by default) and C3
+    (579, mma.sync by default: SF_TAIL_TC_MAXU), and agree with the
+    reference's predict_batched on a spread of rows."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+
+    script = tmp_path / "tail.py"
+    script.write_text(TAIL_WORKER)
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    preds = {}
+    for t in ("0", "1"):
+        out = tmp_path / f"p{t}.npy"
+        subprocess.run([sys.executable, str(script), name, "20000", str(out)], check=True, timeout=900,
+                       env=dict(os.environ, SF_ROOT=root, SF_TAIL_TC=t))
+        preds[t] = np.load(out)
+    assert rel_err(preds["1"], preds["0"]) <= 1e-6
+    d = W.build(name)
+    cfg = d["cfg"]
+    g = sf.Graph.build(cfg.nodes, d["edges"], d["features"])
+    sg = g.extract(d["target"], cfg.hops)
+    bits, _ = ctx.generate_masks(sf.plan_sizes(sg.n, 20_000, True), 99)
+    rg = ref.graph_build(cfg.nodes, d["edges"], d["features"])
+    rm = ref.model_random(cfg.feature_dim, list(cfg.hidden), cfg.classes, cfg.model_seed)
+    pick = np.r_[0:8, 10_000:10_008, 19_992:20_000]
+    want = ref.predict_batched(rm, rg, d["target"], bits[pick], 5)
+    for t in ("0", "1"):
+        assert rel_err(preds[t][pick], want) <= RTOL
