@@ -262,7 +262,8 @@ constexpr int kNbTT = 8;
 constexpr int kNbPer = 2;  // players per thread
 constexpr int kNbPlayers = 256 * kNbPer;
 
-__global__ void __launch_bounds__(256)
+template <int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks)
     nib_transpose_kernel(const uint64_t* __restrict__ mt, uint64_t Wp, uint32_t n, uint64_t ptiles,
                          const uint32_t* __restrict__ split_start, const double* __restrict__ coef,
                          double* __restrict__ s_part) {
@@ -372,20 +373,21 @@ __global__ void __launch_bounds__(256)
 // from u) fill 64 KB of shared memory. Writes the even-row dots per part.
 constexpr uint32_t kNbChunk = 2048;  // players per table chunk (a multiple of 64)
 
+template <uint32_t kChunk>
 __global__ void __launch_bounds__(256)
     nib_forward_kernel(const uint64_t* __restrict__ rT, uint64_t pstride, uint64_t pairs_n,
                        const double* __restrict__ u, uint32_t n, uint32_t part_players,
                        double* __restrict__ vpart) {
-  extern __shared__ __align__(16) double ftab[];  // [kNbChunk / 4][16]
+  extern __shared__ __align__(16) double ftab[];  // [kChunk / 4][16]
   const int tid = threadIdx.x;
   const uint64_t jl = blockIdx.x * 256ull + tid;
   const uint32_t p0 = blockIdx.y * part_players, p1 = min(n, p0 + part_players);
   const uint64_t* col = rT + jl;
   double acc0 = 0.0, acc1 = 0.0;
-  for (uint32_t c0 = p0; c0 < p1; c0 += kNbChunk) {
-    const uint32_t cp = min(kNbChunk, p1 - c0);
+  for (uint32_t c0 = p0; c0 < p1; c0 += kChunk) {
+    const uint32_t cp = min(kChunk, p1 - c0);
     __syncthreads();  // the previous chunk's lookups are done
-    for (uint32_t g = tid; g < kNbChunk / 4; g += 256) {
+    for (uint32_t g = tid; g < kChunk / 4; g += 256) {
       const uint32_t e = c0 + 4 * g;
       double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
       if (4 * g < cp) {  // n need not be a multiple of 4
@@ -1350,7 +1352,8 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     SF_LAUNCHED(ctx);
   }
   if (pairs_n) {
-    set_max_dynamic_smem(nib_forward_kernel, int(kNbChunk / 4 * 16 * 8));
+    set_max_dynamic_smem(nib_forward_kernel<kNbChunk>, int(kNbChunk / 4 * 16 * 8));
+    set_max_dynamic_smem(nib_forward_kernel<kNbChunk / 2>, int(kNbChunk / 8 * 16 * 8));
   }
   const uint32_t* row_start = d_bounds;
   const uint32_t* split_start = d_bounds + bounds.size();
@@ -1423,8 +1426,14 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                        s_part + uint64_t(splits) * n, n, sms, st);
       SF_LAUNCHED(ctx);
     } else if (nsplits) {
-      nib_transpose_kernel<<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
-          mte, Wp, n, ptiles, nsplit_start, ce, s_part + uint64_t(splits) * n);
+      // register-capped to 64 for 4 CTAs per SM (SF_NIB_T4=0: uncapped, 3)
+      static const bool t4 = !(std::getenv("SF_NIB_T4") && std::atoi(std::getenv("SF_NIB_T4")) == 0);
+      if (t4)
+        nib_transpose_kernel<4><<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
+            mte, Wp, n, ptiles, nsplit_start, ce, s_part + uint64_t(splits) * n);
+      else
+        nib_transpose_kernel<1><<<dim3(unsigned(nib_pblocks), nsplits), 256, 0, st>>>(
+            mte, Wp, n, ptiles, nsplit_start, ce, s_part + uint64_t(splits) * n);
       SF_LAUNCHED(ctx);
     }
     if (ov) join();
@@ -1501,6 +1510,9 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
   const uint64_t fwd_blocks = fblocks + lblocks + nb_rowblocks;
   auto forward_v = [&](const double* x, const double* swp, const double* sum_u, double* vout) {
     const bool ov = overlap_env && lblocks && nb_rowblocks;
+    // 1024-player table chunks (32 KB: 4 CTAs per SM) unless SF_NIB_CHUNK=2048
+    // (64 KB, 3 per SM); with the 4-CTA transpose: C2 solve 24.5 -> 23.4 ms
+    static const bool nib_half = !(std::getenv("SF_NIB_CHUNK") && std::atoi(std::getenv("SF_NIB_CHUNK")) == 2048);
     if (lblocks) {
       cudaStream_t ls = ov ? fork() : st;
       list_forward_kernel<<<unsigned(lblocks), 256, 0, ls>>>(row_off, row_idx, pd, x, swp, sum_u, vout,
@@ -1523,8 +1535,12 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
                                                                    dsq + fblocks + lblocks);
       SF_LAUNCHED(ctx);
     } else if (nb_rowblocks) {
-      nib_forward_kernel<<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 4 * 16 * 8, st>>>(
-          rT, pstride, pairs_n, x, n, nb_part_players, vpart);
+      if (nib_half)
+        nib_forward_kernel<kNbChunk / 2><<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 8 * 16 * 8, st>>>(
+            rT, pstride, pairs_n, x, n, nb_part_players, vpart);
+      else
+        nib_forward_kernel<kNbChunk><<<dim3(unsigned(nb_rowblocks), nb_parts), 256, kNbChunk / 4 * 16 * 8, st>>>(
+            rT, pstride, pairs_n, x, n, nb_part_players, vpart);
       SF_LAUNCHED(ctx);
       nib_forward_finish<<<unsigned(nb_rowblocks), 256, 0, st>>>(vpart, nb_parts, pd, pairs, swp,
                                                                    sum_u, vout, dsq + fblocks + lblocks);

@@ -1044,21 +1044,17 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   if (e.tc) build_tc_plan(ctx, e, sg);
   if (e.tc16 && !e.tc) e.tc16 = false;  // the plan may have rejected the tensor-core path
   if (e.tc16) prepare_tc16(ctx, e);
-  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: the mma.sync tail,
-  // 1: always). By default only for |B_1| <= SF_TAIL_TC_MAXU (512): its
-  // CTAs walk their share of B_1 one u at a time (A_u build -> TMEM -> MMA),
-  // which wins at C2 (|B_1| = 425: 11.20M vs 10.71M coalitions/s) and loses
-  // at C3 (579: 3.12M vs 3.19M) and C4 (1,981: 468K vs 591K), where the
-  // mma.sync tail's many small CTAs hide the partial-sum reads better.
+  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: never, 1: every
+  // batch). By default a batch takes it when it has >= 64 tile pairs (one
+  // CTA per tile pair and B_1 share, one per SM): C2 (74 tile pairs per
+  // batch) 11.20M vs 10.71M coalitions/s; C3 (28) 3.09M vs 3.16M and C4
+  // (7) 467K vs 586K favour the mma.sync tail's many small CTAs.
   static const int use_tail_tc = [] {
     const char* v = std::getenv("SF_TAIL_TC");
     return v == nullptr ? 2 : std::atoi(v);
   }();
-  static const uint64_t tail_tc_maxu = [] {
-    const char* v = std::getenv("SF_TAIL_TC_MAXU");
-    return v == nullptr ? uint64_t(512) : std::strtoull(v, nullptr, 10);
-  }();
-  e.tail_tc = use_tail_tc != 0 && tail_tc_supported(e) && (use_tail_tc == 1 || e.U <= tail_tc_maxu);
+  e.tail_tc = use_tail_tc != 0 && tail_tc_supported(e);
+  e.tail_tc_always = use_tail_tc == 1;
   if (e.tail_tc) build_tail_tc(ctx, e);
   // u16 degree rows (masked degree recomputed from a shared-memory table in
   // the fused kernel's staging, no f32 isd pass): measured +0.3% at C2, and
@@ -1184,7 +1180,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       if (!ok) throw std::logic_error("fused width not instantiated");
       if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
-      if (e.tail_tc) {  // tcgen05 tail (sf_tail_tc.cu)
+      if (e.tail_tc && (e.tail_tc_always || e.deg_only || ntp / 2 >= 64)) {  // tcgen05 tail (sf_tail_tc.cu)
         launch_tail_tc(ctx, e, pbuf, maskt, Wp, isd, e.deg_only ? deg16 : nullptr, ntp, cls, row0, rows, dev_out,
                        dev_allprobs);
         continue;

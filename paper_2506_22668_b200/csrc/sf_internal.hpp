@@ -192,7 +192,8 @@ struct Engine {
   DevBuf<uint32_t> tc_ent, tc_seg, tc_item_ent, tc_item_seg, tc_item_order, tc_u_items, tc_const;
   DevBuf<uint8_t> tc_kflags;
   // tensor-core tail (sf_tail_tc.cu): 3-layer, hidden 128/128
-  bool tail_tc = false;
+  bool tail_tc = false;         // tcgen05 tail available (W1 image built)
+  bool tail_tc_always = false;  // SF_TAIL_TC=1: for every batch, not only >= 64 tile pairs
   // degrees as u16 rows + a 1/sqrt table instead of f32 isd rows (tcgen05
   // path with the tcgen05 tail: every consumer reads degrees)
   bool deg_only = false;

@@ -191,10 +191,10 @@ np.save(out, ctx.predict_batched(m, sg, bits, 5))
 
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_tail_variants_agree(ctx, ref, tmp_path, name):
-    """The tcgen05 tail (SF_TAIL_TC=1) and the mma.sync tail (0) give the same
-    predictions within 1e-6 at C2 (|B_1| = 425, tcgen05 by default) and C3
-    (579, mma.sync by default: SF_TAIL_TC_MAXU), and agree with the
-    reference's predict_batched on a spread of rows."""
+    """The tcgen05 tail (SF_TAIL_TC=1: every batch) and the mma.sync tail
+    (0) give the same predictions within 1e-6 at C2 and C3 (by default a
+    batch takes the tcgen05 tail when it holds >= 64 tile pairs), and agree
+    with the reference's predict_batched on a spread of rows."""
     import os
     import pathlib
     import subprocess
