@@ -17,6 +17,8 @@
 // PairwiseFolder; here the parity bar is 1e-3 relative L2).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -244,14 +246,21 @@ __device__ __forceinline__ void subset_sums(double a, double b, double c, double
     for (int l = 0; l < 4; ++l) t[uint32_t(h * 4 + l) ^ key] = (h == 0) ? lo[l] : (l == 0 ? hi[h] : hi[h] + lo[l]);
 }
 
-// acc += sum over the 8 nibbles of x of tab[j][nibble_j] (tab: 8 swizzled
-// rows of 16, keys kbase + j)
-template <uint32_t kbase>
-__device__ __forceinline__ void nib8(uint32_t x, const double* __restrict__ tab, double& acc) {
+// acc += sum over the 8 nibbles of x of tab[j][nibble_j ^ (kbase + j)] (8
+// swizzled rows of 16 at base + wb + kImm). The keys are XORed into x with
+// one constant first; each lookup is then one shift and one LOP3 ((x >> s)
+// & 0x78 | wb, wb a multiple of 2048 with the low bits free) in front of
+// the LDS, whose immediate carries kImm + 128 j.
+template <uint32_t kbase, uint32_t kImm>
+__device__ __forceinline__ void nib8(uint32_t x, const char* __restrict__ base, uint32_t wb, double& acc) {
   if (x == 0u) return;
+  const uint32_t xk = x ^ (kbase == 0 ? 0x76543210u : 0xFEDCBA98u);
   double t[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) t[j] = tab[j * 16 + (((x >> (4 * j)) & 15u) ^ (kbase + j))];
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t off = ((j == 0 ? (xk << 3) : (xk >> (4 * j - 3))) & 0x78u) | wb;
+    t[j] = *reinterpret_cast<const double*>(base + off + kImm + j * 128);
+  }
   acc += ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
 }
 
@@ -296,13 +305,26 @@ __global__ void __launch_bounds__(256, kMinBlocks)
       subset_sums(a, b, c, d, uint32_t(j), &tab[buf][q][j][0]);
     }
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kNbTT; ++q)
+    const char* tbase = reinterpret_cast<const char*>(&tab[0][0][0][0]);
+    const uint32_t wb = uint32_t(buf) * uint32_t(sizeof(tab[0]));
+    static_assert(sizeof(tab[0]) % 2048 == 0, "table halves on 2048-byte boundaries");
+    auto tile = [&](auto qc) {
+      constexpr int q = decltype(qc)::value;
 #pragma unroll
       for (int p = 0; p < kNbPer; ++p) {
-        nib8<0>(uint32_t(w[q][p]), &tab[buf][q][0][0], acc[p]);
-        nib8<8>(uint32_t(w[q][p] >> 32), &tab[buf][q][8][0], acc[p]);
+        nib8<0, q * 2048>(uint32_t(w[q][p]), tbase, wb, acc[p]);
+        nib8<8, q * 2048 + 1024>(uint32_t(w[q][p] >> 32), tbase, wb, acc[p]);
       }
+    };
+    static_assert(kNbTT == 8, "unrolled over 8 tiles");
+    tile(std::integral_constant<int, 0>{});
+    tile(std::integral_constant<int, 1>{});
+    tile(std::integral_constant<int, 2>{});
+    tile(std::integral_constant<int, 3>{});
+    tile(std::integral_constant<int, 4>{});
+    tile(std::integral_constant<int, 5>{});
+    tile(std::integral_constant<int, 6>{});
+    tile(std::integral_constant<int, 7>{});
   }
   double* out = s_part + uint64_t(blockIdx.y) * n;
 #pragma unroll
@@ -404,12 +426,21 @@ __global__ void __launch_bounds__(256)
       uint64_t x[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) x[q] = (k + q < nw) ? __ldcs(col + uint64_t(w0 + k + q) * pstride) : 0ull;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double* t = ftab + (k + q) * 256;
-        nib8<0>(uint32_t(x[q]), t, (q & 1) ? acc1 : acc0);
-        nib8<8>(uint32_t(x[q] >> 32), t + 128, (q & 1) ? acc1 : acc0);
-      }
+      const char* tbase = reinterpret_cast<const char*>(ftab);
+      const uint32_t wb = k * 2048u;  // k is a multiple of 8: bits below 2^14 free
+      auto word = [&](auto qc) {
+        constexpr int q = decltype(qc)::value;
+        nib8<0, q * 2048>(uint32_t(x[q]), tbase, wb, (q & 1) ? acc1 : acc0);
+        nib8<8, q * 2048 + 1024>(uint32_t(x[q] >> 32), tbase, wb, (q & 1) ? acc1 : acc0);
+      };
+      word(std::integral_constant<int, 0>{});
+      word(std::integral_constant<int, 1>{});
+      word(std::integral_constant<int, 2>{});
+      word(std::integral_constant<int, 3>{});
+      word(std::integral_constant<int, 4>{});
+      word(std::integral_constant<int, 5>{});
+      word(std::integral_constant<int, 6>{});
+      word(std::integral_constant<int, 7>{});
     }
   }
   if (jl < pairs_n) vpart[uint64_t(blockIdx.y) * pairs_n + jl] = acc0 + acc1;

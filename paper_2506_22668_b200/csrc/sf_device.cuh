@@ -38,12 +38,17 @@ __device__ __forceinline__ void philox_block(uint64_t seed, uint64_t stream,
 // steps: (hi mod d) then ((r << 32) | lo) mod d, the second with a
 // quotient that fits 32 bits.
 __device__ __forceinline__ uint32_t mod_u64_u32(uint64_t x, uint32_t d) {
-  // x % d exactly: r = hi % d, then y = r:lo < d * 2^32, so y / d < 2^32 and
-  // the FP64 quotient estimate (53-bit) is off by at most one
+  // x % d exactly: r = hi % d, then y = r:lo < d * 2^32, so y / d < 2^32.
+  // Both quotients come from the same FP64 reciprocal (53-bit: the
+  // estimates are off by at most one, fixed below) — no integer division.
+  const double rd = __drcp_rn(static_cast<double>(d));
   const uint32_t hi = static_cast<uint32_t>(x >> 32);
-  const uint32_t r = hi % d;
+  const uint32_t q1 = __double2uint_rz(__dmul_rz(static_cast<double>(hi), rd));
+  int64_t r = static_cast<int64_t>(hi) - static_cast<int64_t>(q1) * d;
+  if (r < 0) r += d;
+  if (r >= static_cast<int64_t>(d)) r -= d;
   const uint64_t y = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(x);
-  const uint64_t q = static_cast<uint64_t>(__dmul_rz(__ull2double_rz(y), __drcp_rn(static_cast<double>(d))));
+  const uint64_t q = static_cast<uint64_t>(__dmul_rz(__ull2double_rz(y), rd));
   int64_t rem = static_cast<int64_t>(y - q * d);
   if (rem < 0) rem += d;
   if (rem >= static_cast<int64_t>(d)) rem -= d;

@@ -1044,8 +1044,8 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   if (e.tc) build_tc_plan(ctx, e, sg);
   if (e.tc16 && !e.tc) e.tc16 = false;  // the plan may have rejected the tensor-core path
   if (e.tc16) prepare_tc16(ctx, e);
-  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: never, 1: every
-  // batch). By default a batch takes it when it has >= 64 tile pairs (one
+  // layer-1 GEMM + last layer on tcgen05 (SF_TAIL_TC=0: never, 1: always).
+  // By default a call takes it when a full batch has >= 64 tile pairs (one
   // CTA per tile pair and B_1 share, one per SM): C2 (74 tile pairs per
   // batch) 11.20M vs 10.71M coalitions/s; C3 (28) 3.09M vs 3.16M and C4
   // (7) 467K vs 586K favour the mma.sync tail's many small CTAs.
@@ -1126,6 +1126,9 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   float* afbuf = reinterpret_cast<float*>(base + off_af);
   uint16_t* deg16 = (e.tc16 || e.deg_only) ? reinterpret_cast<uint16_t*>(base + off_d16) : nullptr;
 
+  // one tail for every batch of the call (the same rounding for all rows):
+  // tcgen05 when a full batch holds >= 64 tile pairs
+  const bool tail_tc_call = e.tail_tc && (e.tail_tc_always || e.deg_only || T / 2 >= 64);
   for (uint64_t t0 = 0; t0 < tiles; t0 += T) {
     const uint64_t nt = std::min(T, tiles - t0);
     const uint64_t row0 = t0 * kTile;
@@ -1180,7 +1183,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       if (!ok) throw std::logic_error("fused width not instantiated");
       if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
-      if (e.tail_tc && (e.tail_tc_always || e.deg_only || ntp / 2 >= 64)) {  // tcgen05 tail (sf_tail_tc.cu)
+      if (tail_tc_call) {  // tcgen05 tail (sf_tail_tc.cu)
         launch_tail_tc(ctx, e, pbuf, maskt, Wp, isd, e.deg_only ? deg16 : nullptr, ntp, cls, row0, rows, dev_out,
                        dev_allprobs);
         continue;

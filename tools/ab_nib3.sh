@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/abnib3; mkdir -p $O
+SF_AB_PORT=1 timeout 600 python tools/cgls_ab.py C2 > $O/ab.json 2>&1; tail -1 $O/ab.json
+timeout 1200 python -m pytest tests/test_gpu_parity_scale.py tests/test_gpu_gcn.py -q -x -s -k "not two_gpu" > $O/tests.log 2>&1; grep -E "C2:|C5|stop differs|passed|failed" $O/tests.log | tail -12
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/c2.json 2>&1; python -c "
+import json; l=[x for x in open('$O/c2.json').read().splitlines() if x.startswith('{')]; d=json.loads(l[-1]); print(d['value'], d['stage_ms_per_step'])"
