@@ -417,9 +417,9 @@ def run_batch(args):
     (explain.cpp:185-202); rank r explains targets[r::world] through
     `explain_nodes` (explain.hpp:54-57) on its own GPU, no collective on the
     data path. A step is the whole batch; value = targets/s over all ranks.
-    Concurrent targets per GPU: 8 worker contexts, host waits yielding
-    (SF_SCHED=yield; the many short per-target stream waits of 8 workers on
-    16 host cores spin-contend: profiles/round2/experiments/c5_workers/)."""
+    Concurrent targets per GPU: 6 worker contexts, host waits yielding
+    (SF_SCHED=yield; more workers' short per-target stream waits contend for
+    the host cores and make steps erratic: profiles/round2/experiments/c5_workers/)."""
     rank, world, local = dist_env()
     os.environ.setdefault("SF_SCHED", "yield")
     import paper_2506_22668_b200 as sf
@@ -498,7 +498,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the explain_node e2e leg (profiling runs)")
     ap.add_argument("--samples", type=int, default=0, help="override k (profiling runs only)")
     ap.add_argument("--targets", type=int, default=0, help="C5: number of target nodes (default 1024)")
-    ap.add_argument("--workers", type=int, default=8, help="C5: concurrent targets per GPU (sf_ctx_set_workers)")
+    ap.add_argument("--workers", type=int, default=6, help="C5: concurrent targets per GPU (sf_ctx_set_workers)")
     ap.add_argument("--explain-only", action="store_true", help="profiling: run explain_node twice and exit")
     args = ap.parse_args()
     if args.warmup < 3:
