@@ -46,7 +46,10 @@ constexpr uint32_t kSelf = 0xFFFFFFFFu;  // coefficient isd(x) (self loop)
 constexpr uint32_t kPad = 0xFFFFFFFEu;   // padding entry: coefficient 0
 constexpr int kM = 128;                  // coalitions per CTA (two tiles)
 constexpr int kKC = 32;                  // entries per chunk (4 MMA k-steps)
-constexpr int kRawStages = 4, kCanStages = 2;
+#ifndef SF_RAW_STAGES
+#define SF_RAW_STAGES 4
+#endif
+constexpr int kRawStages = SF_RAW_STAGES, kCanStages = 2;
 constexpr int kMaxKsteps = 4096;  // per work item (host checks)
 constexpr int kEpiWarps = 8, kStgWarps = 8, kProdWarps = 7;
 constexpr int kProducerWarp = kEpiWarps + kStgWarps, kMmaWarp = kProducerWarp + kProdWarps;
