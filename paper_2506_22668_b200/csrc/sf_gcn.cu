@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256)
                const uint32_t* __restrict__ ep, const uint32_t* __restrict__ order,
                uint32_t nbig, const float* __restrict__ tab, uint32_t V,
                float* __restrict__ isd, uint16_t* __restrict__ deg16,
-               uint32_t tsplit, uint32_t tchunk) {
+               uint32_t tsplit, uint32_t tchunk, uint32_t f32_nodes, uint32_t f32_stride) {
   const int lane = threadIdx.x & 31;
   const Bfly bfly32(lane);
   const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(256)
       clo += __popc(bfly32(uint32_t(x)));
       chi += __popc(bfly32(uint32_t(x >> 32)));
     }
-    if (isd) {
-      float* out = isd + (t * V + u) * kTile;
+    if (isd && u < f32_nodes) {
+      float* out = isd + (t * f32_stride + u) * kTile;
       __stcs(&out[lane], __ldg(&tab[clo]));
       __stcs(&out[lane + 32], __ldg(&tab[chi]));
     }
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(256)
   if (deg == 0) {
     const float one = __ldg(&tab[1]);
     for (uint32_t t = tb0; t < te; ++t) {
-      if (isd) {
-        float* out = isd + (uint64_t(t) * V + u) * kTile;
+      if (isd && u < f32_nodes) {
+        float* out = isd + (uint64_t(t) * f32_stride + u) * kTile;
         out[lane] = one;
         out[lane + 32] = one;
       }
@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(256)
       for (uint32_t q = 0; q < per && tb + q < te; ++q) {
         const uint32_t sh = q << lg;
         const uint32_t dlo = 1 + __popc((lo >> sh) & fmask), dhi = 1 + __popc((hi >> sh) & fmask);
-        if (isd) {
-          float* out = isd + (uint64_t(tb + q) * V + u) * kTile;
+        if (isd && u < f32_nodes) {
+          float* out = isd + (uint64_t(tb + q) * f32_stride + u) * kTile;
           __stcs(&out[lane], __ldg(&tab[dlo]));
           __stcs(&out[lane + 32], __ldg(&tab[dhi]));
         }
@@ -1056,14 +1056,16 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   e.tail_tc = use_tail_tc != 0 && tail_tc_supported(e);
   e.tail_tc_always = use_tail_tc == 1;
   if (e.tail_tc) build_tail_tc(ctx, e);
-  // u16 degree rows (masked degree recomputed from a shared-memory table in
-  // the fused kernel's staging, no f32 isd pass): measured +0.3% at C2, and
-  // the kept predictions move by ~1e-7, so it is opt-in (SF_ISD_U16=1).
-  static const bool use_deg16 = [] {
+  // u16 degree rows + a shared-memory 1/sqrt table instead of f32 isd rows
+  // for the fused kernel (f32 rows kept for B_1 when the mma.sync tail runs).
+  // SF_ISD_U16: unset = with the mma.sync tail only (C3 +3.3%, C4 +4.7%;
+  // with the tcgen05 tail, C2 -0.8%), 1 = always, 0 = never.
+  static const int deg_mode = [] {
     const char* v = std::getenv("SF_ISD_U16");
-    return v != nullptr && std::strcmp(v, "1") == 0;
+    return v == nullptr ? 2 : std::atoi(v);
   }();
-  e.deg_only = use_deg16 && e.tc && !e.tc16 && e.tail_tc && e.isd_tab_n <= tc_deg_table_cap();
+  e.deg_mode = deg_mode;
+  e.deg_capable = e.tc && !e.tc16 && e.L == 3 && e.isd_tab_n <= tc_deg_table_cap();
   dt.lap("tc plan");
   e.sg_id = sg.id;
   e.model_id = m.id;
@@ -1095,7 +1097,9 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   }
   for (int l = first_generic; l + 1 < L; ++l) hmax = std::max(hmax, R[l] * kTile * e.dims[l + 1]);
   for (int l = std::max(1, first_generic); l + 1 < L; ++l) amax = std::max(amax, R[l] * kTile * e.dims[l]);
-  const uint64_t isd_b = e.deg_only ? 2 : (e.tc16 ? 6 : 4);  // f32 isd and / or u16 degrees per (node, coalition)
+  // batch sizing with f32 isd rows (the u16-degree choice below only shrinks
+  // a batch's workspace)
+  const uint64_t isd_b = e.tc16 ? 6 : 4;  // f32 isd and / or u16 degrees per (node, coalition)
   const uint64_t per_tile = Wp * 8 + uint64_t(e.V) * kTile * isd_b + (2 * hmax + amax + apart + afused) * 4;
   // per-batch workspace (masks tiles, isd, partials, activations). Larger
   // batches mean fewer launches and fuller waves for the fused kernel: C2
@@ -1108,27 +1112,32 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
   T = std::min<uint64_t>(T, 65534);
   const bool wide = e.tc;  // the tensor-core kernels take tile pairs
   if (wide) T = (T + 1) & ~uint64_t(1);  // tile pairs: odd batches get an all-zero tile
+  // one tail for every batch of the call (the same rounding for all rows):
+  // tcgen05 when a full batch holds >= 64 tile pairs
+  const bool tail_tc_call = e.tail_tc && (e.tail_tc_always || T / 2 >= 64);
+  const bool deg = e.deg_capable && (e.deg_mode == 1 || (e.deg_mode == 2 && !tail_tc_call));
+  // u16-degree mode: f32 isd rows only for B_1 (the mma.sync tail reads them)
+  const uint64_t f32_stride = deg ? std::max<uint64_t>(e.U, 1) : e.V;
   const uint64_t off_isd = T * Wp * 8;
-  const uint64_t off_h0 = off_isd + (e.deg_only ? 0 : T * uint64_t(e.V) * kTile * 4);
+  const uint64_t off_h0 = off_isd + T * f32_stride * kTile * 4;
   const uint64_t off_h1 = off_h0 + T * hmax * 4;
   const uint64_t off_a = off_h1 + T * hmax * 4;
   const uint64_t off_p = off_a + T * amax * 4;
   const uint64_t off_af = off_p + T * apart * 4;
   const uint64_t off_d16 = (off_af + T * afused * 4 + 255) & ~uint64_t(255);
-  const uint64_t d16_bytes = (e.tc16 || e.deg_only) ? T * uint64_t(e.V) * kTile * 2 : 0;  // u16 degrees
+  const uint64_t d16_bytes = (e.tc16 || deg) ? T * uint64_t(e.V) * kTile * 2 : 0;  // u16 degrees
   ctx.work.reserve(off_d16 + d16_bytes + 256);
   unsigned char* base = ctx.work.p;
   uint64_t* maskt = reinterpret_cast<uint64_t*>(base);
-  float* isd = e.deg_only ? nullptr : reinterpret_cast<float*>(base + off_isd);
+  float* isd = reinterpret_cast<float*>(base + off_isd);
   float* hbuf[2] = {reinterpret_cast<float*>(base + off_h0), reinterpret_cast<float*>(base + off_h1)};
   float* abuf = reinterpret_cast<float*>(base + off_a);
   float* pbuf = reinterpret_cast<float*>(base + off_p);
   float* afbuf = reinterpret_cast<float*>(base + off_af);
-  uint16_t* deg16 = (e.tc16 || e.deg_only) ? reinterpret_cast<uint16_t*>(base + off_d16) : nullptr;
-
-  // one tail for every batch of the call (the same rounding for all rows):
-  // tcgen05 when a full batch holds >= 64 tile pairs
-  const bool tail_tc_call = e.tail_tc && (e.tail_tc_always || e.deg_only || T / 2 >= 64);
+  uint16_t* deg16 = (e.tc16 || deg) ? reinterpret_cast<uint16_t*>(base + off_d16) : nullptr;
+  // f32 isd rows: every node, or (u16 degrees) B_1 for the mma.sync tail, or none
+  const uint32_t f32_nodes = !deg ? uint32_t(e.V) : (tail_tc_call ? 0u : uint32_t(f32_stride));
+  if (deg && tail_tc_call) isd = nullptr;
   for (uint64_t t0 = 0; t0 < tiles; t0 += T) {
     const uint64_t nt = std::min(T, tiles - t0);
     const uint64_t row0 = t0 * kTile;
@@ -1152,7 +1161,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       const uint64_t warps = uint64_t(e.isd_nbig) * ntp + small * tsplit;
       isd_kernel<<<unsigned((warps + 7) / 8), 256, 0, ctx.stream>>>(
           maskt, Wp, uint32_t(ntp), e.row_ptr.p, e.edge_player.p, e.isd_order.p, e.isd_nbig,
-          e.isd_tab.p, e.V, isd, deg16, uint32_t(tsplit), uint32_t(tchunk));
+          e.isd_tab.p, e.V, isd, deg16, uint32_t(tsplit), uint32_t(tchunk), f32_nodes, uint32_t(f32_stride));
       SF_LAUNCHED(ctx);
     }
     const float* X = e.p0.p;  // current layer input: P0 (shared) or per-coalition H
@@ -1174,7 +1183,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         SF_CUDA(cudaEventRecord(ev->first, ctx.stream));
       }
       const bool ok = (e.tc16 && launch_fused_tc16(ctx, e, maskt, Wp, isd, deg16, ntp, pbuf)) ||
-                      (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, e.deg_only ? deg16 : nullptr, ntp, pbuf)) ||
+                      (e.tc && launch_fused_tc(ctx, e, maskt, Wp, isd, deg ? deg16 : nullptr, ntp, pbuf)) ||
                       try_fused<128>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<64>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
                       try_fused<32>(ctx, e, maskt, Wp, isd, nt, pbuf) ||
@@ -1184,7 +1193,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       if (ev) SF_CUDA(cudaEventRecord(ev->second, ctx.stream));
       const uint32_t K = uint32_t(e.dims[1]), N = uint32_t(e.dims[2]);
       if (tail_tc_call) {  // tcgen05 tail (sf_tail_tc.cu)
-        launch_tail_tc(ctx, e, pbuf, maskt, Wp, isd, e.deg_only ? deg16 : nullptr, ntp, cls, row0, rows, dev_out,
+        launch_tail_tc(ctx, e, pbuf, maskt, Wp, isd, deg ? deg16 : nullptr, ntp, cls, row0, rows, dev_out,
                        dev_allprobs);
         continue;
       }
@@ -1203,7 +1212,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
           tail_kernel<<<grid, kTailThreads, smem, ctx.stream>>>(
               reinterpret_cast<const float4*>(pbuf), e.tc ? e.tc_items : e.items,
               e.tc ? e.tc_u_items.p : e.u_items.p, maskt, Wp, e.row_ptr.p, e.col.p,
-              e.edge_player.p, isd, e.V, e.U, K, N, e.w[1]->p, e.b[1]->p,
+              e.edge_player.p, isd, uint32_t(f32_stride), e.U, K, N, e.w[1]->p, e.b[1]->p,
               L == 3 ? e.w[2]->p : nullptr, L == 3 ? e.b[2]->p : nullptr, C, L == 3 ? 1 : 0, cls,
               row0, rows, cpb, dev_out, dev_allprobs);
           SF_LAUNCHED(ctx);
@@ -1215,7 +1224,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         dim3 grid(unsigned((work + 255) / 256), unsigned(nt));
         reduce_partials_kernel<<<grid, 256, 0, ctx.stream>>>(
             reinterpret_cast<const float4*>(pbuf), e.tc ? e.tc_items : e.items,
-            e.tc ? e.tc_u_items.p : e.u_items.p, isd, e.V, K / 4, e.U,
+            e.tc ? e.tc_u_items.p : e.u_items.p, isd, uint32_t(f32_stride), K / 4, e.U,
             reinterpret_cast<float4*>(afbuf));
         SF_LAUNCHED(ctx);
       }
@@ -1241,12 +1250,12 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
       dim3 grid(Rl, unsigned(nt));
       if (l == 0) {  // generic layer 0 (unsupported widths): aggregate P0, bias, ReLU
         agg_generic_kernel<<<grid, 256, 0, ctx.stream>>>(
-            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, e.p0.p, 1, 0, Dout,
+            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, uint32_t(f32_stride), e.p0.p, 1, 0, Dout,
             e.b[0]->p, 1, Rl, out);
         SF_LAUNCHED(ctx);
       } else {
         agg_generic_kernel<<<grid, 256, 0, ctx.stream>>>(
-            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, shared_x ? 1 : 0,
+            maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, uint32_t(f32_stride), X, shared_x ? 1 : 0,
             uint32_t(Rin), Din, nullptr, 0, Rl, abuf);
         SF_LAUNCHED(ctx);
         gemm(ctx, abuf, e.w[l]->p, e.b[l]->p, out, nt * Rl * kTile, Dout, Din, true);
@@ -1265,7 +1274,7 @@ void engine_predict(Ctx& ctx, const uint64_t* dev_rows, uint64_t rows,
         set_max_dynamic_smem(last_kernel, 227 * 1024);
       dim3 grid(unsigned(nt), kTile / cpb);
       last_kernel<<<grid, 256, smem, ctx.stream>>>(
-          maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, e.V, X, shared_x ? 1 : 0,
+          maskt, Wp, e.row_ptr.p, e.col.p, e.edge_player.p, isd, uint32_t(f32_stride), X, shared_x ? 1 : 0,
           uint32_t(Rin), Din, Wt, e.b[L - 1]->p, C, cls, row0, rows, cpb, dev_out, dev_allprobs);
       SF_LAUNCHED(ctx);
     }

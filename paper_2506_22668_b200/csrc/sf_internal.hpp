@@ -194,9 +194,10 @@ struct Engine {
   // tensor-core tail (sf_tail_tc.cu): 3-layer, hidden 128/128
   bool tail_tc = false;         // tcgen05 tail available (W1 image built)
   bool tail_tc_always = false;  // SF_TAIL_TC=1: for every batch, not only >= 64 tile pairs
-  // degrees as u16 rows + a 1/sqrt table instead of f32 isd rows (tcgen05
-  // path with the tcgen05 tail: every consumer reads degrees)
-  bool deg_only = false;
+  // degrees as u16 rows + a 1/sqrt table instead of f32 isd rows for the
+  // fused kernel (decided per predict call, engine_predict)
+  bool deg_capable = false;  // tcgen05 3-layer path with the table in shared memory
+  int deg_mode = 2;           // SF_ISD_U16: 0 never, 1 always, 2 with the mma.sync tail
   DevBuf<float> tail_w1img;  // W1 as a K-major tf32 hi | lo image
 };
 
