@@ -380,6 +380,8 @@ def run_ours(args):
                       f"{((k // 2 + world - 1) // world) * max(sg.words, 1) * 8 / 1e9:.2f} GB per rank)",
                 "accuracy_mode": ("tcgen05 3xTF32 (FP32-equivalent products, FP32 accumulate)"
                                   if kernel_used == "tc" else "FP32 SIMT (CUDA cores)") + ", FP64 solver",
+                "steady_state": "value: per-target engine state (X W0, fused plan, B bank) is built in the "
+                                "warm-up and reused by the timed steps; e2e rebuilds it every call",
             },
             "stage_ms_per_step": {"sampling": stage[0] / args.steps, "prediction": stage[1] / args.steps},
             "e2e": None if not e2e_steps else {
