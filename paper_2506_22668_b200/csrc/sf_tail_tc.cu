@@ -327,12 +327,45 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t tp = blockIdx.x;
   const uint32_t m0 = blockIdx.y * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (uint32_t idx = tid; idx < kD * C; idx += kThreads) sW2[idx] = __ldg(&W2[idx]);
-  for (uint32_t idx = tid; idx < 32 * kD; idx += kThreads) {
-    const uint32_t ml = idx / kD, k = idx % kD;
-    float a = 0.f;
-    for (uint32_t sidx = 0; sidx < S; ++sidx) a += apart[((tp * S + sidx) * kM + m0 + ml) * uint64_t(kD) + k];
-    sA[ml * (kD + 1) + k] = a;
+  // 16-byte loads, all of a thread's in flight before the first use (the
+  // kernel is load-latency bound: ~50 KB per CTA from L2)
+  {
+    const float4* w4 = reinterpret_cast<const float4*>(W2);
+    float4* s4 = reinterpret_cast<float4*>(sW2);
+    const uint32_t n4 = kD * C / 4;  // kD is a multiple of 4
+#pragma unroll 6
+    for (uint32_t idx = tid; idx < n4; idx += kThreads) s4[idx] = __ldg(&w4[idx]);
+  }
+  {
+    constexpr uint32_t kQ = 32 * kD / 4 / kThreads;  // float4 of a per thread (4)
+    static_assert(32 * kD / 4 % kThreads == 0, "partial sums: whole float4 per thread");
+    float4 acc[kQ];
+#pragma unroll
+    for (uint32_t q = 0; q < kQ; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t sidx = 0; sidx < S; ++sidx) {
+      float4 v[kQ];
+#pragma unroll
+      for (uint32_t q = 0; q < kQ; ++q) {
+        const uint32_t idx = tid + q * kThreads, ml = idx / (kD / 4), k4 = idx % (kD / 4);
+        v[q] = __ldg(reinterpret_cast<const float4*>(apart + ((tp * S + sidx) * kM + m0 + ml) * uint64_t(kD)) + k4);
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < kQ; ++q) {
+        acc[q].x += v[q].x;
+        acc[q].y += v[q].y;
+        acc[q].z += v[q].z;
+        acc[q].w += v[q].w;
+      }
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < kQ; ++q) {
+      const uint32_t idx = tid + q * kThreads, ml = idx / (kD / 4), k = 4 * (idx % (kD / 4));
+      float* d = sA + ml * (kD + 1) + k;
+      d[0] = acc[q].x;
+      d[1] = acc[q].y;
+      d[2] = acc[q].z;
+      d[3] = acc[q].w;
+    }
   }
   __syncthreads();
   for (uint32_t idx = tid; idx < 32 * C; idx += kThreads) {
