@@ -139,7 +139,10 @@ __global__ void __launch_bounds__(256)
   const uint32_t fmask = G == 32 ? 0xFFFFFFFFu : (1u << G) - 1u;
   // kIsdAhead groups of `per` tiles per step: their mask words are all in
   // flight before the first transpose (the loop is latency-bound otherwise)
-  constexpr int kIsdAhead = 4;
+#ifndef SF_ISD_AHEAD
+#define SF_ISD_AHEAD 4
+#endif
+  constexpr int kIsdAhead = SF_ISD_AHEAD;
   for (uint32_t t0 = tb0; t0 < te; t0 += kIsdAhead * per) {
     uint64_t xs[kIsdAhead];
 #pragma unroll
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int k = 0; k < kIsdAhead; ++k) {
       const uint32_t tb = t0 + k * per;
-      if (tb >= te) break;  // warp-uniform
+      if (tb >= te) continue;  // warp-uniform (continue, not break: xs stays in registers)
       const uint32_t lo = bfly32(uint32_t(xs[k])), hi = bfly32(uint32_t(xs[k] >> 32));
       for (uint32_t q = 0; q < per && tb + q < te; ++q) {
         const uint32_t sh = q << lg;
