@@ -310,7 +310,17 @@ def run_ours(args):
                   "avg_launch_ms": avg_launch_s * 1000.0, "launches": dom_n.value,
                   "pairs_per_launch": pairs_per_launch,
                   "share_of_step": dom_ms.value / max(ms.value, 1e-9)}
-        if kernel_used == "tc":
+        if kernel_used == "tc16":
+            # tcgen05 kind::f16 (fp16x2: 3 MMAs per product at K = 16) against the f16 dense peak
+            peak = bf16_peak
+            issued = 3 * 2.0 * 2 * pairs_per_launch * pad.value * width.value / avg_launch_s / 1e12
+            name = f"fused_f16_kernel<{width.value}>"
+            roof = {"bound": "tensor", "achieved": useful_tflops, "peak": peak, "unit": "TFLOP/s",
+                    "frac": useful_tflops / peak, "traffic": ncu_traffic(name),
+                    "kernel": name + " (tcgen05 fp16x2, opt-in)",
+                    "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}) for kind::f16",
+                    "issued_mma_tflops": issued, "issued_frac": issued / peak, **common}
+        elif kernel_used == "tc":
             # tcgen05 kind::tf32 dense peak = half the measured bf16 dense peak
             peak = bf16_peak / 2.0
             issued = 3 * 2.0 * 2 * pairs_per_launch * pad.value * width.value / avg_launch_s / 1e12
@@ -378,8 +388,9 @@ def run_ours(args):
                 "ball_sizes": sg.ball_sizes(cfg.hops), "parallelism": f"coalition pairs g mod {world}",
                 "l2": "inputs larger than L2 (kept-set mask rows regenerated each step: "
                       f"{((k // 2 + world - 1) // world) * max(sg.words, 1) * 8 / 1e9:.2f} GB per rank)",
-                "accuracy_mode": ("tcgen05 3xTF32 (FP32-equivalent products, FP32 accumulate)"
-                                  if kernel_used == "tc" else "FP32 SIMT (CUDA cores)") + ", FP64 solver",
+                "accuracy_mode": {"tc": "tcgen05 3xTF32 (FP32-equivalent products, FP32 accumulate)",
+                                  "tc16": "tcgen05 fp16x2 (hi/lo fp16 products, FP32 accumulate)"}.get(
+                                      kernel_used, "FP32 SIMT (CUDA cores)") + ", FP64 solver",
                 "steady_state": "value: per-target engine state (X W0, fused plan, B bank) is built in the "
                                 "warm-up and reused by the timed steps; e2e rebuilds it every call",
             },
