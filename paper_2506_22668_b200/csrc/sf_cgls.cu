@@ -614,7 +614,11 @@ __global__ void axpy_kernel(double* __restrict__ y, const double* __restrict__ x
 // ||v||^2 (all-reduced, scal[1]) + v_c^2 with v_c = sqrt(cw) sum_u
 // (scal[0]); stop flag scal[12] = 2 non-finite, 1 delta <= 0; theta =
 // gamma / delta applied through scal[8] / scal[9]; r_c (scal[7]) -= theta v_c.
-__global__ void step_kernel(double* __restrict__ scal, double scw, int gslot) {
+// (scal[gslot] = scal[nslot] first: the previous iteration's gamma_next
+// becomes this iteration's gamma, so every iteration runs the same kernels
+// with the same arguments — one CUDA graph replays them)
+__global__ void step_kernel(double* __restrict__ scal, double scw, int gslot, int nslot) {
+  scal[gslot] = scal[nslot];
   const double v_c = scw * scal[0];
   const double delta = scal[1] + v_c * v_c;
   const double stop = !isfinite(delta) ? 2.0 : (delta <= 0.0 ? 1.0 : 0.0);
@@ -1417,13 +1421,17 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     const char* v = std::getenv("SF_CGLS_OVERLAP");
     return v == nullptr || std::strcmp(v, "0") != 0;
   }();
-  auto fork = [&]() {
+  auto ensure_side = [&]() {
     SideStream& sd = ctx.side;
     if (!sd.s) {
       SF_CUDA(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
       SF_CUDA(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
       SF_CUDA(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
     }
+  };
+  auto fork = [&]() {
+    SideStream& sd = ctx.side;
+    ensure_side();
     SF_CUDA(cudaEventRecord(sd.fork, st));
     SF_CUDA(cudaStreamWaitEvent(sd.s, sd.fork, 0));
     return sd.s;
@@ -1814,13 +1822,16 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     // r untouched, like the reference's break before the update.
     host[7] = r_c;
     SF_CUDA(cudaMemcpyAsync(scal + 7, host + 7, sizeof(double), cudaMemcpyHostToDevice, st));
-    int g = 2;  // gamma slot (scal[2] from the init reduce); gamma_next goes to 5 - g
-    while (res.iterations < maxit) {
+    // gamma in scal[2] (from the init reduce), gamma_next in scal[3]; the
+    // step kernel moves gamma_next into gamma at the start of an iteration
+    constexpr int g = 2, gn = 3;
+    SF_CUDA(cudaMemcpyAsync(scal + gn, scal + g, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    auto body = [&]() {
       reduce(u, n, 0, 0.0, scal + 0);  // sum_u
       if (rows) forward_v(u, in.dev_sw, scal + 0, v);
       reduce(dsq, rows ? fwd_blocks : 0, 0, 0.0, scal + 1);
       comm_allreduce_sum(ctx, scal + 1, 1);
-      step_kernel<<<1, 1, 0, st>>>(scal, scw, g);
+      step_kernel<<<1, 1, 0, st>>>(scal, scw, g, gn);
       SF_LAUNCHED(ctx);
       axpy_stop_kernel<<<blocks_for(n), 256, 0, st>>>(phi, u, scal, 1.0, n);
       SF_LAUNCHED(ctx);
@@ -1832,17 +1843,76 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       comm_allreduce_sum(ctx, s, n);
       add_pin_kernel<<<blocks_for(n), 256, 0, st>>>(s, scw, scal + 7, n);
       SF_LAUNCHED(ctx);
-      reduce(s, n, 1, 0.0, scal + (5 - g));  // gamma_next
-      direction_kernel<<<blocks_for(n), 256, 0, st>>>(u, s, scal + (5 - g), scal + g, n);
+      reduce(s, n, 1, 0.0, scal + gn);  // gamma_next
+      direction_kernel<<<blocks_for(n), 256, 0, st>>>(u, s, scal + gn, scal + g, n);
       SF_LAUNCHED(ctx);
       ctx.d2h_bytes += 16 * sizeof(double);
       SF_CUDA(cudaMemcpyAsync(host, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    };
+    // One worker, no host communicator, not one of several concurrent
+    // explain workers: the iteration body is captured once as a CUDA graph
+    // and replayed — one graph launch instead of ~15 kernel launches per
+    // iteration (C1 solve 2.8 -> 2.2 ms). Concurrent workers launch the
+    // kernels directly (their short solves do not repay the capture, and
+    // instantiation contends across threads: C5 -34% with graphs).
+    // SF_CGLS_GRAPH=0 disables it.
+    static const bool graphs_env = [] {
+      const char* e = std::getenv("SF_CGLS_GRAPH");
+      return e == nullptr || std::strcmp(e, "0") != 0;
+    }();
+    const bool graph_ok = graphs_env && ctx.world == 1 && ctx.host_comm.all_reduce == nullptr && !i8 &&
+                          !ctx.concurrent && maxit - res.iterations >= 3;
+    struct GraphExec {
+      cudaGraphExec_t e = nullptr;
+      ~GraphExec() {
+        if (e) cudaGraphExecDestroy(e);
+      }
+    } gexec;
+    uint64_t glaunches = 0, gd2h = 0;
+    CommStats gstats;
+    if (graph_ok) {
+      if (lists && overlap_env) ensure_side();
+      const uint64_t l0 = ctx.launches, d0 = ctx.d2h_bytes;
+      const CommStats s0 = ctx.stats;
+      cudaGraph_t gr = nullptr;
+      SF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(st, &gr);
+        if (gr) cudaGraphDestroy(gr);
+        throw;
+      }
+      SF_CUDA(cudaStreamEndCapture(st, &gr));
+      const cudaError_t ie = cudaGraphInstantiate(&gexec.e, gr, 0);
+      cudaGraphDestroy(gr);
+      SF_CUDA(ie);
+      glaunches = ctx.launches - l0;
+      gd2h = ctx.d2h_bytes - d0;
+      gstats.scalar_allreduce = ctx.stats.scalar_allreduce - s0.scalar_allreduce;
+      gstats.vector_allreduce = ctx.stats.vector_allreduce - s0.vector_allreduce;
+      gstats.doubles_reduced = ctx.stats.doubles_reduced - s0.doubles_reduced;
+      ctx.launches = l0;
+      ctx.d2h_bytes = d0;
+      ctx.stats = s0;
+    }
+    while (res.iterations < maxit) {
+      if (graph_ok) {
+        SF_CUDA(cudaGraphLaunch(gexec.e, st));
+        ctx.launches += glaunches;
+        ctx.d2h_bytes += gd2h;
+        ctx.stats.scalar_allreduce += gstats.scalar_allreduce;
+        ctx.stats.vector_allreduce += gstats.vector_allreduce;
+        ctx.stats.doubles_reduced += gstats.doubles_reduced;
+      } else {
+        body();
+      }
       comm_sync(ctx);
       if (host[12] == 2.0)
         throw NumericalError("iterative solve diverged at iteration " + std::to_string(res.iterations) +
                              ": non-finite step norm");
       if (host[12] == 1.0) break;
-      const double gamma_next = host[5 - g];
+      const double gamma_next = host[gn];
       ++res.iterations;
       res.relative_residual = std::sqrt(gamma_next / reference);
       if (!std::isfinite(gamma_next) || res.relative_residual > blowup)
@@ -1852,7 +1922,6 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
         res.converged = true;
         break;
       }
-      g = 5 - g;
       di.lap("");
     }
     download_phi();

@@ -1922,6 +1922,11 @@ int sf_explain_nodes(sf_ctx* ctx, const sf_graph* g, const sf_model* m, const ui
       std::vector<char> filled(count, 0);
       auto run = [&](Ctx& c) {
         cudaSetDevice(c.device);
+        c.concurrent = true;
+        struct Reset {
+          Ctx& c;
+          ~Reset() { c.concurrent = false; }
+        } reset{c};
         for (;;) {
           const uint64_t i = next++;
           if (i >= count) return;

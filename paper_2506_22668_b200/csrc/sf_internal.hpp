@@ -262,6 +262,7 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   SideStream side;  // CGLS: the sparse-pair list passes beside the dense-pair passes
+  bool concurrent = false;  // one of several explain_nodes worker contexts right now
   int rank = 0, world = 1;
   std::unique_ptr<Nccl> nccl;
   HostComm host_comm;
