@@ -1180,11 +1180,15 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
     init_r_kernel<<<blocks_for(rows), 256, 0, st>>>(in.dev_sw, in.dev_targets, rows, r);
     SF_LAUNCHED(ctx);
   }
-  std::vector<uint32_t> h_pop(rows);
-  std::vector<uint8_t> h_comp(pairs);
+  // per-row set-bit counts and complement flags on the host (pinned: the
+  // copies run at full PCIe rate and overlap nothing else anyway)
+  ctx.cgls_hpop.reserve(std::max<uint64_t>(rows, 1));
+  ctx.cgls_hcomp.reserve(std::max<uint64_t>(pairs, 1));
+  uint32_t* const h_pop = ctx.cgls_hpop.p;
+  uint8_t* const h_comp = ctx.cgls_hcomp.p;
   if (rows) {
-    SF_CUDA(cudaMemcpyAsync(h_pop.data(), pop, rows * 4, cudaMemcpyDeviceToHost, st));
-    SF_CUDA(cudaMemcpyAsync(h_comp.data(), is_comp, pairs, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaMemcpyAsync(h_pop, pop, rows * 4, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaMemcpyAsync(h_comp, is_comp, pairs, cudaMemcpyDeviceToHost, st));
     SF_CUDA(cudaStreamSynchronize(st));
     ctx.d2h_bytes += rows * 4 + pairs;
   }

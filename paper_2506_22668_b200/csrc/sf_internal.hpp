@@ -302,6 +302,8 @@ struct Ctx {
   DevBuf<uint32_t> pop_dev;     // set bits per row (assemble_pairs)
   DevBuf<uint8_t> comp_dev;     // complement flag per pair
   PinnedBuf<double> solver_host;  // CGLS scalars fetched by the host loop
+  PinnedBuf<uint32_t> cgls_hpop;  // CGLS setup: set bits per row, complement flags
+  PinnedBuf<uint8_t> cgls_hcomp;
   DevBuf<float> feat_dev, w0_dev; // engine_prepare temporaries (X, W0 for P0 = X W0)
   DevBuf<float> graph_feat;       // device copy of a graph's features (explain path)
   uint64_t graph_feat_id = 0;     // Graph::id it holds
