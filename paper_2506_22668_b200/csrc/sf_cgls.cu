@@ -1864,8 +1864,8 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       const char* e = std::getenv("SF_CGLS_GRAPH");
       return e == nullptr || std::strcmp(e, "0") != 0;
     }();
-    const bool graph_ok = graphs_env && ctx.world == 1 && ctx.host_comm.all_reduce == nullptr && !i8 &&
-                          !ctx.concurrent && maxit - res.iterations >= 3;
+    bool graph_ok = graphs_env && ctx.world == 1 && ctx.host_comm.all_reduce == nullptr && !i8 &&
+                    !ctx.concurrent && maxit - res.iterations >= 3;
     struct GraphExec {
       cudaGraphExec_t e = nullptr;
       ~GraphExec() {
@@ -1878,19 +1878,29 @@ CglsResult cgls_solve(Ctx& ctx, const CglsInput& in, double tol,
       if (lists && overlap_env) ensure_side();
       const uint64_t l0 = ctx.launches, d0 = ctx.d2h_bytes;
       const CommStats s0 = ctx.stats;
+      // a capture or instantiation failure falls back to direct launches
+      // (nothing of the body has run: captured work is only recorded)
       cudaGraph_t gr = nullptr;
-      SF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      try {
-        body();
-      } catch (...) {
-        cudaStreamEndCapture(st, &gr);
+      bool captured = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (captured) {
+        try {
+          body();
+        } catch (...) {
+          captured = false;
+        }
+        if (cudaStreamEndCapture(st, &gr) != cudaSuccess) captured = false;
+        if (captured && gr && cudaGraphInstantiate(&gexec.e, gr, 0) != cudaSuccess) {
+          gexec.e = nullptr;
+          captured = false;
+        }
         if (gr) cudaGraphDestroy(gr);
-        throw;
       }
-      SF_CUDA(cudaStreamEndCapture(st, &gr));
-      const cudaError_t ie = cudaGraphInstantiate(&gexec.e, gr, 0);
-      cudaGraphDestroy(gr);
-      SF_CUDA(ie);
+      if (!captured || !gexec.e) {
+        cudaGetLastError();  // clear the capture error
+        if (gexec.e) cudaGraphExecDestroy(gexec.e);
+        gexec.e = nullptr;
+        graph_ok = false;
+      }
       glaunches = ctx.launches - l0;
       gd2h = ctx.d2h_bytes - d0;
       gstats.scalar_allreduce = ctx.stats.scalar_allreduce - s0.scalar_allreduce;
