@@ -947,7 +947,9 @@ void build_fused_plan(Ctx& ctx, Engine& e, const Subgraph& sg) {
   e.item_order.upload(order.data(), order.size(), ctx.stream);
   e.u_items.upload(u_items.data(), u_items.size(), ctx.stream);
   ctx.h2d_bytes += (ent.size() + item_ent.size() + order.size() + u_items.size()) * 4;
-  SF_CUDA(cudaStreamSynchronize(ctx.stream));
+  // (no sync: cudaMemcpyAsync from pageable memory returns once the source
+  // is staged, so the vectors may go; the host builds the next plan while
+  // the device copies)
 }
 }  // namespace
 
@@ -1021,7 +1023,8 @@ void engine_prepare(Ctx& ctx, const Subgraph& sg, const Model& m) {
   }
   ctx.h2d_bytes += (rp.size() + sg.col.size() + sg.edge_player.size()) * 4;
   for (const Layer& l : m.layers) ctx.h2d_bytes += (l.weight.size() + l.bias.size()) * 4;
-  SF_CUDA(cudaStreamSynchronize(ctx.stream));  // host sources of the uploads may go now
+  // (no sync: the pageable sources are staged before cudaMemcpyAsync
+  // returns; the host goes on with the plans while X W0 runs)
   dt.lap("p0 gemm + weights");
   e.fused = e.L >= 2 && fused_width(e.dims[1]) && e.n > 0;
   if (e.fused) build_fused_plan(ctx, e, sg);
